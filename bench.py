@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""Benchmark: stencil-chain effective GB/s on B200 (BASELINE.json metric).
+
+Workload (configs[1]): CloverLeaf-2D analogue miniflow2d at 15360 x 15360 fp64
+(18.9 GB of datasets), one step = one flushed chain of 10 iterations (140 par_loops
++ the fieldsum reduction, 141 loops, exactly the reference's steady-state chain).
+Inputs are far larger than L2 (126 MB), so no L2 flush is needed between steps.
+
+  value : in-core (datasets resident in HBM), effective GB/s = Σ metric bytes
+          (proj/src/metrics.cpp:10-12) / device time of the K steps (CUDA events
+          on the compute queue, after W warm-up steps).
+  e2e   : the same metric through the reference-facing API with HOST buffers:
+          the out-of-core streaming executor at a 3x budget (capacity = problem/3,
+          cyclic on, config 3) — every step uploads its inputs from pinned host
+          memory and downloads its results; host wall time around K steps.
+  roofline: the dominant kernel (the sm_100a par_loop kernel, all loops) against
+          the measured HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs).
+  cpu_baseline: the unmodified reference (oracle/_ref, OpenMP on all host cores),
+          reference executor, on a bounded sample of the same app.
+
+--impl reference runs only the reference CPU path (rank 0) and prints its line.
+Multi-GPU (torchrun, N>1): each rank runs the workload on its own GPU (replicas,
+weak scaling); times are the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "stencil-chain effective GB/s & out-of-core/in-core efficiency at 1–3× HBM"
+UNIT = "GB/s"
+ITERS_PER_STEP = 10
+
+
+# ------------------------------------------------------------------ helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during a timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu),
+                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        return rank, world, local, dist
+    return rank, world, local, None
+
+
+def max_over_ranks(x, dist, local):
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([float(x)], device=f"cuda:{local}", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ reference CPU arm
+def cpu_reference(steps, n_sample=1920, warmup=1):
+    """Reference executor of the unmodified reference (oracle/_ref/libooc_ref.so),
+    OpenMP on every host core; one step = one 10-iteration miniflow2d chain."""
+    from oracle import refo
+    from oracle import programs as P  # noqa: F401  (same app, run through run_app)
+    cores = os.cpu_count()
+    ref = refo.RefRuntime("reference", openmp=True)
+    iters = ITERS_PER_STEP * (warmup + steps)
+    t0 = time.perf_counter()
+    ref.run_app("miniflow2d", n_sample, n_sample, iters)
+    wall = time.perf_counter() - t0
+    tot = ref.totals()
+    # the reference reports Σ metric bytes / Σ loop wall time (runtime.cpp:79-88)
+    gbs = tot["metric_bytes"] / tot["loop_time_s"] / 1e9
+    ref.close()
+    return {"value": gbs, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"miniflow2d {n_sample}x{n_sample}, {iters} iterations "
+                      f"({tot['chains']} chains), reference executor, OpenMP {cores} threads; "
+                      f"wall {wall:.2f} s",
+            "metric_bytes": tot["metric_bytes"], "loop_time_s": tot["loop_time_s"]}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0):
+    rt = B.Runtime("resident", profile=profile, gpu=gpu, resident_budget=resident_budget)
+    t_decl = time.perf_counter()
+    rt.declare_app("miniflow2d", n, n)
+    t_decl = time.perf_counter() - t_decl
+    rt.app_iterations("miniflow2d", n, n, 0, 0, ITERS_PER_STEP * warmup)
+    rt.sync()
+    dev0 = rt.device()
+    rep0 = rt.report()
+    lm0 = {m[0] for m in rt.loop_metrics()}
+    with ClockSampler(gpu) as clk:
+        m0 = rt.mark()
+        rt.app_iterations("miniflow2d", n, n, 0, ITERS_PER_STEP * warmup,
+                          ITERS_PER_STEP * (warmup + steps))
+        m1 = rt.mark()
+        dt = rt.elapsed(m0, m1)
+    rep1 = rt.report()
+    dev1 = rt.device()
+    loops = [m for m in rt.loop_metrics() if m[0] not in lm0]
+    out = {"bytes": rep1["total_bytes"] - rep0["total_bytes"], "seconds": dt,
+           "launches": dev1["kernel_launches"] - dev0["kernel_launches"],
+           "clocks": clk.summary(), "declare_s": t_decl, "loops": loops,
+           "tiles": rep1["tiles"], "device": dev1}
+    red = rt.fetch_reduction("fieldsum")
+    out["fieldsum"] = red
+    rt.close()
+    return out
+
+
+def run_e2e(B, n, steps, warmup, gpu, ratio=3.0, cyclic=True):
+    pb = B.problem_bytes("miniflow2d", n, n)
+    cap = int(pb / ratio)
+    rt = B.Runtime("explicit", capacity=cap, gpu=gpu)
+    rt.declare_app("miniflow2d", n, n)
+    rt.app_iterations("miniflow2d", n, n, 0, 0, ITERS_PER_STEP * warmup, cyclic=False)
+    if cyclic:
+        rt.set_cyclic_flag(True)
+    rt.sync()
+    rep0 = rt.report()
+    dev0 = rt.device()
+    with ClockSampler(gpu) as clk:
+        m0 = rt.mark()
+        t0 = time.perf_counter()
+        rt.app_iterations("miniflow2d", n, n, 0, ITERS_PER_STEP * warmup,
+                          ITERS_PER_STEP * (warmup + steps), cyclic=cyclic)
+        m1 = rt.mark()
+        rt.sync()
+        wall = time.perf_counter() - t0
+        dt = rt.elapsed(m0, m1)
+    rep1 = rt.report()
+    dev1 = rt.device()
+    out = {"bytes": rep1["total_bytes"] - rep0["total_bytes"], "wall": wall, "device_s": dt,
+           "uploaded": rep1["uploaded"] - rep0["uploaded"],
+           "downloaded": rep1["downloaded"] - rep0["downloaded"],
+           "d2d": rep1["d2d"] - rep0["d2d"], "tiles": rep1["tiles"], "capacity": cap,
+           "problem_bytes": pb, "launches": dev1["kernel_launches"] - dev0["kernel_launches"],
+           "clocks": clk.summary(), "h2d_dev": dev1["h2d_bytes"] - dev0["h2d_bytes"],
+           "d2h_dev": dev1["d2h_bytes"] - dev0["d2h_bytes"]}
+    rt.close()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=15360)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", type=int, default=1)
+    args = ap.parse_args()
+    rank, world, local, dist = dist_init()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        ref = cpu_reference(args.steps, warmup=0)
+        line = {"metric": METRIC, "value": ref["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step":
+                    1e3 * ref["loop_time_s"] / max(args.steps, 1),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (reference closed-form fills)", "impl": "reference",
+                "config": {"workload": "miniflow2d (CloverLeaf-2D analogue) fp64, reference CPU "
+                                       "executor, bounded sample", "parallelism": "openmp"},
+                "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import paper_1709_02125_b200 as B
+    gpu = local if world > 1 else 0
+    n = args.n
+    barrier(dist)
+    inc = run_incore(B, n, args.steps, args.warmup, bool(args.profile), gpu)
+    dt = max_over_ranks(inc["seconds"], dist, local)
+    value = world * inc["bytes"] / dt / 1e9
+    e2e = None
+    if not args.no_e2e:
+        barrier(dist)
+        e2e = run_e2e(B, n, args.steps, args.warmup, gpu)
+        e2e_wall = max_over_ranks(e2e["wall"], dist, local)
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peaks()
+    # dominant kernel: the sm_100a par_loop kernel, over every non-reducing launch
+    loops = [m for m in inc["loops"] if m[3] > 0]
+    kb = sum(m[2] for m in loops)
+    kt = sum(m[3] for m in loops)
+    achieved = kb / kt / 1e9 if kt > 0 else None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference closed-form fills, proj/src/apps.cpp:61-67)",
+        "config": {"workload": f"miniflow2d {n}x{n} fp64 in-core (CloverLeaf-2D analogue, "
+                               "BASELINE configs[1], untiled)",
+                   "step": f"one chain = {ITERS_PER_STEP} iterations, 141 par_loops",
+                   "problem_bytes": B.problem_bytes("miniflow2d", n, n),
+                   "l2": "inputs (18.9 GB) >> L2 (126 MB); no flush needed",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "peak_source": peak_kind,
+                     "kernel": "k_interp (generic sm_100a par_loop kernel), all 140 loops/step"},
+        "gpu_launches": inc["launches"],
+        "clocks": inc["clocks"],
+        "incore": {"seconds": inc["seconds"], "metric_bytes": inc["bytes"],
+                   "fieldsum": inc["fieldsum"], "declare_s": inc["declare_s"]},
+    }
+    if e2e:
+        e2e_val = world * e2e["bytes"] / e2e_wall / 1e9
+        line["e2e"] = {"value": e2e_val, "unit": UNIT,
+                       "h2d_bytes_per_step": e2e["uploaded"] // args.steps,
+                       "d2h_bytes_per_step": e2e["downloaded"] // args.steps,
+                       "mode": "out-of-core streamed, capacity = problem/3 (artificial cap "
+                               f"{e2e['capacity']} B), cyclic, T={e2e['tiles']}",
+                       "device_s": e2e["device_s"], "wall_s": e2e["wall"],
+                       "ooc_over_incore": e2e_val / value, "launches": e2e["launches"],
+                       "clocks": e2e["clocks"]}
+    if not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_reference(1, n_sample=1920, warmup=0)
+            line["cpu_baseline"].pop("metric_bytes", None)
+            line["cpu_baseline"].pop("loop_time_s", None)
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,53 @@
+// Internal state of the device layer (never exposed through include/ooc_device.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+
+#include "ooc_device.h"
+
+namespace oocdev {
+
+void set_error(const std::string& msg);
+
+#define OOC_CUDA_TRY(expr)                                                                  \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      ::oocdev::set_error(std::string(#expr) + ": " + cudaGetErrorString(e_) + " (" +       \
+                          __FILE__ + ":" + std::to_string(__LINE__) + ")");                 \
+      return OOC_ERR_CUDA;                                                                  \
+    }                                                                                       \
+  } while (0)
+
+#define OOC_ARG_CHECK(cond, msg)      \
+  do {                                \
+    if (!(cond)) {                    \
+      ::oocdev::set_error(msg);       \
+      return OOC_ERR_ARG;             \
+    }                                 \
+  } while (0)
+
+}  // namespace oocdev
+
+struct ooc_event {
+  cudaEvent_t ev = nullptr;
+};
+
+struct ooc_ctx {
+  int device = 0;
+  cudaStream_t q[OOC_NUM_QUEUES] = {nullptr, nullptr, nullptr};
+  cudaDeviceProp prop{};
+  // device memory manager bookkeeping
+  std::unordered_map<void*, size_t> allocs;
+  long long in_use = 0, peak = 0;
+  // reduction accumulators + per-queue block-partials scratch
+  double* red_acc = nullptr;   // OOC_REDUCE_SLOTS
+  double* red_part[OOC_NUM_QUEUES] = {nullptr, nullptr, nullptr};
+  int red_part_cap = 0;
+  ooc_dev_stats stats{};
+};

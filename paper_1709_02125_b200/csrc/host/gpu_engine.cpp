@@ -1,0 +1,599 @@
+// The B200 streaming engine (paper Alg. 1) and the resident in-core executor.
+//
+// Streaming executor — restates the data movement of the reference's
+// run_chain_explicit (proj/src/explicit_exec.cpp:55-281) on real hardware:
+//   * three slots in HBM, slot(t) = (cursor + t) % 3 (explicit_exec.cpp:75, 273);
+//   * tile 0 uploads full[0], tile t+1 uploads right_fp[t+1] on the H2D queue while
+//     tile t computes (explicit_exec.cpp:174-186);
+//   * kernels of tile t on the compute queue, then the right edge is carried
+//     device-to-device into slot(t+1) (explicit_exec.cpp:206-231);
+//   * left_fp[t] of written datasets downloads on the D2H queue
+//     (explicit_exec.cpp:233-242): read-only data never travels back, write-first
+//     data never travels up (:86, :235), cyclic drops write-first data (:236-239).
+// Every cross-queue hazard is an explicit CUDA event wait, including the
+// compute-waits-for-its-upload dependency the reference's simulated timeline
+// omits (kernels of tile t wait for the H2D of tile t).
+#include "ooc/gpu_engine.hpp"
+
+#include <cmath>
+#include <cstring>
+
+namespace ooc {
+
+void device_check(int rc, const char* what) {
+  if (rc == OOC_OK) return;
+  std::string msg = std::string(what) + ": " + ooc_dev_last_error();
+  if (rc == OOC_ERR_CAPACITY) throw CapacityError(-1, -1);
+  throw DeviceError(rc, msg);
+}
+
+#define DEV(call) device_check((call), #call)
+
+// ---------------------------------------------------------------- lowering / layouts
+
+LoweredLoop lower_loop(const ParLoop& loop) {
+  LoweredLoop lw;
+  auto put = [&](const ExprTape& t) {
+    for (const auto& in : t.ins) {
+      ooc_ins o{};
+      o.op = static_cast<int32_t>(in.op);
+      o.arg = in.arg;
+      o.value = in.value;
+      for (int d = 0; d < 3; ++d) o.offset[d] = in.offset[d];
+      lw.tape.push_back(o);
+    }
+    return static_cast<int>(t.ins.size());
+  };
+  for (std::size_t w = 0; w < loop.kernel.writes.size(); ++w) {
+    lw.write_arg.push_back(loop.kernel.writes[w].arg);
+    lw.write_len.push_back(put(loop.write_tapes[w]));
+  }
+  if (loop.has_reduction()) {
+    lw.reduce_op = loop.kernel.reduce == ReduceOp::sum   ? OOC_RED_SUM
+                   : loop.kernel.reduce == ReduceOp::min ? OOC_RED_MIN
+                                                         : OOC_RED_MAX;
+    lw.reduce_len = put(loop.reduce_tape);
+  }
+  return lw;
+}
+
+BoxLayout padded_layout(const Extent& box, index_t pad) {
+  BoxLayout L;
+  L.box = box;
+  const int nd = box.ndim;
+  const index_t n0 = box.len(0), n1 = box.len(1), n2 = box.len(2);
+  auto up = [&](index_t v) { return (v + pad - 1) / pad * pad; };
+  if (nd == 1) {
+    L.stride = {1, 1, 1};
+    L.elems = n0;
+  } else if (nd == 2) {
+    L.stride = {up(n1), 1, 1};
+    L.elems = L.stride[0] * n0;
+  } else {
+    L.stride = {up(n2) * n1, up(n2), 1};
+    L.elems = L.stride[0] * n0;
+  }
+  return L;
+}
+
+ooc_view view_at(double* data, const Extent& box, const Point& stride) {
+  ooc_view v{};
+  v.data = data;
+  for (int d = 0; d < 3; ++d) {
+    v.lo[d] = box.lo[d];
+    v.hi[d] = box.hi[d];
+    v.stride[d] = stride[d];
+  }
+  return v;
+}
+
+ooc_view host_view(Dataset& ds) {
+  const Extent a = ds.alloc();
+  return view_at(ds.host.data(), a, a.strides());
+}
+
+// ---------------------------------------------------------------- engine
+
+GpuEngine::GpuEngine(const RuntimeOptions& opts) : opts_(opts) {
+  DEV(ooc_ctx_create(opts.gpu, &ctx_));
+  DEV(ooc_ctx_props(ctx_, &props_));
+  void* p = nullptr;
+  DEV(ooc_host_alloc(sizeof(double) * OOC_REDUCE_SLOTS, &p));
+  red_host_ = static_cast<double*>(p);
+  std::memset(red_host_, 0, sizeof(double) * OOC_REDUCE_SLOTS);
+}
+
+GpuEngine::~GpuEngine() {
+  if (!ctx_) return;
+  ooc_ctx_sync(ctx_);
+  auto drop = [&](std::vector<ooc_event*>& v) {
+    for (auto* e : v) ooc_event_destroy(ctx_, e);
+    v.clear();
+  };
+  drop(ev_h2d_);
+  drop(ev_k_);
+  drop(ev_q0_);
+  drop(ev_d2h_);
+  drop(free_timing_);
+  for (auto& pc : pending_chains_) {
+    ooc_event_destroy(ctx_, pc.start);
+    ooc_event_destroy(ctx_, pc.end);
+  }
+  for (auto& pl : pending_loops_) {
+    ooc_event_destroy(ctx_, pl.a);
+    ooc_event_destroy(ctx_, pl.b);
+  }
+  for (auto& [slot, e] : red_ready_) ooc_event_destroy(ctx_, e);
+  for (auto* e : marks_) ooc_event_destroy(ctx_, e);
+  if (red_host_) ooc_host_free(red_host_);
+  ooc_ctx_destroy(ctx_);  // frees pool and resident buffers tracked by the manager
+}
+
+ooc_event* GpuEngine::ev(std::vector<ooc_event*>& pool, std::size_t i, bool timing) {
+  while (pool.size() <= i) {
+    ooc_event* e = nullptr;
+    DEV(ooc_event_create(ctx_, timing ? 1 : 0, &e));
+    pool.push_back(e);
+  }
+  return pool[i];
+}
+
+ooc_event* GpuEngine::fresh_timing_event() {
+  if (!free_timing_.empty()) {
+    ooc_event* e = free_timing_.back();
+    free_timing_.pop_back();
+    return e;
+  }
+  ooc_event* e = nullptr;
+  DEV(ooc_event_create(ctx_, 1, &e));
+  return e;
+}
+
+void GpuEngine::recycle(ooc_event* e) {
+  if (e) free_timing_.push_back(e);
+}
+
+int GpuEngine::alloc_red_slot() {
+  int s = next_red_slot_;
+  next_red_slot_ = (next_red_slot_ + 1) % OOC_REDUCE_SLOTS;
+  auto it = red_ready_.find(s);
+  if (it != red_ready_.end()) {  // slot reuse: its previous value must have landed
+    DEV(ooc_event_sync(ctx_, it->second));
+  }
+  return s;
+}
+
+void GpuEngine::launch(int queue, const ParLoop& loop, const LoweredLoop& lw, const Extent& sub,
+                       const std::vector<ooc_view>& views, int red_slot) {
+  ooc_loop L{};
+  L.ndim = sub.ndim;
+  for (int d = 0; d < 3; ++d) {
+    L.lo[d] = sub.lo[d];
+    L.hi[d] = sub.hi[d];
+  }
+  L.nargs = static_cast<int32_t>(views.size());
+  for (std::size_t a = 0; a < views.size(); ++a) L.args[a] = views[a];
+  L.nwrites = static_cast<int32_t>(lw.write_arg.size());
+  for (std::size_t w = 0; w < lw.write_arg.size(); ++w) {
+    L.write_arg[w] = lw.write_arg[w];
+    L.write_len[w] = lw.write_len[w];
+  }
+  L.reduce_op = lw.reduce_op;
+  L.reduce_len = lw.reduce_len;
+  L.reduce_slot = red_slot;
+  L.ntape = static_cast<int32_t>(lw.tape.size());
+  L.tape = lw.tape.data();
+  if (opts_.profile_loops) {
+    PendingLoop pl{loop.id, fresh_timing_event(), fresh_timing_event()};
+    DEV(ooc_event_record(ctx_, pl.a, queue));
+    DEV(ooc_launch_loop(ctx_, queue, &L));
+    DEV(ooc_event_record(ctx_, pl.b, queue));
+    pending_loops_.push_back(pl);
+  } else {
+    DEV(ooc_launch_loop(ctx_, queue, &L));
+  }
+}
+
+void GpuEngine::ensure_pool(index_t elems) {
+  if (elems <= pool_elems_) return;
+  if (pool_) {
+    DEV(ooc_ctx_sync(ctx_));  // earlier chains may still read the old pool
+    DEV(ooc_mem_free(ctx_, pool_));
+    pool_ = nullptr;
+  }
+  void* p = nullptr;
+  DEV(ooc_mem_alloc(ctx_, static_cast<std::size_t>(elems) * sizeof(double), &p));
+  pool_ = static_cast<double*>(p);
+  pool_elems_ = elems;
+}
+
+void GpuEngine::finish_chain(const LoopChain& chain, const std::map<int, int>& red,
+                             PendingChain pc) {
+  // reductions: one 8-byte D2H per reducing loop, on the compute queue after its kernels
+  if (!red.empty()) {
+    for (const auto& [loop_id, slot] : red) {
+      DEV(ooc_reduce_fetch(ctx_, OOC_Q_COMPUTE, slot, red_host_ + slot));
+      ooc_event*& e = red_ready_[slot];
+      if (!e) DEV(ooc_event_create(ctx_, 0, &e));
+      DEV(ooc_event_record(ctx_, e, OOC_Q_COMPUTE));
+    }
+  }
+  DEV(ooc_event_record(ctx_, pc.end, OOC_Q_COMPUTE));
+  pc.t.chain_id = chain.chain_id;
+  pc.t.loops = static_cast<int>(chain.loops.size());
+  pending_chains_.push_back(pc);
+}
+
+// ---------------------------------------------------------------- streaming executor
+
+void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan& plan,
+                             const Footprints& fp, bool cyclic, ChainOut& out) {
+  const int T = plan.tile_count;
+  if (3 * fp.slot_bytes > opts_.device.capacity_bytes)  // explicit_exec.cpp:61-62
+    throw CapacityError(3 * fp.slot_bytes, opts_.device.capacity_bytes);
+
+  std::vector<DatasetId> used;
+  for (std::size_t d = 0; d < fp.per_dataset.size(); ++d)
+    if (fp.per_dataset[d].accessed) used.push_back(static_cast<DatasetId>(d));
+
+  // Slot layout: every dataset gets a region able to hold its largest tile box
+  // (per-dim max over tiles of full[t]); rows padded to 128 B.
+  std::vector<BoxLayout> lay(mesh.datasets.size());
+  std::vector<index_t> off(mesh.datasets.size(), 0);
+  index_t slot_elems = 0;
+  for (DatasetId d : used) {
+    const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+    Extent big = Extent::none(mesh[d].core.ndim);
+    for (const Extent& f : pd.full)
+      if (!f.empty()) {
+        if (big.empty()) {
+          big = f;
+        } else {
+          for (int k = 0; k < 3; ++k) {
+            index_t len = std::max(big.len(k), f.len(k));
+            big.lo[k] = 0;
+            big.hi[k] = len;
+          }
+        }
+      }
+    if (big.empty()) continue;
+    lay[static_cast<std::size_t>(d)] = padded_layout(big);
+    off[static_cast<std::size_t>(d)] = slot_elems;
+    slot_elems += (lay[static_cast<std::size_t>(d)].elems + 31) / 32 * 32;  // 256-B aligned
+  }
+  ensure_pool(3 * std::max<index_t>(slot_elems, 32));
+
+  auto slot_of = [&](int t) { return (slot_cursor_ + t) % 3; };
+  auto arena = [&](DatasetId d, int t) {
+    const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+    return view_at(pool_ + static_cast<index_t>(slot_of(t)) * slot_elems + off[static_cast<std::size_t>(d)],
+                   pd.full[t], lay[static_cast<std::size_t>(d)].stride);
+  };
+  std::map<std::pair<DatasetId, int>, AuditRow> audit;
+  auto row = [&](DatasetId d, int t) -> AuditRow& {
+    AuditRow& r = audit[{d, t}];
+    r.dataset = d;
+    r.tile = t;
+    return r;
+  };
+  auto copy = [&](int q, int kind, const ooc_view& s, const ooc_view& dv, const Extent& region) {
+    int64_t lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = region.lo[k];
+      hi[k] = region.hi[k];
+    }
+    DEV(ooc_copy_box(ctx_, q, kind, &s, &dv, lo, hi));
+  };
+  auto fill_tile = [&](int t, int q) {
+    if (!opts_.arena_fill) return;
+    const double v = opts_.arena_fill == 2 ? std::nan("") : 0.0;
+    for (DatasetId d : used) {
+      const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+      if (pd.full[t].empty()) continue;
+      ooc_view a = arena(d, t);
+      DEV(ooc_fill_box(ctx_, q, &a, v));
+    }
+  };
+
+  PendingChain pc;
+  pc.start = fresh_timing_event();
+  pc.end = fresh_timing_event();
+  pc.t.tiles = T;
+  // Chain start on the compute queue; the H2D / D2H queues follow it, so nothing of
+  // this chain overtakes the previous chain's downloads (host RAW) or slot use.
+  DEV(ooc_event_record(ctx_, pc.start, OOC_Q_COMPUTE));
+  DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, pc.start));
+  DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, pc.start));
+
+  // reduction accumulators (explicit_exec.cpp:159-162)
+  for (const ParLoop& l : chain.loops)
+    if (l.has_reduction()) {
+      int s = alloc_red_slot();
+      out.reduction_slot[l.id] = s;
+      DEV(ooc_reduce_reset(ctx_, OOC_Q_COMPUTE, s, lower_loop(l).reduce_op));
+    }
+
+  std::vector<Extent> down_hull(mesh.datasets.size()), skip_hull(mesh.datasets.size());
+  for (DatasetId d : used) {
+    down_hull[static_cast<std::size_t>(d)] = Extent::none(mesh[d].alloc().ndim);
+    skip_hull[static_cast<std::size_t>(d)] = Extent::none(mesh[d].alloc().ndim);
+  }
+  std::vector<const LoweredLoop*> lowered(chain.loops.size());
+  for (std::size_t j = 0; j < chain.loops.size(); ++j) {
+    auto it = lowered_.find(chain.loops[j].id);
+    if (it == lowered_.end()) it = lowered_.emplace(chain.loops[j].id, lower_loop(chain.loops[j])).first;
+    lowered[j] = &it->second;
+  }
+  std::vector<ooc_view> hviews(mesh.datasets.size());
+  for (DatasetId d : used) hviews[static_cast<std::size_t>(d)] = host_view(mesh[d]);
+
+  for (int t = 0; t < T; ++t) {
+    if (t == 0) {
+      fill_tile(0, OOC_Q_H2D);
+      for (DatasetId d : used) {
+        const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+        if (pd.write_first || pd.full[0].empty()) continue;
+        copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), pd.full[0]);
+        row(d, 0).uploaded += pd.full[0].size() * mesh[d].elem_bytes;
+      }
+      DEV(ooc_event_record(ctx_, ev(ev_h2d_, 0), OOC_Q_H2D));
+    }
+    if (t + 1 < T) {
+      if (t >= 2) {  // slot(t+1) == slot(t-2): its readers must be done
+        DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, ev(ev_q0_, t - 2)));
+        DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, ev(ev_d2h_, t - 2)));
+      }
+      fill_tile(t + 1, OOC_Q_H2D);
+      for (DatasetId d : used) {
+        const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+        if (pd.write_first || pd.right_fp[t + 1].empty()) continue;
+        copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, t + 1),
+             pd.right_fp[t + 1]);
+        row(d, t + 1).uploaded += pd.right_fp[t + 1].size() * mesh[d].elem_bytes;
+      }
+      DEV(ooc_event_record(ctx_, ev(ev_h2d_, t + 1), OOC_Q_H2D));
+    }
+
+    // kernels of tile t wait for tile t's upload (missing from the reference model)
+    DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, ev(ev_h2d_, t)));
+    for (std::size_t j = 0; j < chain.loops.size(); ++j) {
+      const ParLoop& loop = chain.loops[j];
+      const Extent sub = plan.subrange(static_cast<int>(j), t);
+      if (sub.empty()) continue;
+      std::vector<ooc_view> views;
+      views.reserve(loop.args.size());
+      for (const LoopArg& a : loop.args) {
+        views.push_back(arena(a.dataset, t));
+        if (access_writes(a.mode)) mesh[a.dataset].ever_written = true;
+      }
+      auto rs = out.reduction_slot.find(loop.id);
+      launch(OOC_Q_COMPUTE, loop, *lowered[j], sub, views,
+             rs == out.reduction_slot.end() ? 0 : rs->second);
+    }
+    DEV(ooc_event_record(ctx_, ev(ev_k_, t), OOC_Q_COMPUTE));
+
+    if (t + 1 < T) {
+      if (t >= 2) DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, ev(ev_d2h_, t - 2)));
+      for (DatasetId d : used) {
+        const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+        if (pd.right_edge[t].empty()) continue;
+        copy(OOC_Q_COMPUTE, OOC_COPY_D2D, arena(d, t), arena(d, t + 1), pd.right_edge[t]);
+        row(d, t + 1).d2d += pd.right_edge[t].size() * mesh[d].elem_bytes;
+      }
+    }
+    DEV(ooc_event_record(ctx_, ev(ev_q0_, t), OOC_Q_COMPUTE));
+
+    DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, ev(ev_k_, t)));
+    for (DatasetId d : used) {
+      const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+      if (!pd.written_any) continue;  // read-only data never travels back
+      if (cyclic && pd.write_first) {  // cyclic: temporaries are dropped
+        skip_hull[static_cast<std::size_t>(d)] = skip_hull[static_cast<std::size_t>(d)].hull(pd.left_fp[t]);
+        continue;
+      }
+      if (!pd.left_fp[t].empty()) {
+        copy(OOC_Q_D2H, OOC_COPY_D2H, arena(d, t), hviews[static_cast<std::size_t>(d)], pd.left_fp[t]);
+        row(d, t).downloaded += pd.left_fp[t].size() * mesh[d].elem_bytes;
+      }
+      down_hull[static_cast<std::size_t>(d)] = down_hull[static_cast<std::size_t>(d)].hull(pd.left_fp[t]);
+    }
+    DEV(ooc_event_record(ctx_, ev(ev_d2h_, t), OOC_Q_D2H));
+  }
+  DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, ev(ev_d2h_, T - 1)));
+
+  // host staleness bookkeeping (explicit_exec.cpp:245-258)
+  for (DatasetId d : used) {
+    Dataset& ds = mesh[d];
+    const Extent& sk = skip_hull[static_cast<std::size_t>(d)];
+    const Extent& dn = down_hull[static_cast<std::size_t>(d)];
+    if (!sk.empty()) {
+      ds.stale_region = ds.host_stale ? ds.stale_region.hull(sk) : sk;
+      ds.host_stale = true;
+      ds.stale_chain = chain.chain_id;
+    } else if (ds.host_stale && !dn.empty() && dn.contains(ds.stale_region)) {
+      ds.host_stale = false;
+      ds.stale_chain = -1;
+      ds.stale_region = Extent::none(ds.alloc().ndim);
+    }
+  }
+  slot_cursor_ = (slot_cursor_ + T) % 3;
+
+  for (auto& [k, r] : audit) {
+    out.audit.push_back(r);
+    pc.t.uploaded += r.uploaded;
+    pc.t.downloaded += r.downloaded;
+    pc.t.d2d += r.d2d;
+  }
+  for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
+  finish_chain(chain, out.reduction_slot, pc);
+}
+
+// ---------------------------------------------------------------- resident executor
+
+void GpuEngine::ensure_resident(Mesh& mesh, DatasetId d) {
+  if (res_.size() < mesh.datasets.size()) res_.resize(mesh.datasets.size());
+  Resident& r = res_[static_cast<std::size_t>(d)];
+  Dataset& ds = mesh[d];
+  if (r.dev && r.host_ptr != ds.host.data()) {  // mesh replaced underneath us
+    DEV(ooc_ctx_sync(ctx_));
+    DEV(ooc_mem_free(ctx_, r.dev));
+    r = Resident{};
+  }
+  if (!r.dev) {
+    r.layout = padded_layout(ds.alloc());
+    void* p = nullptr;
+    int rc = ooc_mem_alloc(ctx_, static_cast<std::size_t>(r.layout.elems) * sizeof(double), &p);
+    if (rc == OOC_ERR_CAPACITY) {
+      long long in_use = 0;
+      ooc_mem_usage(ctx_, &in_use, nullptr);
+      throw CapacityError(in_use + r.layout.elems * 8, props_.hbm_bytes);
+    }
+    DEV(rc);
+    r.dev = static_cast<double*>(p);
+    r.host_ptr = ds.host.data();
+  }
+  if (!r.dev_valid) {
+    ooc_view hv = host_view(ds);
+    ooc_view dv = view_at(r.dev, ds.alloc(), r.layout.stride);
+    DEV(ooc_copy_box(ctx_, OOC_Q_COMPUTE, OOC_COPY_H2D, &hv, &dv, hv.lo, hv.hi));
+    r.dev_valid = true;
+    r.host_outdated = false;
+  }
+}
+
+bool GpuEngine::host_outdated(DatasetId d) const {
+  return static_cast<std::size_t>(d) < res_.size() && res_[static_cast<std::size_t>(d)].host_outdated;
+}
+
+void GpuEngine::download_resident(Mesh& mesh, DatasetId d) {
+  if (!host_outdated(d)) return;
+  Resident& r = res_[static_cast<std::size_t>(d)];
+  Dataset& ds = mesh[d];
+  ooc_view hv = host_view(ds);
+  ooc_view dv = view_at(r.dev, ds.alloc(), r.layout.stride);
+  DEV(ooc_copy_box(ctx_, OOC_Q_COMPUTE, OOC_COPY_D2H, &dv, &hv, hv.lo, hv.hi));
+  DEV(ooc_queue_sync(ctx_, OOC_Q_COMPUTE));
+  r.host_outdated = false;
+}
+
+void GpuEngine::forget_resident(DatasetId d) {
+  if (static_cast<std::size_t>(d) < res_.size()) res_[static_cast<std::size_t>(d)].dev_valid = false;
+}
+
+void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan* plan,
+                             const Footprints* fp, ChainOut& out) {
+  (void)fp;
+  PendingChain pc;
+  pc.start = fresh_timing_event();
+  pc.end = fresh_timing_event();
+  pc.t.tiles = plan ? plan->tile_count : 1;
+  std::vector<char> used(mesh.datasets.size(), 0);
+  for (const ParLoop& l : chain.loops)
+    for (const LoopArg& a : l.args) used[static_cast<std::size_t>(a.dataset)] = 1;
+  // first touch of a dataset uploads it (in order on the compute queue, before the
+  // chain's start event, so uploads are not part of the chain's device time)
+  index_t up = 0;
+  for (std::size_t d = 0; d < used.size(); ++d)
+    if (used[d]) {
+      bool had = d < res_.size() && res_[d].dev_valid;
+      ensure_resident(mesh, static_cast<DatasetId>(d));
+      if (!had) up += mesh[static_cast<DatasetId>(d)].alloc().size() * mesh[static_cast<DatasetId>(d)].elem_bytes;
+    }
+  pc.t.uploaded = up;
+  DEV(ooc_event_record(ctx_, pc.start, OOC_Q_COMPUTE));
+  for (const ParLoop& l : chain.loops)
+    if (l.has_reduction()) {
+      int s = alloc_red_slot();
+      out.reduction_slot[l.id] = s;
+      DEV(ooc_reduce_reset(ctx_, OOC_Q_COMPUTE, s, lower_loop(l).reduce_op));
+    }
+  std::vector<const LoweredLoop*> lowered(chain.loops.size());
+  std::vector<std::vector<ooc_view>> views(chain.loops.size());
+  for (std::size_t j = 0; j < chain.loops.size(); ++j) {
+    const ParLoop& l = chain.loops[j];
+    auto it = lowered_.find(l.id);
+    if (it == lowered_.end()) it = lowered_.emplace(l.id, lower_loop(l)).first;
+    lowered[j] = &it->second;
+    for (const LoopArg& a : l.args) {
+      const Resident& r = res_[static_cast<std::size_t>(a.dataset)];
+      views[j].push_back(view_at(r.dev, mesh[a.dataset].alloc(), r.layout.stride));
+      if (access_writes(a.mode)) {
+        mesh[a.dataset].ever_written = true;
+        res_[static_cast<std::size_t>(a.dataset)].host_outdated = true;
+      }
+    }
+  }
+  const int T = plan ? plan->tile_count : 1;
+  for (int t = 0; t < T; ++t)
+    for (std::size_t j = 0; j < chain.loops.size(); ++j) {
+      const ParLoop& l = chain.loops[j];
+      const Extent sub = plan ? plan->subrange(static_cast<int>(j), t) : l.range;
+      if (sub.empty()) continue;
+      auto rs = out.reduction_slot.find(l.id);
+      launch(OOC_Q_COMPUTE, l, *lowered[j], sub, views[j],
+             rs == out.reduction_slot.end() ? 0 : rs->second);
+    }
+  for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
+  finish_chain(chain, out.reduction_slot, pc);
+}
+
+double GpuEngine::reduction_value(int slot) {
+  auto it = red_ready_.find(slot);
+  if (it != red_ready_.end()) DEV(ooc_event_sync(ctx_, it->second));
+  return red_host_[slot];
+}
+
+void GpuEngine::sync() { DEV(ooc_ctx_sync(ctx_)); }
+
+int GpuEngine::mark() {
+  ooc_event* tail = nullptr;
+  DEV(ooc_event_create(ctx_, 0, &tail));
+  DEV(ooc_event_record(ctx_, tail, OOC_Q_D2H));
+  DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, tail));
+  DEV(ooc_event_destroy(ctx_, tail));
+  ooc_event* e = nullptr;
+  DEV(ooc_event_create(ctx_, 1, &e));
+  DEV(ooc_event_record(ctx_, e, OOC_Q_COMPUTE));
+  marks_.push_back(e);
+  return static_cast<int>(marks_.size()) - 1;
+}
+
+double GpuEngine::mark_elapsed(int a, int b) {
+  if (a < 0 || b < 0 || a >= static_cast<int>(marks_.size()) || b >= static_cast<int>(marks_.size()))
+    throw ValidationError("unknown timing mark");
+  DEV(ooc_event_sync(ctx_, marks_[static_cast<std::size_t>(b)]));
+  float ms = 0.f;
+  DEV(ooc_event_elapsed_ms(marks_[static_cast<std::size_t>(a)], marks_[static_cast<std::size_t>(b)], &ms));
+  return ms * 1e-3;
+}
+
+std::vector<ChainTiming> GpuEngine::take_timings() {
+  std::vector<ChainTiming> out;
+  for (auto& pc : pending_chains_) {
+    DEV(ooc_event_sync(ctx_, pc.end));
+    float ms = 0.f;
+    DEV(ooc_event_elapsed_ms(pc.start, pc.end, &ms));
+    pc.t.seconds = ms * 1e-3;
+    out.push_back(pc.t);
+    recycle(pc.start);
+    recycle(pc.end);
+  }
+  pending_chains_.clear();
+  return out;
+}
+
+std::map<int, double> GpuEngine::take_loop_times() {
+  std::map<int, double> out;
+  for (auto& pl : pending_loops_) {
+    DEV(ooc_event_sync(ctx_, pl.b));
+    float ms = 0.f;
+    DEV(ooc_event_elapsed_ms(pl.a, pl.b, &ms));
+    out[pl.loop_id] += ms * 1e-3;
+    recycle(pl.a);
+    recycle(pl.b);
+  }
+  pending_loops_.clear();
+  return out;
+}
+
+}  // namespace ooc

@@ -1,0 +1,189 @@
+// Lazy loop-chain runtime (flush semantics of proj/src/runtime.cpp:5-148) over the
+// B200 engine.
+#include "ooc/runtime.hpp"
+
+#include "ooc/gpu_engine.hpp"
+
+namespace ooc {
+
+Runtime::Runtime(RuntimeOptions opts) : opts_(opts) {
+  if (opts_.executor == ExecutorKind::tiled_cache || opts_.executor == ExecutorKind::unified)
+    throw ValidationError(std::string("executor '") + executor_name(opts_.executor) +
+                          "' (a KNL cache / unified-memory cost model of the reference) is not "
+                          "part of the B200 build; use tiled_explicit or resident");
+}
+
+Runtime::~Runtime() = default;
+
+GpuEngine& Runtime::engine() {
+  if (!gpu_) gpu_ = std::make_unique<GpuEngine>(opts_);
+  return *gpu_;
+}
+
+void Runtime::enqueue_loop(ParLoop loop) {  // runtime.cpp:5-11
+  validate_loop(mesh_, loop);
+  loop.id = next_loop_id_++;
+  const bool reduces = loop.has_reduction();
+  pending_.push_back(std::move(loop));
+  if (reduces) flush(FlushReason::reduction_fetch);
+}
+
+std::vector<double> Runtime::fetch_dataset(DatasetId d) {  // runtime.cpp:13-19
+  if (d < 0 || d >= static_cast<DatasetId>(mesh_.datasets.size()))
+    throw ValidationError("fetch of an unknown dataset");
+  std::vector<double> out(mesh_[d].host.size());
+  fetch_dataset_into(d, out.data(), out.size());
+  return out;
+}
+
+void Runtime::fetch_dataset_into(DatasetId d, double* dst, std::size_t n) {
+  flush(FlushReason::data_fetch);
+  if (d < 0 || d >= static_cast<DatasetId>(mesh_.datasets.size()))
+    throw ValidationError("fetch of an unknown dataset");
+  if (opts_.executor == ExecutorKind::plan_only && next_chain_id_ > 0)
+    throw ValidationError("plan_only runtime executes nothing; no results to fetch");
+  Dataset& ds = mesh_[d];
+  if (ds.host_stale) throw StaleDataError(ds.name, ds.stale_chain);
+  if (n != ds.host.size()) throw ValidationError("fetch buffer has the wrong length");
+  if (gpu_) {
+    if (gpu_->host_outdated(d))
+      gpu_->download_resident(mesh_, d);
+    else
+      gpu_->sync();  // streamed downloads of earlier chains must have landed
+  }
+  std::copy(ds.host.begin(), ds.host.end(), dst);
+}
+
+double Runtime::fetch_reduction(const std::string& name) {  // runtime.cpp:21-26
+  flush(FlushReason::data_fetch);
+  if (opts_.executor == ExecutorKind::plan_only)
+    throw ValidationError("plan_only runtime executes nothing; no results to fetch");
+  auto it = red_slot_.find(name);
+  if (it == red_slot_.end()) throw ValidationError("unknown reduction '" + name + "'");
+  return engine().reduction_value(it->second);
+}
+
+void Runtime::flush(FlushReason reason) {  // runtime.cpp:28-39
+  if (pending_.empty()) return;
+  LoopChain chain;
+  chain.chain_id = next_chain_id_++;
+  chain.reason = reason;
+  chain.loops = std::move(pending_);
+  pending_.clear();
+  flush_log_.push_back({chain.chain_id, reason, static_cast<int>(chain.loops.size())});
+  last_chain_ = chain;
+  if (opts_.record_chains) chain_log_.push_back(chain);
+  execute(std::move(chain));
+}
+
+void Runtime::finish() {
+  flush(FlushReason::program_end);
+  sync_host();
+}
+
+void Runtime::sync() {
+  if (gpu_) gpu_->sync();
+}
+
+void Runtime::sync_host() {
+  if (!gpu_) return;
+  for (std::size_t d = 0; d < mesh_.datasets.size(); ++d)
+    if (gpu_->host_outdated(static_cast<DatasetId>(d)))
+      gpu_->download_resident(mesh_, static_cast<DatasetId>(d));
+  gpu_->sync();
+}
+
+const PlanCache::Entry& Runtime::plan_for(const LoopChain& chain) {  // runtime.cpp:41-62
+  if (opts_.tiles > 0) return plans_.get(mesh_, chain, opts_.tiles, opts_.tiled_dim);
+  index_t budget = opts_.device.capacity_bytes;
+  if (opts_.executor == ExecutorKind::resident) budget = opts_.resident_budget;
+  TileChoice c = choose_tile_count(mesh_, chain, budget, opts_.tiled_dim);
+  return plans_.get(mesh_, chain, c.tile_count, opts_.tiled_dim);
+}
+
+void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
+  for (const ParLoop& l : chain.loops) {
+    auto it = metric_index_.find(l.id);
+    if (it != metric_index_.end()) continue;
+    LoopMetric m;
+    m.loop_id = l.id;
+    m.points = l.range.size();
+    m.bytes = l.range.size() * loop_bytes_per_point(mesh_, l);
+    metric_index_[l.id] = loop_metrics_.size();
+    loop_metrics_.push_back(m);
+  }
+  if (opts_.executor == ExecutorKind::plan_only) {
+    const PlanCache::Entry& e = plan_for(chain);
+    last_tiles_ = e.plan.tile_count;
+    return;
+  }
+  GpuEngine& g = engine();
+  GpuEngine::ChainOut out;
+  if (opts_.executor == ExecutorKind::tiled_explicit) {
+    const PlanCache::Entry& e = plan_for(chain);
+    last_tiles_ = e.plan.tile_count;
+    // a chain that would upload cyclically discarded data would ship garbage
+    for (std::size_t d = 0; d < e.footprints.per_dataset.size(); ++d) {
+      const auto& pd = e.footprints.per_dataset[d];
+      const Dataset& ds = mesh_[static_cast<DatasetId>(d)];
+      if (pd.accessed && ds.host_stale && !pd.write_first)
+        throw StaleDataError(ds.name, ds.stale_chain);
+    }
+    g.run_explicit(mesh_, chain, e.plan, e.footprints, cyclic_, out);
+  } else {
+    const bool tiled = opts_.executor == ExecutorKind::resident &&
+                       (opts_.tiles > 1 || (opts_.tiles == 0 && opts_.resident_budget > 0));
+    if (tiled) {
+      const PlanCache::Entry& e = plan_for(chain);
+      last_tiles_ = e.plan.tile_count;
+      g.run_resident(mesh_, chain, &e.plan, &e.footprints, out);
+    } else {
+      last_tiles_ = 1;
+      g.run_resident(mesh_, chain, nullptr, nullptr, out);
+    }
+  }
+  for (const ParLoop& l : chain.loops)
+    if (l.has_reduction()) red_slot_[l.kernel.reduce_name] = out.reduction_slot.at(l.id);
+  for (const AuditRow& r : out.audit) {
+    audit_.push_back(r);
+    uploaded_ += r.uploaded;
+    downloaded_ += r.downloaded;
+    d2d_ += r.d2d;
+  }
+}
+
+const std::vector<ChainTiming>& Runtime::chain_timings() {
+  if (gpu_)
+    for (ChainTiming& t : gpu_->take_timings()) timings_.push_back(t);
+  return timings_;
+}
+
+const std::vector<LoopMetric>& Runtime::loop_metrics() {
+  if (gpu_) {
+    for (const auto& [id, s] : gpu_->take_loop_times()) {
+      auto it = metric_index_.find(id);
+      if (it == metric_index_.end()) continue;
+      LoopMetric& m = loop_metrics_[it->second];
+      m.time_s += s;
+      m.bandwidth = m.time_s > 0 ? static_cast<double>(m.bytes) / m.time_s : 0.0;
+    }
+  }
+  return loop_metrics_;
+}
+
+RunReport Runtime::report() {
+  RunReport r;
+  r.mode = executor_name(opts_.executor);
+  r.tiles = opts_.tiles > 0 ? opts_.tiles : last_tiles_;
+  for (const LoopMetric& m : loop_metrics()) r.total_bytes += m.bytes;
+  for (const ChainTiming& t : chain_timings()) r.total_time += t.seconds;
+  r.makespan = r.total_time;
+  if (r.total_time > 0) r.average_bandwidth = static_cast<double>(r.total_bytes) / r.total_time;
+  r.uploaded = uploaded_;
+  r.downloaded = downloaded_;
+  r.d2d = d2d_;
+  r.capacity = opts_.device.capacity_bytes;
+  return r;
+}
+
+}  // namespace ooc

@@ -1,0 +1,118 @@
+// B200 execution engine behind ooc::Runtime: the out-of-core streaming executor
+// (paper Algorithm 1; reference run_chain_explicit, proj/src/explicit_exec.cpp:55-281)
+// and the in-core resident executor, both driving the device layer through the C
+// ABI in include/ooc_device.h.
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ooc/runtime.hpp"
+#include "ooc_device.h"
+
+namespace ooc {
+
+void device_check(int rc, const char* what);  // throws DeviceError on failure
+
+/// Lowered loop: flattened tapes in the device ABI format, reused per tile.
+struct LoweredLoop {
+  std::vector<ooc_ins> tape;
+  std::vector<int> write_arg, write_len;
+  int reduce_op = OOC_RED_NONE;
+  int reduce_len = 0;
+};
+LoweredLoop lower_loop(const ParLoop& loop);
+
+/// Dense (optionally row-padded) device layout of a box.
+struct BoxLayout {
+  Extent box;       // the largest box the layout must hold (per-dim max lengths)
+  Point stride{0, 0, 0};
+  index_t elems = 0;
+};
+BoxLayout padded_layout(const Extent& box, index_t pad_elems = 16);
+ooc_view view_at(double* data, const Extent& box, const Point& stride);
+ooc_view host_view(Dataset& ds);
+
+class GpuEngine {
+ public:
+  explicit GpuEngine(const RuntimeOptions& opts);
+  ~GpuEngine();
+
+  struct ChainOut {
+    std::vector<AuditRow> audit;
+    std::map<int, int> reduction_slot;  // loop id -> accumulator slot
+  };
+
+  void run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan& plan,
+                    const Footprints& fp, bool cyclic, ChainOut& out);
+  void run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan* plan,
+                    const Footprints* fp, ChainOut& out);
+
+  /// Resident mode: newest values of `d` are on the device (host copy stale).
+  bool host_outdated(DatasetId d) const;
+  void download_resident(Mesh& mesh, DatasetId d);
+  void forget_resident(DatasetId d);
+  /// Block until the reduction written to `slot` has reached host memory.
+  double reduction_value(int slot);
+  void sync();
+  /// Record a timing event on the compute queue; wait on the D2H queue first so a
+  /// mark also covers every download issued so far.
+  int mark();
+  double mark_elapsed(int a, int b);
+  std::vector<ChainTiming> take_timings();
+  std::map<int, double> take_loop_times();
+  ooc_ctx* ctx() { return ctx_; }
+  const ooc_dev_props& props() const { return props_; }
+
+ private:
+  struct Resident {
+    double* dev = nullptr;
+    BoxLayout layout;
+    bool dev_valid = false;
+    bool host_outdated = false;
+    const double* host_ptr = nullptr;
+  };
+  struct PendingChain {
+    ChainTiming t;
+    ooc_event* start = nullptr;
+    ooc_event* end = nullptr;
+  };
+  struct PendingLoop {
+    int loop_id;
+    ooc_event* a;
+    ooc_event* b;
+  };
+
+  ooc_event* ev(std::vector<ooc_event*>& pool, std::size_t i, bool timing = false);
+  ooc_event* fresh_timing_event();
+  void recycle(ooc_event* e);
+  int alloc_red_slot();
+  void launch(int queue, const ParLoop& loop, const LoweredLoop& lw, const Extent& sub,
+              const std::vector<ooc_view>& views, int red_slot);
+  void ensure_pool(index_t elems);
+  void ensure_resident(Mesh& mesh, DatasetId d);
+  void finish_chain(const LoopChain& chain, const std::map<int, int>& red, PendingChain pc);
+
+  RuntimeOptions opts_;
+  ooc_ctx* ctx_ = nullptr;
+  ooc_dev_props props_{};
+  // explicit-mode slot pool (three slots)
+  double* pool_ = nullptr;
+  index_t pool_elems_ = 0;
+  int slot_cursor_ = 0;
+  std::vector<ooc_event*> ev_h2d_, ev_k_, ev_q0_, ev_d2h_;
+  // resident buffers by dataset id
+  std::vector<Resident> res_;
+  // reductions: device accumulator slot -> pinned host mirror
+  double* red_host_ = nullptr;
+  int next_red_slot_ = 0;
+  std::map<int, ooc_event*> red_ready_;  // slot -> event after its D2H
+  std::vector<ooc_event*> free_timing_;
+  std::vector<PendingChain> pending_chains_;
+  std::vector<PendingLoop> pending_loops_;
+  std::map<int, LoweredLoop> lowered_;  // loop id -> lowered tapes
+  std::vector<ooc_event*> marks_;
+};
+
+}  // namespace ooc

@@ -1,0 +1,221 @@
+// Lazy loop-chain runtime with B200 executors.
+//
+// Source-compatible with the reference Runtime (proj/include/ooc/runtime.hpp:53-137):
+// declare / enqueue_loop / fetch_dataset / fetch_reduction / set_cyclic_flag /
+// flush / finish and the same flush semantics (proj/src/runtime.cpp:5-39). What
+// changes is what a flush runs on:
+//
+//   ExecutorKind::tiled_explicit  the out-of-core streaming engine: Algorithm 1 of
+//                                 the paper over three HBM slots and three CUDA
+//                                 streams (H2D / compute+D2D / D2H), pinned host
+//                                 memory, tile-edge reuse device-to-device, no
+//                                 upload of write-first data, no download of
+//                                 read-only data, cyclic discard of temporaries.
+//   ExecutorKind::resident        in-core: datasets stay in HBM across chains;
+//                                 optionally skew-tiled to an L2-sized budget.
+//   ExecutorKind::reference       the reference's whole-range semantics, run as
+//                                 resident with one tile (there is no CPU path).
+//   ExecutorKind::plan_only       flush = plan + record only; nothing executes (CPU
+//                                 planner checks; no results can be fetched).
+//   tiled_cache / unified         KNL/UM cost models of the reference: out of scope.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "ooc/core.hpp"
+#include "ooc/tiler.hpp"
+
+namespace ooc {
+
+enum class ExecutorKind { reference, tiled_cache, tiled_explicit, unified, resident, plan_only };
+
+inline const char* executor_name(ExecutorKind k) {
+  switch (k) {
+    case ExecutorKind::reference:
+      return "reference";
+    case ExecutorKind::tiled_cache:
+      return "cache";
+    case ExecutorKind::tiled_explicit:
+      return "explicit";
+    case ExecutorKind::unified:
+      return "unified";
+    case ExecutorKind::resident:
+      return "resident";
+    default:
+      return "plan_only";
+  }
+}
+
+/// Device description. `capacity_bytes` is the (artificial) HBM budget the
+/// planner sizes the three slots against (proj/include/ooc/device_config.hpp:14-36);
+/// the bandwidth fields are kept for source compatibility only — this build
+/// measures instead of modelling.
+struct DeviceConfig {
+  index_t capacity_bytes = 16000000000;
+  double h2d_bandwidth = 16e9;
+  double d2h_bandwidth = 16e9;
+  double d2d_bandwidth = 510e9;
+  double device_kernel_bandwidth = 510e9;
+  double transfer_latency = 1e-6;
+  index_t cache_page_bytes = 65536;
+  double fault_latency = 50e-6;
+  double prefetch_bandwidth = 16e9;
+  double prefetch_degradation = 1.0;
+  static DeviceConfig pcie() { return DeviceConfig{}; }
+  static DeviceConfig nvlink() {
+    DeviceConfig c;
+    c.h2d_bandwidth = c.d2h_bandwidth = c.prefetch_bandwidth = 40e9;
+    return c;
+  }
+};
+
+enum class ExecPolicy { serial, openmp };  // source compatibility; kernels run on the GPU
+inline ExecPolicy default_exec_policy() { return ExecPolicy::openmp; }
+
+struct RuntimeOptions {
+  ExecutorKind executor = ExecutorKind::reference;
+  DeviceConfig device;
+  int tiles = 0;  // 0 = choose by capacity (explicit) / 1 (resident)
+  int tiled_dim = 0;
+  bool prefetch = false;
+  ExecPolicy policy = default_exec_policy();
+  bool record_chains = false;
+  // ---- B200 additions
+  int gpu = 0;                      // CUDA device ordinal of this runtime
+  index_t resident_budget = 0;      // resident: >0 picks T with 3*slot <= budget (L2 tiling)
+  bool profile_loops = false;       // per-launch CUDA events -> per-loop device time
+  int arena_fill = 0;               // debug: 0 none, 1 zero (reference behaviour), 2 NaN poison
+};
+
+struct FlushRecord {
+  int chain_id;
+  FlushReason reason;
+  int loop_count;
+};
+
+/// Per-(dataset, tile) byte audit (proj/include/ooc/explicit_exec.hpp:20-24).
+struct AuditRow {
+  DatasetId dataset = -1;
+  int tile = -1;
+  index_t uploaded = 0, downloaded = 0, d2d = 0;
+};
+
+struct LoopMetric {
+  int loop_id = -1;
+  index_t points = 0;
+  index_t bytes = 0;
+  double time_s = 0.0;
+  double bandwidth = 0.0;
+};
+
+/// One executed chain as measured on the device (CUDA events).
+struct ChainTiming {
+  int chain_id = -1;
+  int tiles = 1;
+  int loops = 0;
+  index_t metric_bytes = 0;
+  index_t uploaded = 0, downloaded = 0, d2d = 0;
+  double seconds = 0.0;  // first device op of the chain -> last (H2D..D2H)
+};
+
+struct RunReport {
+  std::string mode;
+  int tiles = 1;
+  double average_bandwidth = 0.0;  // metric bytes / device time
+  index_t total_bytes = 0;
+  double total_time = 0.0;
+  double makespan = 0.0;
+  index_t uploaded = 0, downloaded = 0, d2d = 0;
+  double efficiency = 0.0;
+  double hit_rate = -1.0;
+  index_t faults = -1;
+  std::string app, size;
+  int iters = 0;
+  index_t capacity = 0;
+  std::string error;
+};
+
+class GpuEngine;  // device-side state: context, slots, resident buffers, events
+
+class Runtime {
+ public:
+  explicit Runtime(RuntimeOptions opts = {});
+  ~Runtime();
+  Runtime(const Runtime&) = delete;
+  Runtime& operator=(const Runtime&) = delete;
+
+  Mesh& mesh() { return mesh_; }
+  const Mesh& mesh() const { return mesh_; }
+  const RuntimeOptions& options() const { return opts_; }
+
+  DatasetId declare(const std::string& name, const Extent& core, Point halo, index_t elem_bytes,
+                    double fill) {
+    return declare_dataset(mesh_, name, core, halo, elem_bytes, fill);
+  }
+  DatasetId declare(const std::string& name, const Extent& core, Point halo, index_t elem_bytes,
+                    const std::function<double(Point)>& fill) {
+    return declare_dataset(mesh_, name, core, halo, elem_bytes, fill);
+  }
+
+  void enqueue_loop(ParLoop loop);
+  std::vector<double> fetch_dataset(DatasetId d);
+  /// Flushing fetch into caller memory (no intermediate std::vector).
+  void fetch_dataset_into(DatasetId d, double* out, std::size_t n);
+  double fetch_reduction(const std::string& name);
+
+  void set_cyclic_flag(bool on) { cyclic_ = on; }
+  bool cyclic_flag() const { return cyclic_; }
+
+  void flush(FlushReason reason = FlushReason::explicit_flush);
+  void finish();
+  /// Wait for every queued device operation (no host copy-back).
+  void sync();
+  /// Copy every dataset whose newest values live on the device back to host.
+  void sync_host();
+
+  int pending_loops() const { return static_cast<int>(pending_.size()); }
+  int chains_flushed() const { return next_chain_id_; }
+  const std::vector<FlushRecord>& flush_log() const { return flush_log_; }
+  const std::vector<LoopMetric>& loop_metrics();
+  const std::vector<AuditRow>& audit_rows() const { return audit_; }
+  index_t uploaded() const { return uploaded_; }
+  index_t downloaded() const { return downloaded_; }
+  index_t d2d_bytes() const { return d2d_; }
+  PlanCache& plan_cache() { return plans_; }
+  const std::optional<LoopChain>& last_chain() const { return last_chain_; }
+  const std::vector<LoopChain>& chain_log() const { return chain_log_; }
+  int last_tile_count() const { return last_tiles_; }
+  /// Device-measured chain times (forces a device sync to resolve events).
+  const std::vector<ChainTiming>& chain_timings();
+  RunReport report();
+  GpuEngine& engine();
+
+ private:
+  void execute(LoopChain&& chain);
+  const PlanCache::Entry& plan_for(const LoopChain& chain);
+
+  RuntimeOptions opts_;
+  Mesh mesh_;
+  std::vector<ParLoop> pending_;
+  bool cyclic_ = false;
+  int next_loop_id_ = 0;
+  int next_chain_id_ = 0;
+  PlanCache plans_;
+  std::vector<FlushRecord> flush_log_;
+  std::vector<LoopMetric> loop_metrics_;
+  std::map<int, std::size_t> metric_index_;
+  std::vector<AuditRow> audit_;
+  index_t uploaded_ = 0, downloaded_ = 0, d2d_ = 0;
+  int last_tiles_ = 1;
+  std::optional<LoopChain> last_chain_;
+  std::vector<LoopChain> chain_log_;
+  std::map<std::string, int> red_slot_;  // reduction name -> device accumulator slot
+  std::vector<ChainTiming> timings_;
+  std::unique_ptr<GpuEngine> gpu_;
+};
+
+}  // namespace ooc
