@@ -154,6 +154,13 @@ typedef struct {
 } ooc_loop;
 
 int ooc_launch_loop(ooc_ctx* ctx, int queue, const ooc_loop* loop);
+/* One launch running n consecutive loops per point, in order (loop fusion).
+ * Legal only when every cross-loop access is point-wise: a dataset written by an
+ * earlier loop of the group is read by later ones at offset 0 only, and a dataset
+ * read by an earlier loop is written by later ones only if that read was at
+ * offset 0 (the host engine checks this). Points outside a loop's own range skip
+ * it. Reducing loops are launched alone. Same observable result as n launches. */
+int ooc_launch_group(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n);
 
 /* ------------------------------------------------------------ reductions */
 int ooc_reduce_reset(ooc_ctx* ctx, int queue, int slot, int op);

@@ -68,6 +68,7 @@ typedef struct {
   int gpu;
   int profile_loops;
   int arena_fill;            /* debug: 0 none, 1 zero, 2 NaN */
+  int no_fuse;               /* 1: one launch per par_loop (disable loop fusion) */
 } ooc_runtime_options;
 
 void ooc_rt_default_options(ooc_runtime_options* o);

@@ -99,7 +99,8 @@ class Runtime:
     """ooc::Runtime (proj/include/ooc/runtime.hpp:53-137) on a B200."""
 
     def __init__(self, executor="resident", tiles=0, capacity=16_000_000_000, resident_budget=0,
-                 prefetch=False, record=False, gpu=0, profile=False, arena_fill=0, tiled_dim=0):
+                 prefetch=False, record=False, gpu=0, profile=False, arena_fill=0, tiled_dim=0,
+                 fuse=True):
         L = _native.lib()
         o = _native.Options()
         L.ooc_rt_default_options(ctypes.byref(o))
@@ -113,6 +114,7 @@ class Runtime:
         o.gpu = gpu
         o.profile_loops = int(profile)
         o.arena_fill = arena_fill
+        o.no_fuse = 0 if fuse else 1
         h = ctypes.c_void_p()
         _check(L.ooc_rt_create(ctypes.byref(o), ctypes.byref(h)))
         self._h = h

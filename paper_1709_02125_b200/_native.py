@@ -29,6 +29,7 @@ class Options(ctypes.Structure):
         ("gpu", ctypes.c_int),
         ("profile_loops", ctypes.c_int),
         ("arena_fill", ctypes.c_int),
+        ("no_fuse", ctypes.c_int),
     ]
 
 

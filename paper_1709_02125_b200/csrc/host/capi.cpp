@@ -136,6 +136,7 @@ int ooc_rt_create(const ooc_runtime_options* o, ooc_runtime** out) {
     ro.gpu = o->gpu;
     ro.profile_loops = o->profile_loops != 0;
     ro.arena_fill = o->arena_fill;
+    ro.fuse = o->no_fuse == 0;
     auto* h = new ooc_runtime;
     h->rt = std::make_unique<ooc::Runtime>(ro);
     *out = h;

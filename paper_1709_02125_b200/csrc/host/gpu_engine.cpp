@@ -163,8 +163,49 @@ int GpuEngine::alloc_red_slot() {
   return s;
 }
 
+// Loop fusion: consecutive loops run in one launch when every cross-loop access is
+// point-wise, i.e. a point only ever consumes values its own thread produced
+// earlier in the launch (RAW), and no loop overwrites what an earlier loop of the
+// group reads at a neighbour (WAR). Reducing loops always run alone.
+bool GpuEngine::fusable(const ParLoop& b) const {
+  if (group_.loops.empty()) return true;
+  if (!opts_.fuse || b.has_reduction() || group_.loops.size() >= 8) return false;
+  std::size_t tape = group_.tape_len;
+  for (const auto& t : b.write_tapes) tape += t.ins.size();
+  if (tape > 200) return false;
+  for (const ParLoop* a : group_.loops) {
+    if (a->has_reduction() || a->range.ndim != b.range.ndim) return false;
+    for (const LoopArg& x : a->args)
+      for (const LoopArg& y : b.args) {
+        if (x.dataset != y.dataset) continue;
+        if (access_writes(x.mode) && access_reads(y.mode) && !y.stencil.is_point()) return false;
+        if (access_reads(x.mode) && access_writes(y.mode) && !x.stencil.is_point()) return false;
+      }
+  }
+  return true;
+}
+
+void GpuEngine::flush_group(int queue) {
+  if (group_.calls.empty()) return;
+  if (opts_.profile_loops) {
+    PendingLoop pl{{}, fresh_timing_event(), fresh_timing_event()};
+    double total = 0;
+    for (index_t b : group_.bytes) total += static_cast<double>(b);
+    for (std::size_t i = 0; i < group_.loops.size(); ++i)
+      pl.weights.push_back({group_.loops[i]->id, total > 0 ? group_.bytes[i] / total : 1.0});
+    DEV(ooc_event_record(ctx_, pl.a, queue));
+    DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
+    DEV(ooc_event_record(ctx_, pl.b, queue));
+    pending_loops_.push_back(std::move(pl));
+  } else {
+    DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
+  }
+  group_ = Group{};
+}
+
 void GpuEngine::launch(int queue, const ParLoop& loop, const LoweredLoop& lw, const Extent& sub,
                        const std::vector<ooc_view>& views, int red_slot) {
+  if (!fusable(loop)) flush_group(queue);
   ooc_loop L{};
   L.ndim = sub.ndim;
   for (int d = 0; d < 3; ++d) {
@@ -183,15 +224,17 @@ void GpuEngine::launch(int queue, const ParLoop& loop, const LoweredLoop& lw, co
   L.reduce_slot = red_slot;
   L.ntape = static_cast<int32_t>(lw.tape.size());
   L.tape = lw.tape.data();
-  if (opts_.profile_loops) {
-    PendingLoop pl{loop.id, fresh_timing_event(), fresh_timing_event()};
-    DEV(ooc_event_record(ctx_, pl.a, queue));
-    DEV(ooc_launch_loop(ctx_, queue, &L));
-    DEV(ooc_event_record(ctx_, pl.b, queue));
-    pending_loops_.push_back(pl);
-  } else {
-    DEV(ooc_launch_loop(ctx_, queue, &L));
-  }
+  group_.calls.push_back(L);
+  group_.loops.push_back(&loop);
+  group_.bytes.push_back(sub.size() * loop_bytes_per_point_views(loop));
+  group_.tape_len += lw.tape.size();
+  if (loop.has_reduction()) flush_group(queue);
+}
+
+index_t GpuEngine::loop_bytes_per_point_views(const ParLoop& loop) const {
+  index_t n = 0;
+  for (const LoopArg& a : loop.args) n += 8 * (a.mode == AccessMode::read_write ? 2 : 1);
+  return n;
 }
 
 void GpuEngine::ensure_pool(index_t elems) {
@@ -318,11 +361,12 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     down_hull[static_cast<std::size_t>(d)] = Extent::none(mesh[d].alloc().ndim);
     skip_hull[static_cast<std::size_t>(d)] = Extent::none(mesh[d].alloc().ndim);
   }
+  // tapes are lowered once per chain; ooc_launch_loop copies them into kernel params
+  std::vector<LoweredLoop> lowered_store(chain.loops.size());
   std::vector<const LoweredLoop*> lowered(chain.loops.size());
   for (std::size_t j = 0; j < chain.loops.size(); ++j) {
-    auto it = lowered_.find(chain.loops[j].id);
-    if (it == lowered_.end()) it = lowered_.emplace(chain.loops[j].id, lower_loop(chain.loops[j])).first;
-    lowered[j] = &it->second;
+    lowered_store[j] = lower_loop(chain.loops[j]);
+    lowered[j] = &lowered_store[j];
   }
   std::vector<ooc_view> hviews(mesh.datasets.size());
   for (DatasetId d : used) hviews[static_cast<std::size_t>(d)] = host_view(mesh[d]);
@@ -370,6 +414,7 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
       launch(OOC_Q_COMPUTE, loop, *lowered[j], sub, views,
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
+    flush_group(OOC_Q_COMPUTE);
     DEV(ooc_event_record(ctx_, ev(ev_k_, t), OOC_Q_COMPUTE));
 
     if (t + 1 < T) {
@@ -507,13 +552,13 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
       out.reduction_slot[l.id] = s;
       DEV(ooc_reduce_reset(ctx_, OOC_Q_COMPUTE, s, lower_loop(l).reduce_op));
     }
+  std::vector<LoweredLoop> lowered_store(chain.loops.size());
   std::vector<const LoweredLoop*> lowered(chain.loops.size());
   std::vector<std::vector<ooc_view>> views(chain.loops.size());
   for (std::size_t j = 0; j < chain.loops.size(); ++j) {
     const ParLoop& l = chain.loops[j];
-    auto it = lowered_.find(l.id);
-    if (it == lowered_.end()) it = lowered_.emplace(l.id, lower_loop(l)).first;
-    lowered[j] = &it->second;
+    lowered_store[j] = lower_loop(l);
+    lowered[j] = &lowered_store[j];
     for (const LoopArg& a : l.args) {
       const Resident& r = res_[static_cast<std::size_t>(a.dataset)];
       views[j].push_back(view_at(r.dev, mesh[a.dataset].alloc(), r.layout.stride));
@@ -533,6 +578,7 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
       launch(OOC_Q_COMPUTE, l, *lowered[j], sub, views[j],
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
+  flush_group(OOC_Q_COMPUTE);
   for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
   finish_chain(chain, out.reduction_slot, pc);
 }
@@ -588,7 +634,7 @@ std::map<int, double> GpuEngine::take_loop_times() {
     DEV(ooc_event_sync(ctx_, pl.b));
     float ms = 0.f;
     DEV(ooc_event_elapsed_ms(pl.a, pl.b, &ms));
-    out[pl.loop_id] += ms * 1e-3;
+    for (const auto& [id, w] : pl.weights) out[id] += w * ms * 1e-3;
     recycle(pl.a);
     recycle(pl.b);
   }

@@ -96,7 +96,9 @@ void Runtime::sync_host() {
 const PlanCache::Entry& Runtime::plan_for(const LoopChain& chain) {  // runtime.cpp:41-62
   if (opts_.tiles > 0) return plans_.get(mesh_, chain, opts_.tiles, opts_.tiled_dim);
   index_t budget = opts_.device.capacity_bytes;
-  if (opts_.executor == ExecutorKind::resident) budget = opts_.resident_budget;
+  // resident (in-core) tiling has no slot rotation: one tile's working set must fit
+  // the budget (e.g. L2), so choose the smallest T with slot_bytes <= budget.
+  if (opts_.executor == ExecutorKind::resident) budget = 3 * opts_.resident_budget;
   TileChoice c = choose_tile_count(mesh_, chain, budget, opts_.tiled_dim);
   return plans_.get(mesh_, chain, c.tile_count, opts_.tiled_dim);
 }

@@ -79,9 +79,15 @@ class GpuEngine {
     ooc_event* end = nullptr;
   };
   struct PendingLoop {
-    int loop_id;
+    std::vector<std::pair<int, double>> weights;  // loop id -> share of the launch time
     ooc_event* a;
     ooc_event* b;
+  };
+  struct Group {  // loops collected for one fused launch
+    std::vector<ooc_loop> calls;
+    std::vector<const ParLoop*> loops;
+    std::vector<index_t> bytes;
+    std::size_t tape_len = 0;
   };
 
   ooc_event* ev(std::vector<ooc_event*>& pool, std::size_t i, bool timing = false);
@@ -90,6 +96,9 @@ class GpuEngine {
   int alloc_red_slot();
   void launch(int queue, const ParLoop& loop, const LoweredLoop& lw, const Extent& sub,
               const std::vector<ooc_view>& views, int red_slot);
+  bool fusable(const ParLoop& b) const;
+  void flush_group(int queue);
+  index_t loop_bytes_per_point_views(const ParLoop& loop) const;
   void ensure_pool(index_t elems);
   void ensure_resident(Mesh& mesh, DatasetId d);
   void finish_chain(const LoopChain& chain, const std::map<int, int>& red, PendingChain pc);
@@ -111,8 +120,8 @@ class GpuEngine {
   std::vector<ooc_event*> free_timing_;
   std::vector<PendingChain> pending_chains_;
   std::vector<PendingLoop> pending_loops_;
-  std::map<int, LoweredLoop> lowered_;  // loop id -> lowered tapes
   std::vector<ooc_event*> marks_;
+  Group group_;
 };
 
 }  // namespace ooc

@@ -89,6 +89,7 @@ struct RuntimeOptions {
   index_t resident_budget = 0;      // resident: >0 picks T with 3*slot <= budget (L2 tiling)
   bool profile_loops = false;       // per-launch CUDA events -> per-loop device time
   int arena_fill = 0;               // debug: 0 none, 1 zero (reference behaviour), 2 NaN poison
+  bool fuse = true;                 // run point-wise-dependent consecutive loops in one launch
 };
 
 struct FlushRecord {

@@ -91,7 +91,7 @@ def test_apps_medium_vs_oracle(app, nx, ny, nz, iters, span, mode):
         kw = dict(check_audit=False, check_totals=False)
     elif mode == "l2tiled":
         want = oracle_record(prog, "reference")
-        got = product_record(prog, "resident", resident_budget=max(pb // 6, 4096))
+        got = product_record(prog, "resident", resident_budget=max(pb // 2, 4096))
         kw = dict(check_audit=False, check_totals=False)
     else:
         want = oracle_record(prog, "explicit", capacity=pb // 3)
@@ -106,9 +106,9 @@ def test_apps_medium_vs_oracle(app, nx, ny, nz, iters, span, mode):
 def test_native_app_equals_program_on_gpu():
     """run_app through the C++ API == the chain-file program (fields bit-exact)."""
     prog = P.app_program("miniflow2d", 128, 96, iters=12)
-    a = B.load_program(B.Runtime("explicit", capacity=B.problem_bytes("miniflow2d", 128, 96) // 3),
-                       prog)
-    b = B.Runtime("explicit", capacity=B.problem_bytes("miniflow2d", 128, 96) // 3)
+    cap = B.problem_bytes("miniflow2d", 128, 96) // 2
+    a = B.load_program(B.Runtime("explicit", capacity=cap), prog)
+    b = B.Runtime("explicit", capacity=cap)
     b.run_app("miniflow2d", 128, 96, 0, 12)
     for d in range(a.num_datasets):
         assert np.array_equal(a.host(d).view(np.uint64), b.host(d).view(np.uint64))
