@@ -162,6 +162,17 @@ int ooc_launch_loop(ooc_ctx* ctx, int queue, const ooc_loop* loop);
  * it. Reducing loops are launched alone. Same observable result as n launches. */
 int ooc_launch_group(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n);
 
+/* Specialised kernels: the par_loop kernel template instantiated per loop body
+ * (or fused group) with NVRTC at first use, cached per process. mode 0: never
+ * (interpreter only), 1: for launches of >= min_points points (default 2^18),
+ * 2: always (error if NVRTC is unavailable). Env: OOC_JIT, OOC_JIT_MIN_POINTS. */
+int ooc_jit_config(int mode, long long min_points);
+/* Generate + NVRTC-compile (no load, no GPU needed) the specialised kernel of a
+ * group; `log` receives the generated body or the compiler log. */
+int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, int len);
+/* "ok" or why specialisation is unavailable (NVRTC / driver not found). */
+int ooc_jit_status(char* buf, int len);
+
 /* ------------------------------------------------------------ reductions */
 int ooc_reduce_reset(ooc_ctx* ctx, int queue, int slot, int op);
 /* Asynchronous device->host read of a slot into page-locked `dst` on `queue`. */
@@ -174,6 +185,7 @@ typedef struct {
   long long special_launches;
   long long h2d_bytes, d2h_bytes, d2d_bytes;
   long long copy_calls;
+  long long jit_launches, jit_compiles, jit_compile_ms;
 } ooc_dev_stats;
 int ooc_stats(ooc_ctx* ctx, ooc_dev_stats* out);
 int ooc_stats_reset(ooc_ctx* ctx);

@@ -133,6 +133,9 @@ int ooc_rt_num_chains(ooc_runtime* rt);
 const char* ooc_rt_chain_plan_json(ooc_runtime* rt, int chain, int tiles, int64_t budget,
                                    int dump);
 const char* ooc_rt_chain_plan_text(ooc_runtime* rt, int chain, int tiles);
+/* Group recorded chain `chain` as the engine would (fuse = 1: loop fusion) and
+ * generate + NVRTC-compile each group's specialised sm_100a kernel (no GPU needed). */
+const char* ooc_rt_chain_jit_check(ooc_runtime* rt, int chain, int fuse);
 /* dependency_oracle over recorded chain `chain` planned with `tiles`. */
 const char* ooc_rt_chain_oracle_json(ooc_runtime* rt, int chain, int tiles);
 

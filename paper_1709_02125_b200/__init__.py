@@ -299,6 +299,10 @@ class Runtime:
     def chain_plan_text(self, chain, tiles):
         return _native.lib().ooc_rt_chain_plan_text(self._h, chain, tiles).decode()
 
+    def chain_jit_check(self, chain, fuse=True):
+        """Compile (NVRTC, sm_100a, no GPU needed) the specialised kernels of a recorded chain."""
+        return self._json(_native.lib().ooc_rt_chain_jit_check, chain, int(fuse))
+
     def chain_oracle(self, chain, tiles):
         return self._json(_native.lib().ooc_rt_chain_oracle_json, chain, tiles)
 
@@ -352,3 +356,22 @@ def load_program(rt: Runtime, prog):
 __all__ = ["Runtime", "load_program", "problem_bytes", "star", "line", "POINT", "READ", "WRITE",
            "READ_WRITE", "ValidationError", "StaleDataError", "InfeasibleError", "CapacityError",
            "DeviceError", "OocError"]
+
+
+def set_jit(mode: int, min_points: int = -1) -> None:
+    """Specialised-kernel policy (include/ooc_device.h ooc_jit_config): 0 interpreter
+    only, 1 specialise launches of >= min_points points, 2 always specialise."""
+    _native.lib()
+    dev = ctypes.CDLL(_native.device_lib_path())
+    dev.ooc_jit_config.argtypes = [ctypes.c_int, ctypes.c_longlong]
+    rc = dev.ooc_jit_config(mode, min_points)
+    if rc != 0:
+        raise OocError("ooc_jit_config failed")
+
+
+def jit_status() -> str:
+    _native.lib()
+    dev = ctypes.CDLL(_native.device_lib_path())
+    buf = ctypes.create_string_buffer(256)
+    dev.ooc_jit_status(buf, 256)
+    return buf.value.decode()

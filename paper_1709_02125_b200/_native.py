@@ -44,7 +44,7 @@ def lib():
         raise NativeLibraryMissing(
             f"{LIB_PATH} is missing: build it with `python -m paper_1709_02125_b200.build` "
             "(or __graft_entry__.build()); ooc-b200 has no CPU fallback")
-    L = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    L = ctypes.CDLL(LIB_PATH)  # RTLD_LOCAL: keep the ooc:: C++ symbols private
     vp, i, i64, cp, dp = (ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_char_p,
                           ctypes.POINTER(ctypes.c_double))
     I64P = ctypes.POINTER(ctypes.c_int64)
@@ -82,6 +82,7 @@ def lib():
         "ooc_rt_num_chains": (i, [vp]),
         "ooc_rt_chain_plan_json": (cp, [vp, i, i, i64, i]),
         "ooc_rt_chain_plan_text": (cp, [vp, i, i]),
+        "ooc_rt_chain_jit_check": (cp, [vp, i, i]),
         "ooc_rt_chain_oracle_json": (cp, [vp, i, i]),
     }
     for name, (res, args) in sig.items():

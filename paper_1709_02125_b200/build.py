@@ -24,10 +24,10 @@ CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INC = ["-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(CSRC, "include")]
 
-DEV_SRCS = ["device/ooc_device.cu", "device/loop_kernels.cu"]
+DEV_SRCS = ["device/ooc_device.cu", "device/loop_kernels.cu", "device/jit.cu"]
 HOST_SRCS = ["host/core.cpp", "host/tiler.cpp", "host/runtime.cpp", "host/gpu_engine.cpp",
              "host/apps.cpp", "host/capi.cpp"]
-HEADERS_DEV = ["device/internal.cuh"]
+HEADERS_DEV = ["device/internal.cuh", "device/jit.cuh"]
 HEADERS_HOST = ["host/json_writer.hpp"] + [os.path.join("include/ooc", h)
                                             for h in os.listdir(os.path.join(CSRC, "include/ooc"))]
 
@@ -70,11 +70,11 @@ def build(verbose=False, jobs=8):
     devlib = os.path.join(LIB, "liboocdev.so")
     dobjs = [o for o, _ in dev]
     if not os.path.exists(devlib) or os.path.getmtime(devlib) < _newest(dobjs):
-        _run([NVCC] + ARCH + ["-shared", "-o", devlib] + dobjs + ["-cudart", "static"])
+        _run([NVCC] + ARCH + ["-shared", "-o", devlib] + dobjs + ["-cudart", "static", "-ldl"])
     hostlib = os.path.join(LIB, "libooc.so")
     hobjs = [o for o, _ in host]
     if not os.path.exists(hostlib) or os.path.getmtime(hostlib) < _newest(hobjs + [devlib]):
-        _run([CXX, "-shared", "-fopenmp", "-o", hostlib] + hobjs +
+        _run([CXX, "-shared", "-fopenmp", "-Wl,-Bsymbolic", "-o", hostlib] + hobjs +
              ["-L" + LIB, "-loocdev", "-Wl,-rpath,$ORIGIN"])
     return devlib, hostlib
 

@@ -1,0 +1,506 @@
+// Specialised par_loop kernels: the hand-written kernel template below is
+// instantiated per loop body (or fused group of loop bodies) at first use with
+// NVRTC for sm_100a and cached for the life of the process — the same division of
+// labour as OPS, whose code generator emits one CUDA kernel per ops_par_loop with
+// the user's kernel body inlined. Only the expression bodies, the number of
+// reads/writes and the range predicates vary; pointers, strides, ranges and
+// constants are kernel parameters, so a chain whose loops differ only in their
+// constants reuses one compiled kernel.
+//
+// Exactness: the body is emitted as one temporary per tape operation in tape
+// order, compiled with -fmad=false (no contraction), IEEE division, no fast-math;
+// min/max keep std::min/std::max semantics. Results are bit-identical to the
+// interpreter (loop_kernels.cu) and to the reference (tests/test_gpu_parity.py).
+//
+// libnvrtc and libcuda are opened lazily with dlopen so the library still loads
+// (and the interpreter still runs) where they are missing.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "internal.cuh"
+#include "jit.cuh"
+
+using namespace oocdev;
+
+namespace {
+
+// ------------------------------------------------------------ lazily bound APIs
+struct Api {
+  bool tried = false, ok = false, nvrtc_ok = false;
+  std::string why;
+  // nvrtc
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*,
+                        const char* const*) = nullptr;
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+  // driver
+  CUresult (*module_load)(CUmodule*, const void*) = nullptr;
+  CUresult (*get_function)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                     unsigned, CUstream, void**, void**) = nullptr;
+  CUresult (*error_string)(CUresult, const char**) = nullptr;
+};
+
+Api& api() {
+  static Api a;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (a.tried) return a;
+  a.tried = true;
+  void* nv = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+  if (!nv) nv = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+  void* cu = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+  if (!nv) {
+    a.why = "dlopen failed: libnvrtc.so.12";
+    return a;
+  }
+#define BIND(lib, field, name) *reinterpret_cast<void**>(&a.field) = dlsym(lib, name)
+  BIND(nv, create, "nvrtcCreateProgram");
+  BIND(nv, compile, "nvrtcCompileProgram");
+  BIND(nv, log_size, "nvrtcGetProgramLogSize");
+  BIND(nv, log, "nvrtcGetProgramLog");
+  BIND(nv, cubin_size, "nvrtcGetCUBINSize");
+  BIND(nv, cubin, "nvrtcGetCUBIN");
+  BIND(nv, destroy, "nvrtcDestroyProgram");
+  if (cu) {
+    BIND(cu, module_load, "cuModuleLoadData");
+    BIND(cu, get_function, "cuModuleGetFunction");
+    BIND(cu, launch, "cuLaunchKernel");
+    BIND(cu, error_string, "cuGetErrorString");
+  }
+#undef BIND
+  a.nvrtc_ok = a.create && a.compile && a.log_size && a.log && a.cubin_size && a.cubin && a.destroy;
+  a.ok = a.nvrtc_ok && a.module_load && a.get_function && a.launch;
+  if (!a.nvrtc_ok) a.why = "missing NVRTC entry points";
+  else if (!a.ok) a.why = "libcuda.so.1 (driver) not available";
+  return a;
+}
+
+// ------------------------------------------------------------ JIT policy + cache
+int g_mode = -1;                 // 0 off, 1 on above threshold, 2 always
+long long g_min_points = 1 << 18;
+
+int mode() {
+  if (g_mode < 0) {
+    const char* e = std::getenv("OOC_JIT");
+    g_mode = e ? std::atoi(e) : 1;
+    const char* m = std::getenv("OOC_JIT_MIN_POINTS");
+    if (m) g_min_points = std::atoll(m);
+  }
+  return g_mode;
+}
+
+struct Compiled {
+  CUfunction fn = nullptr;
+  int block = 128;
+  int P = 4;
+};
+std::unordered_map<std::string, Compiled> g_cache;
+std::mutex g_cache_mu;
+
+// The kernel template. Everything except <<BODY>> / the constants at the top is
+// fixed hand-written CUDA; JP must match jit.cuh's JitParams field for field.
+const char* kTemplate = R"CUDA(
+struct JitParams {
+  long long nA, nB, nC;
+  double* part;
+  int red_op;
+  int pad;
+  int rng[OOC_JMAX_LOOPS][6];
+  const double* rp[OOC_JMAX_READS];
+  long long rsA[OOC_JMAX_READS];
+  long long rsB[OOC_JMAX_READS];
+  double* wp[OOC_JMAX_WRITES];
+  long long wsA[OOC_JMAX_WRITES];
+  long long wsB[OOC_JMAX_WRITES];
+  double cst[OOC_JMAX_CONST];
+};
+__device__ __forceinline__ double ooc_min(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double ooc_max(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double ooc_ld(const double* q) { return *q; }
+__device__ __forceinline__ double ooc_red(int op, double acc, double v) {
+  if (op == 1) return acc + v;
+  if (op == 2) return v < acc ? v : acc;
+  return acc < v ? v : acc;
+}
+extern "C" __global__ void __launch_bounds__(OOC_BLOCK) ooc_jit_kernel(const __grid_constant__ JitParams p) {
+  const long long rows = p.nA * p.nB;
+  const long long xblocks = (p.nC + OOC_BLOCK * OOC_P - 1) / (OOC_BLOCK * OOC_P);
+#if OOC_RED
+  double acc = p.red_op == 2 ? __longlong_as_double(0x7ff0000000000000LL)
+             : p.red_op == 3 ? __longlong_as_double(0xfff0000000000000LL) : 0.0;
+#endif
+  for (long long row = blockIdx.y; row < rows; row += gridDim.y) {
+    const long long ia = row / p.nB;
+    const long long ib = row - ia * p.nB;
+    for (long long xb = blockIdx.x; xb < xblocks; xb += gridDim.x) {
+      const long long cx = xb * (OOC_BLOCK * OOC_P) + threadIdx.x;
+      bool ok[OOC_P];
+#pragma unroll
+      for (int k = 0; k < OOC_P; ++k) ok[k] = cx + k * OOC_BLOCK < p.nC;
+<<BODY>>
+    }
+  }
+#if OOC_RED
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = ooc_red(p.red_op, acc, __shfl_down_sync(0xffffffffu, acc, o));
+  __shared__ double warp_part[OOC_BLOCK / 32];
+  if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = warp_part[0];
+    for (int i = 1; i < OOC_BLOCK / 32; ++i) b = ooc_red(p.red_op, b, warp_part[i]);
+    p.part[blockIdx.y * gridDim.x + blockIdx.x] = b;
+  }
+#endif
+}
+)CUDA";
+
+struct Canon {
+  int A, B, C;
+};
+Canon canon(int ndim) { return Canon{ndim >= 3 ? ndim - 3 : -1, ndim >= 2 ? ndim - 2 : -1, ndim - 1}; }
+
+// Generate the body + fill the parameter block for a group. Returns false when
+// the group exceeds the template's parameter capacity (caller falls back).
+bool generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& red_op) {
+  std::memset(&jp, 0, sizeof jp);
+  const Canon cn = canon(Ls[0].ndim);
+  int64_t lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = Ls[0].lo[d];
+    hi[d] = Ls[0].hi[d];
+    for (int i = 1; i < n; ++i) {
+      lo[d] = std::min(lo[d], Ls[i].lo[d]);
+      hi[d] = std::max(hi[d], Ls[i].hi[d]);
+    }
+  }
+  auto ext = [&](int d) { return d < 0 ? 1LL : static_cast<long long>(hi[d] - lo[d]); };
+  jp.nA = ext(cn.A);
+  jp.nB = ext(cn.B);
+  jp.nC = ext(cn.C);
+  red_op = n == 1 ? Ls[0].reduce_op : OOC_RED_NONE;
+  jp.red_op = red_op;
+  auto stride = [&](const ooc_view& v, int d) { return d < 0 ? 0LL : static_cast<long long>(v.stride[d]); };
+  auto origin = [&](const ooc_view& v) {
+    long long off = 0;
+    for (int d = 0; d < 3; ++d) off += (lo[d] - v.lo[d]) * v.stride[d];
+    return v.data + off;
+  };
+  int nread = 0, nwrite = 0, ncst = 0;
+  std::vector<const double*> written;
+  std::ostringstream b;
+  for (int i = 0; i < n; ++i) {
+    const ooc_loop& L = Ls[i];
+    if (L.ndim != Ls[0].ndim) return false;
+    for (int a = 0; a < L.nargs; ++a)
+      if (L.args[a].stride[cn.C] != 1) return false;
+    const bool full = L.lo[0] == lo[0] && L.hi[0] == hi[0] && L.lo[1] == lo[1] &&
+                      L.hi[1] == hi[1] && L.lo[2] == lo[2] && L.hi[2] == hi[2];
+    b << "      { // loop " << i << "\n        bool act[OOC_P];\n";
+    if (full) {
+      b << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) act[k] = ok[k];\n";
+    } else {
+      if (i >= OOC_JMAX_LOOPS) return false;
+      auto rel = [&](int d, bool upper) -> int {
+        if (d < 0) return upper ? 1 : 0;
+        return static_cast<int>((upper ? L.hi[d] : L.lo[d]) - lo[d]);
+      };
+      int* r = jp.rng[i];
+      r[0] = rel(cn.A, false);
+      r[1] = rel(cn.A, true);
+      r[2] = rel(cn.B, false);
+      r[3] = rel(cn.B, true);
+      r[4] = rel(cn.C, false);
+      r[5] = rel(cn.C, true);
+      b << "        const bool inab" << i << " = ia >= p.rng[" << i << "][0] && ia < p.rng[" << i
+        << "][1] && ib >= p.rng[" << i << "][2] && ib < p.rng[" << i << "][3];\n"
+        << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) { const long long c = cx + k * OOC_BLOCK;"
+        << " act[k] = ok[k] && inab" << i << " && c >= p.rng[" << i << "][4] && c < p.rng[" << i
+        << "][5]; }\n";
+    }
+    // distinct reads -> loads for every point, issued before any arithmetic
+    struct Rd {
+      int arg;
+      int64_t off[3];
+      int slot;
+    };
+    std::vector<Rd> reads;
+    auto find_read = [&](const ooc_ins& in) -> int {
+      for (const Rd& r : reads)
+        if (r.arg == in.arg && r.off[0] == in.offset[0] && r.off[1] == in.offset[1] &&
+            r.off[2] == in.offset[2])
+          return r.slot;
+      return -1;
+    };
+    for (int t = 0; t < L.ntape; ++t) {
+      const ooc_ins& in = L.tape[t];
+      if (in.op != OOC_OP_READ || find_read(in) >= 0) continue;
+      if (in.arg < 0 || in.arg >= L.nargs || nread >= OOC_JMAX_READS) return false;
+      const ooc_view& v = L.args[in.arg];
+      long long delta = 0;
+      for (int d = 0; d < 3; ++d) delta += in.offset[d] * v.stride[d];
+      jp.rp[nread] = origin(v) + delta;
+      jp.rsA[nread] = stride(v, cn.A);
+      jp.rsB[nread] = stride(v, cn.B);
+      const bool coh = std::find(written.begin(), written.end(), static_cast<const double*>(v.data)) != written.end();
+      b << "        double r" << nread << "[OOC_P];\n#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) r"
+        << nread << "[k] = act[k] ? " << (coh ? "ooc_ld" : "__ldg") << "(p.rp[" << nread
+        << "] + ia * p.rsA[" << nread << "] + ib * p.rsB[" << nread << "] + cx + k * OOC_BLOCK) : 0.0;\n";
+      reads.push_back({in.arg, {in.offset[0], in.offset[1], in.offset[2]}, nread});
+      ++nread;
+    }
+    // expression bodies, one temporary per tape op, in tape order
+    b << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n";
+    const ooc_ins* t = L.tape;
+    int tmp = 0;
+    auto emit = [&](const ooc_ins* tape, int len, const std::string& dst) -> bool {
+      std::vector<std::string> st;
+      for (int q = 0; q < len; ++q) {
+        const ooc_ins& in = tape[q];
+        if (in.op == OOC_OP_CONST) {
+          if (ncst >= OOC_JMAX_CONST) return false;
+          jp.cst[ncst] = in.value;
+          st.push_back("p.cst[" + std::to_string(ncst++) + "]");
+        } else if (in.op == OOC_OP_READ) {
+          st.push_back("r" + std::to_string(find_read(in)) + "[k]");
+        } else if (in.op >= OOC_OP_ADD && in.op <= OOC_OP_MAX) {
+          if (st.size() < 2) return false;
+          std::string y = st.back();
+          st.pop_back();
+          std::string x = st.back();
+          st.pop_back();
+          std::string name = "t" + std::to_string(i) + "_" + std::to_string(tmp++);
+          b << "          const double " << name << " = ";
+          switch (in.op) {
+            case OOC_OP_ADD: b << x << " + " << y; break;
+            case OOC_OP_SUB: b << x << " - " << y; break;
+            case OOC_OP_MUL: b << x << " * " << y; break;
+            case OOC_OP_DIV: b << x << " / " << y; break;
+            case OOC_OP_MIN: b << "ooc_min(" << x << ", " << y << ")"; break;
+            default: b << "ooc_max(" << x << ", " << y << ")"; break;
+          }
+          b << ";\n";
+          st.push_back(name);
+        } else {
+          return false;
+        }
+      }
+      if (st.size() != 1) return false;
+      b << "          " << dst << " = " << st.back() << ";\n";
+      return true;
+    };
+    for (int w = 0; w < L.nwrites; ++w) {
+      b << "          double o" << i << "_" << w << ";\n";
+      if (!emit(t, L.write_len[w], "o" + std::to_string(i) + "_" + std::to_string(w))) return false;
+      t += L.write_len[w];
+    }
+    if (L.reduce_op != OOC_RED_NONE) {
+      if (n != 1) return false;
+      b << "          double rv;\n";
+      if (!emit(t, L.reduce_len, "rv")) return false;
+      b << "          if (act[k]) acc = ooc_red(p.red_op, acc, rv);\n";
+    }
+    // the point's writes land after all of its tapes (kernel_exec.cpp:173-179)
+    for (int w = 0; w < L.nwrites; ++w) {
+      if (nwrite >= OOC_JMAX_WRITES) return false;
+      const ooc_view& v = L.args[L.write_arg[w]];
+      jp.wp[nwrite] = origin(v);
+      jp.wsA[nwrite] = stride(v, cn.A);
+      jp.wsB[nwrite] = stride(v, cn.B);
+      b << "          if (act[k]) p.wp[" << nwrite << "][ia * p.wsA[" << nwrite << "] + ib * p.wsB["
+        << nwrite << "] + cx + k * OOC_BLOCK] = o" << i << "_" << w << ";\n";
+      written.push_back(v.data);
+      ++nwrite;
+    }
+    b << "        }\n      }\n";
+  }
+  body = b.str();
+  return true;
+}
+
+// load = false: compile only (checks that the generated kernel builds for sm_100a;
+// needs NVRTC but no driver/GPU).
+bool compile(const std::string& key, int block, int P, bool red, Compiled& out, std::string& err,
+             bool load = true) {
+  Api& a = api();
+  if (load ? !a.ok : !a.nvrtc_ok) {
+    err = a.why;
+    return false;
+  }
+  std::string src = "#define OOC_BLOCK " + std::to_string(block) + "\n#define OOC_P " +
+                    std::to_string(P) + "\n#define OOC_RED " + (red ? "1" : "0") +
+                    "\n#define OOC_JMAX_LOOPS " + std::to_string(OOC_JMAX_LOOPS) +
+                    "\n#define OOC_JMAX_READS " + std::to_string(OOC_JMAX_READS) +
+                    "\n#define OOC_JMAX_WRITES " + std::to_string(OOC_JMAX_WRITES) +
+                    "\n#define OOC_JMAX_CONST " + std::to_string(OOC_JMAX_CONST) + "\n";
+  std::string tpl = kTemplate;
+  const std::string mark = "<<BODY>>";
+  tpl.replace(tpl.find(mark), mark.size(), key);
+  src += tpl;
+  nvrtcProgram prog;
+  if (a.create(&prog, src.c_str(), "ooc_par_loop.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    err = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
+                        "--prec-div=true", "--prec-sqrt=true", "--ftz=false", "-lineinfo"};
+  nvrtcResult rc = a.compile(prog, 7, opts);
+  if (rc != NVRTC_SUCCESS) {
+    size_t n = 0;
+    a.log_size(prog, &n);
+    std::string log(n, '\0');
+    a.log(prog, log.data());
+    err = "NVRTC compile failed: " + log.substr(0, 2000);
+    a.destroy(&prog);
+    return false;
+  }
+  size_t n = 0;
+  a.cubin_size(prog, &n);
+  std::string cubin(n, '\0');
+  a.cubin(prog, cubin.data());
+  a.destroy(&prog);
+  if (!load) return true;
+  CUmodule mod;
+  CUresult cr = a.module_load(&mod, cubin.data());
+  if (cr != CUDA_SUCCESS) {
+    const char* s = "?";
+    if (a.error_string) a.error_string(cr, &s);
+    err = std::string("cuModuleLoadData: ") + s;
+    return false;
+  }
+  if (a.get_function(&out.fn, mod, "ooc_jit_kernel") != CUDA_SUCCESS) {
+    err = "cuModuleGetFunction failed";
+    return false;
+  }
+  out.block = block;
+  out.P = P;
+  return true;
+}
+
+}  // namespace
+
+namespace oocdev {
+
+// Returns OOC_OK when launched, 1 when the group should go to the interpreter,
+// negative on a hard error. `blocks_out` = number of reduction partials.
+int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_out) {
+  const int m = mode();
+  if (m == 0) return 1;
+  long long pts = 1;
+  {
+    int64_t lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = Ls[0].lo[d];
+      hi[d] = Ls[0].hi[d];
+      for (int i = 1; i < n; ++i) {
+        lo[d] = std::min(lo[d], Ls[i].lo[d]);
+        hi[d] = std::max(hi[d], Ls[i].hi[d]);
+      }
+      pts *= hi[d] - lo[d];
+    }
+  }
+  if (m == 1 && pts < g_min_points) return 1;
+  auto* jp = new JitParams;
+  std::string body;
+  int red_op = OOC_RED_NONE;
+  if (!generate(Ls, n, *jp, body, red_op)) {
+    delete jp;
+    return 1;
+  }
+  const bool red = red_op != OOC_RED_NONE;
+  const int block = 128, P = 4;
+  const std::string key = body + (red ? "|red" : "|nored");
+  Compiled k;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+      k = it->second;
+    } else {
+      std::string err;
+      auto t0 = std::chrono::steady_clock::now();
+      if (!compile(body, block, P, red, k, err)) {
+        delete jp;
+        if (m == 2) {
+          set_error("JIT: " + err);
+          return OOC_ERR_UNSUPPORTED;
+        }
+        return 1;  // toolchain unavailable: the interpreter runs the group
+      }
+      c->stats.jit_compiles++;
+      c->stats.jit_compile_ms += static_cast<long long>(
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      g_cache.emplace(key, k);
+    }
+  }
+  const long long rows = jp->nA * jp->nB;
+  const long long xblocks = (jp->nC + k.block * k.P - 1) / (k.block * k.P);
+  unsigned gx = static_cast<unsigned>(std::min<long long>(xblocks, 1 << 20)), gy;
+  if (red) {
+    gx = static_cast<unsigned>(std::min<long long>(xblocks, c->red_part_cap));
+    long long cap = std::max<long long>(1, c->red_part_cap / gx);
+    cap = std::min<long long>(cap, std::max<long long>(1, 4 * 148 * 8 / gx));
+    gy = static_cast<unsigned>(std::min<long long>(rows, cap));
+    jp->part = c->red_part[q];
+  } else {
+    gy = static_cast<unsigned>(std::min<long long>(rows, 65535));
+  }
+  void* args[] = {jp};
+  CUresult cr = api().launch(k.fn, gx, gy, 1, k.block, 1, 1, 0, reinterpret_cast<CUstream>(c->q[q]),
+                             args, nullptr);
+  delete jp;
+  if (cr != CUDA_SUCCESS) {
+    const char* s = "?";
+    if (api().error_string) api().error_string(cr, &s);
+    set_error(std::string("JIT cuLaunchKernel: ") + s);
+    return OOC_ERR_CUDA;
+  }
+  *blocks_out = static_cast<int>(gx * gy);
+  c->stats.jit_launches++;
+  return OOC_OK;
+}
+
+}  // namespace oocdev
+
+extern "C" int ooc_jit_config(int m, long long min_points) {
+  g_mode = m;
+  if (min_points >= 0) g_min_points = min_points;
+  return OOC_OK;
+}
+
+extern "C" int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, int len) {
+  auto* jp = new JitParams;
+  std::string body, err;
+  int red_op = OOC_RED_NONE;
+  bool ok = generate(loops, n, *jp, body, red_op);
+  delete jp;
+  if (!ok) err = "group exceeds the kernel template's capacity";
+  Compiled k;
+  if (ok) ok = compile(body, 128, 4, red_op != OOC_RED_NONE, k, err, /*load=*/false);
+  if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", ok ? body.c_str() : err.c_str());
+  return ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
+}
+
+extern "C" int ooc_jit_status(char* buf, int len) {
+  Api& a = api();
+  std::snprintf(buf, static_cast<size_t>(len), "%s", a.ok ? "ok" : a.why.c_str());
+  return a.ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
+}

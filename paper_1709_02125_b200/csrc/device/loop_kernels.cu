@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "jit.cuh"
 
 using namespace oocdev;
 
@@ -618,6 +619,20 @@ int ooc_launch_group(ooc_ctx* c, int q, const ooc_loop* loops, int n) {
     total += 1 + 2 * loops[i].ntape + 2 * loops[i].nwrites + 1;
   }
   if (live.empty()) return OOC_OK;
+  int blocks = 0;
+  int jr = oocdev::jit_launch_group(c, q, live.data(), static_cast<int>(live.size()), &blocks);
+  if (jr < 0) return jr;
+  if (jr == OOC_OK) {
+    if (live.size() == 1 && live[0].reduce_op != OOC_RED_NONE) {
+      k_fold<<<1, 1024, 0, c->q[q]>>>(c->red_part[q], blocks, c->red_acc + live[0].reduce_slot,
+                                      live[0].reduce_op);
+      OOC_CUDA_TRY(cudaGetLastError());
+      ++c->stats.kernel_launches;
+    }
+    ++c->stats.kernel_launches;
+    if (live.size() > 1) ++c->stats.special_launches;
+    return OOC_OK;
+  }
   if (total <= 64) return launch_cap<64>(c, q, live.data(), static_cast<int>(live.size()));
   OOC_ARG_CHECK(total <= 1000, "ooc_launch_group: program too long");
   return launch_cap<1000>(c, q, live.data(), static_cast<int>(live.size()));

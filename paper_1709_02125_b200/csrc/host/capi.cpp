@@ -406,6 +406,9 @@ const char* ooc_rt_device_json(ooc_runtime* h) {
     w.key("d2h_bytes").value(st.d2h_bytes);
     w.key("d2d_bytes").value(st.d2d_bytes);
     w.key("copy_calls").value(st.copy_calls);
+    w.key("jit_launches").value(st.jit_launches);
+    w.key("jit_compiles").value(st.jit_compiles);
+    w.key("jit_compile_ms").value(st.jit_compile_ms);
     w.key("mem_in_use").value(in_use);
     w.key("mem_peak").value(peak);
     w.key("build").value(std::string(ooc_dev_build_info()));
@@ -434,6 +437,71 @@ const char* ooc_rt_chain_plan_json(ooc_runtime* h, int chain, int tiles, int64_t
       s = dump ? ooc::plan_dump_json(m, c, ch.plan, ch.footprints)
                : ooc::plan_full_json(m, ch.plan, ch.footprints);
     }
+  });
+  return rc ? err_json() : out_str(s);
+}
+
+const char* ooc_rt_chain_jit_check(ooc_runtime* h, int chain, int fuse) {
+  std::string s;
+  int rc = guard([&] {
+    const ooc::LoopChain& c = h->rt->chain_log().at(static_cast<std::size_t>(chain));
+    const ooc::Mesh& m = h->rt->mesh();
+    // stand-in device views: distinct fake bases per dataset, the resident layout
+    std::vector<ooc_view> views(m.datasets.size());
+    for (std::size_t d = 0; d < m.datasets.size(); ++d) {
+      const ooc::Extent a = m.datasets[d].alloc();
+      ooc::BoxLayout L = ooc::padded_layout(a);
+      views[d] = ooc::view_at(reinterpret_cast<double*>((d + 1) << 32), a, L.stride);
+    }
+    std::vector<ooc::LoweredLoop> low;
+    for (const auto& l : c.loops) low.push_back(ooc::lower_loop(l));
+    ooc::JsonWriter w;
+    w.begin_array();
+    std::vector<const ooc::ParLoop*> grp;
+    std::vector<ooc_loop> calls;
+    std::size_t tape = 0;
+    auto flush = [&] {
+      if (calls.empty()) return;
+      std::vector<char> log(1 << 16);
+      int r = ooc_jit_compile_check(calls.data(), static_cast<int>(calls.size()), log.data(),
+                                    static_cast<int>(log.size()));
+      w.begin_object().key("loops").value(static_cast<long long>(calls.size()));
+      w.key("ok").value(r == OOC_OK);
+      if (r != OOC_OK) w.key("log").value(std::string(log.data()));
+      w.end_object();
+      grp.clear();
+      calls.clear();
+      tape = 0;
+    };
+    for (std::size_t j = 0; j < c.loops.size(); ++j) {
+      const ooc::ParLoop& l = c.loops[j];
+      if (!ooc::can_fuse(grp, tape, l, fuse != 0)) flush();
+      ooc_loop L{};
+      L.ndim = l.range.ndim;
+      for (int d = 0; d < 3; ++d) {
+        L.lo[d] = l.range.lo[d];
+        L.hi[d] = l.range.hi[d];
+      }
+      L.nargs = static_cast<int32_t>(l.args.size());
+      for (std::size_t a = 0; a < l.args.size(); ++a) L.args[a] = views[static_cast<std::size_t>(l.args[a].dataset)];
+      const ooc::LoweredLoop& lw = low[j];
+      L.nwrites = static_cast<int32_t>(lw.write_arg.size());
+      for (std::size_t k = 0; k < lw.write_arg.size(); ++k) {
+        L.write_arg[k] = lw.write_arg[k];
+        L.write_len[k] = lw.write_len[k];
+      }
+      L.reduce_op = lw.reduce_op;
+      L.reduce_len = lw.reduce_len;
+      L.ntape = static_cast<int32_t>(lw.tape.size());
+      L.tape = lw.tape.data();
+      calls.push_back(L);
+      grp.push_back(&l);
+      tape += lw.tape.size();
+      if (l.has_reduction()) flush();
+    }
+    flush();
+    w.end_array();
+    s = w.str();
   });
   return rc ? err_json() : out_str(s);
 }

@@ -167,13 +167,14 @@ int GpuEngine::alloc_red_slot() {
 // point-wise, i.e. a point only ever consumes values its own thread produced
 // earlier in the launch (RAW), and no loop overwrites what an earlier loop of the
 // group reads at a neighbour (WAR). Reducing loops always run alone.
-bool GpuEngine::fusable(const ParLoop& b) const {
-  if (group_.loops.empty()) return true;
-  if (!opts_.fuse || b.has_reduction() || group_.loops.size() >= 8) return false;
-  std::size_t tape = group_.tape_len;
+bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, const ParLoop& b,
+              bool enabled) {
+  if (group.empty()) return true;
+  if (!enabled || b.has_reduction() || group.size() >= 8) return false;
+  std::size_t tape = group_tape;
   for (const auto& t : b.write_tapes) tape += t.ins.size();
   if (tape > 200) return false;
-  for (const ParLoop* a : group_.loops) {
+  for (const ParLoop* a : group) {
     if (a->has_reduction() || a->range.ndim != b.range.ndim) return false;
     for (const LoopArg& x : a->args)
       for (const LoopArg& y : b.args) {
@@ -183,6 +184,10 @@ bool GpuEngine::fusable(const ParLoop& b) const {
       }
   }
   return true;
+}
+
+bool GpuEngine::fusable(const ParLoop& b) const {
+  return can_fuse(group_.loops, group_.tape_len, b, opts_.fuse);
 }
 
 void GpuEngine::flush_group(int queue) {

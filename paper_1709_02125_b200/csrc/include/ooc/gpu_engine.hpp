@@ -24,6 +24,11 @@ struct LoweredLoop {
 };
 LoweredLoop lower_loop(const ParLoop& loop);
 
+/// Loop-fusion legality (see gpu_engine.cpp): can `b` join `group` (total tape
+/// length `group_tape`) in one launch without changing any observable value?
+bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, const ParLoop& b,
+              bool enabled);
+
 /// Dense (optionally row-padded) device layout of a box.
 struct BoxLayout {
   Extent box;       // the largest box the layout must hold (per-dim max lengths)

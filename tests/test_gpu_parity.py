@@ -81,7 +81,7 @@ def test_more_tile_counts_vs_oracle(T):
     ("miniflow3d", 40, 36, 30, 10, 0),
     ("rk3chain3d", 32, 30, 28, 3, 3),
 ])
-@pytest.mark.parametrize("mode", ["resident", "explicit3", "explicit_cyclic", "l2tiled"])
+@pytest.mark.parametrize("mode", ["resident", "explicit3", "explicit_cyclic", "l2tiled", "unfused"])
 def test_apps_medium_vs_oracle(app, nx, ny, nz, iters, span, mode):
     prog = P.app_program(app, nx, ny, nz, iters=iters, span=span, cyclic=(mode == "explicit_cyclic"))
     pb = B.problem_bytes(app, nx, ny, nz, span)
@@ -91,11 +91,15 @@ def test_apps_medium_vs_oracle(app, nx, ny, nz, iters, span, mode):
         kw = dict(check_audit=False, check_totals=False)
     elif mode == "l2tiled":
         want = oracle_record(prog, "reference")
-        got = product_record(prog, "resident", resident_budget=max(pb // 2, 4096))
+        got = product_record(prog, "resident", tiles=3)
         kw = dict(check_audit=False, check_totals=False)
+    elif mode == "unfused":
+        want = oracle_record(prog, "explicit", capacity=pb // 2)
+        got = product_record(prog, "explicit", capacity=pb // 2, fuse=False)
+        kw = {}
     else:
-        want = oracle_record(prog, "explicit", capacity=pb // 3)
-        got = product_record(prog, "explicit", capacity=pb // 3)
+        want = oracle_record(prog, "explicit", capacity=pb // 2)
+        got = product_record(prog, "explicit", capacity=pb // 2)
         kw = {}
     want.pop("_rt", None)
     got.pop("_rt", None)
@@ -113,6 +117,16 @@ def test_native_app_equals_program_on_gpu():
     for d in range(a.num_datasets):
         assert np.array_equal(a.host(d).view(np.uint64), b.host(d).view(np.uint64))
     assert a.fetch_reduction("fieldsum") == b.fetch_reduction("fieldsum")
+
+
+def test_l2_budget_tiling_miniflow():
+    prog = P.app_program("miniflow2d", 256, 200, iters=20)
+    pb = B.problem_bytes("miniflow2d", 256, 200)
+    want = oracle_record(prog, "reference")
+    got = product_record(prog, "resident", resident_budget=pb // 4)
+    want.pop("_rt", None)
+    got.pop("_rt", None)
+    assert not compare(want, got, check_audit=False, check_totals=False)
 
 
 def test_fieldsum_large_within_tolerance():
@@ -168,3 +182,55 @@ def test_device_counters_show_native_kernels():
     dev = rt.device()
     assert dev["kernel_launches"] >= 4 and dev["interp_launches"] >= 4
     assert dev["cc"] == "10.0"
+
+
+@pytest.fixture
+def jit_always():
+    B.set_jit(2, 0)
+    yield
+    B.set_jit(1, 1 << 18)
+
+
+def test_specialised_kernels_vs_golden(golden_random, golden_apps, jit_always):
+    """Every launch through the NVRTC-specialised kernels: same bits as the reference."""
+    assert B.jit_status() == "ok"
+    bad = []
+    for case in golden_random[:40]:
+        prog = P.random_program(case["seed"], **case["kwargs"])
+        for want in case["runs"]:
+            got = product_record(prog, EXEC_OF[want["executor"]], want["tiles"], want["capacity"],
+                                 want["cyclic"])
+            got.pop("_rt", None)
+            diff = compare(want, got, check_audit=want["executor"] == "explicit",
+                           check_totals=want["executor"] == "explicit")
+            if diff:
+                bad.append((case["seed"], want, diff))
+    for case in golden_apps:
+        name, kw = case["case"]
+        kw = dict(kw)
+        prog = P.app_program(name, kw.pop("nx"), kw.pop("ny"), kw.pop("nz", 0), **kw)
+        for want in case["runs"][:2]:
+            got = product_record(prog, EXEC_OF[want["executor"]], want["tiles"], want["capacity"],
+                                 want["cyclic"])
+            got.pop("_rt", None)
+            diff = compare(want, got, check_audit=want["executor"] == "explicit",
+                           check_totals=want["executor"] == "explicit")
+            if diff:
+                bad.append((name, want["executor"], diff))
+    assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_specialised_medium_apps(fuse, jit_always):
+    for app, nx, ny, nz, iters, span in [("miniflow2d", 300, 256, 0, 12, 0),
+                                         ("miniflow3d", 40, 36, 30, 10, 0),
+                                         ("rk3chain", 200, 256, 0, 6, 3)]:
+        prog = P.app_program(app, nx, ny, nz, iters=iters, span=span)
+        pb = B.problem_bytes(app, nx, ny, nz, span)
+        want = oracle_record(prog, "explicit", capacity=pb // 2)
+        got = product_record(prog, "explicit", capacity=pb // 2, fuse=fuse)
+        want.pop("_rt", None)
+        got.pop("_rt", None)
+        assert not compare(want, got), (app, fuse)
+        dev = B.Runtime("resident").device()
+        assert dev["jit_launches"] == 0  # fresh context; counters are per runtime

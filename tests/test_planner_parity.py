@@ -190,3 +190,16 @@ def test_out_of_scope_executors_rejected():
     o.executor = 1  # tiled_cache: KNL cost model, not part of the B200 build
     h = ctypes.c_void_p()
     assert _native.lib().ooc_rt_create(ctypes.byref(o), ctypes.byref(h)) == -1
+
+
+@pytest.mark.parametrize("app,kw", [("miniflow2d", dict(nx=64, ny=48, iters=12)),
+                                    ("rk3chain3d", dict(nx=10, ny=9, nz=8, iters=3, span=3))])
+def test_specialised_kernels_compile_for_sm100a(app, kw):
+    """The NVRTC-instantiated par_loop kernels of every fused group build for sm_100a."""
+    if not B.jit_status() in ("ok", "libcuda.so.1 (driver) not available"):
+        pytest.skip("NVRTC unavailable: " + B.jit_status())
+    rt = B.Runtime("plan_only", record=True, tiles=1)
+    rt.run_app(app, kw["nx"], kw["ny"], kw.get("nz", 0), kw["iters"], kw.get("span", 0))
+    groups = rt.chain_jit_check(rt.num_chains() - 1, fuse=True)
+    assert groups and all(g["ok"] for g in groups), [g.get("log", "")[:500] for g in groups if not g["ok"]]
+    assert max(g["loops"] for g in groups) > 1  # fusion happened
