@@ -110,13 +110,22 @@ int mode() {
 struct Compiled {
   CUfunction fn = nullptr;
   int block = 128;
+  int Q = 1;
   int P = 4;
 };
 std::unordered_map<std::string, Compiled> g_cache;
 std::mutex g_cache_mu;
 
-// The kernel template. Everything except <<BODY>> / the constants at the top is
-// fixed hand-written CUDA; JP must match jit.cuh's JitParams field for field.
+// The kernel template. Everything except <<BODY>> and the constants prepended at
+// compile time is fixed hand-written CUDA; JitParams must match jit.cuh.
+//
+// Thread tile: OOC_Q consecutive rows (canonical b) x OOC_P columns (canonical c,
+// OOC_BLOCK apart so every warp access is a coalesced 256-B line pair). Every load
+// of the tile is issued first, deduplicated per (view, a-offset, c-offset) family
+// across all loops of the group and all b-offsets, so a 5-point stencil reads Q+2
+// rows per Q outputs instead of 3 per output; then each point evaluates the loops
+// in order with values produced earlier in the launch forwarded in registers, and
+// stores.
 const char* kTemplate = R"CUDA(
 struct JitParams {
   long long nA, nB, nC;
@@ -124,37 +133,33 @@ struct JitParams {
   int red_op;
   int pad;
   int rng[OOC_JMAX_LOOPS][6];
-  const double* rp[OOC_JMAX_READS];
-  long long rsA[OOC_JMAX_READS];
-  long long rsB[OOC_JMAX_READS];
+  const double* fp[OOC_JMAX_FAMILIES];
+  long long fsA[OOC_JMAX_FAMILIES], fsB[OOC_JMAX_FAMILIES];
+  long long fbox[OOC_JMAX_FAMILIES][6];
   double* wp[OOC_JMAX_WRITES];
-  long long wsA[OOC_JMAX_WRITES];
-  long long wsB[OOC_JMAX_WRITES];
+  long long wsA[OOC_JMAX_WRITES], wsB[OOC_JMAX_WRITES];
   double cst[OOC_JMAX_CONST];
 };
 __device__ __forceinline__ double ooc_min(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double ooc_max(double a, double b) { return a < b ? b : a; }
-__device__ __forceinline__ double ooc_ld(const double* q) { return *q; }
 __device__ __forceinline__ double ooc_red(int op, double acc, double v) {
   if (op == 1) return acc + v;
   if (op == 2) return v < acc ? v : acc;
   return acc < v ? v : acc;
 }
 extern "C" __global__ void __launch_bounds__(OOC_BLOCK) ooc_jit_kernel(const __grid_constant__ JitParams p) {
-  const long long rows = p.nA * p.nB;
+  const long long nBq = (p.nB + OOC_Q - 1) / OOC_Q;
+  const long long rows = p.nA * nBq;
   const long long xblocks = (p.nC + OOC_BLOCK * OOC_P - 1) / (OOC_BLOCK * OOC_P);
 #if OOC_RED
   double acc = p.red_op == 2 ? __longlong_as_double(0x7ff0000000000000LL)
              : p.red_op == 3 ? __longlong_as_double(0xfff0000000000000LL) : 0.0;
 #endif
   for (long long row = blockIdx.y; row < rows; row += gridDim.y) {
-    const long long ia = row / p.nB;
-    const long long ib = row - ia * p.nB;
+    const long long ia = row / nBq;
+    const long long ib0 = (row - ia * nBq) * OOC_Q;
     for (long long xb = blockIdx.x; xb < xblocks; xb += gridDim.x) {
       const long long cx = xb * (OOC_BLOCK * OOC_P) + threadIdx.x;
-      bool ok[OOC_P];
-#pragma unroll
-      for (int k = 0; k < OOC_P; ++k) ok[k] = cx + k * OOC_BLOCK < p.nC;
 <<BODY>>
     }
   }
@@ -178,9 +183,22 @@ struct Canon {
 };
 Canon canon(int ndim) { return Canon{ndim >= 3 ? ndim - 3 : -1, ndim >= 2 ? ndim - 2 : -1, ndim - 1}; }
 
-// Generate the body + fill the parameter block for a group. Returns false when
-// the group exceeds the template's parameter capacity (caller falls back).
-bool generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& red_op) {
+struct Family {
+  const double* data;
+  long long sA, sB;
+  int64_t oa, oc;
+  int64_t obmin = 0, obmax = 0;
+  const ooc_view* view;
+};
+
+struct Shape {
+  int Q = 1, P = 4;
+};
+
+// Generate the body + parameter block of a group for tile shape (Q, P). Returns
+// false when the group exceeds the template's capacity (caller falls back).
+bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::string& body,
+              int& red_op, int* loaded_values) {
   std::memset(&jp, 0, sizeof jp);
   const Canon cn = canon(Ls[0].ndim);
   int64_t lo[3], hi[3];
@@ -196,29 +214,97 @@ bool generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& 
   jp.nA = ext(cn.A);
   jp.nB = ext(cn.B);
   jp.nC = ext(cn.C);
+  if (n > OOC_JMAX_LOOPS) return false;
   red_op = n == 1 ? Ls[0].reduce_op : OOC_RED_NONE;
+  if (n > 1)
+    for (int i = 0; i < n; ++i)
+      if (Ls[i].reduce_op != OOC_RED_NONE) return false;
   jp.red_op = red_op;
   auto stride = [&](const ooc_view& v, int d) { return d < 0 ? 0LL : static_cast<long long>(v.stride[d]); };
+  auto off_of = [&](const int64_t* o, int d) { return d < 0 ? int64_t{0} : o[d]; };
   auto origin = [&](const ooc_view& v) {
     long long off = 0;
     for (int d = 0; d < 3; ++d) off += (lo[d] - v.lo[d]) * v.stride[d];
     return v.data + off;
   };
-  int nread = 0, nwrite = 0, ncst = 0;
-  std::vector<const double*> written;
-  std::ostringstream b;
+  // ---- families over every read of every loop
+  std::vector<Family> fam;
+  auto family_of = [&](const ooc_view& v, const int64_t* o) -> int {
+    const int64_t oa = off_of(o, cn.A), oc = off_of(o, cn.C);
+    for (std::size_t f = 0; f < fam.size(); ++f)
+      if (fam[f].data == v.data && fam[f].sA == stride(v, cn.A) && fam[f].sB == stride(v, cn.B) &&
+          fam[f].oa == oa && fam[f].oc == oc)
+        return static_cast<int>(f);
+    Family F{v.data, stride(v, cn.A), stride(v, cn.B), oa, oc, off_of(o, cn.B), off_of(o, cn.B), &v};
+    fam.push_back(F);
+    return static_cast<int>(fam.size()) - 1;
+  };
   for (int i = 0; i < n; ++i) {
     const ooc_loop& L = Ls[i];
     if (L.ndim != Ls[0].ndim) return false;
     for (int a = 0; a < L.nargs; ++a)
       if (L.args[a].stride[cn.C] != 1) return false;
+    for (int t = 0; t < L.ntape; ++t) {
+      const ooc_ins& in = L.tape[t];
+      if (in.op != OOC_OP_READ) continue;
+      if (in.arg < 0 || in.arg >= L.nargs) return false;
+      int f = family_of(L.args[in.arg], in.offset);
+      const int64_t ob = off_of(in.offset, cn.B);
+      fam[f].obmin = std::min(fam[f].obmin, ob);
+      fam[f].obmax = std::max(fam[f].obmax, ob);
+    }
+  }
+  if (static_cast<int>(fam.size()) > OOC_JMAX_FAMILIES) return false;
+  std::ostringstream b;
+  int values = 0;
+  for (std::size_t f = 0; f < fam.size(); ++f) {
+    const Family& F = fam[f];
+    const ooc_view& v = *F.view;
+    const int nr = sh.Q - 1 + static_cast<int>(F.obmax - F.obmin) + 1;
+    values += nr * sh.P;
+    jp.fp[f] = origin(v) + F.oa * F.sA;
+    jp.fsA[f] = F.sA;
+    jp.fsB[f] = F.sB;
+    auto rel = [&](int d, bool upper) -> long long {
+      if (d < 0) return upper ? 1 : 0;
+      return (upper ? v.hi[d] : v.lo[d]) - lo[d];
+    };
+    jp.fbox[f][0] = rel(cn.A, false) - F.oa;
+    jp.fbox[f][1] = rel(cn.A, true) - F.oa;
+    jp.fbox[f][2] = rel(cn.B, false);
+    jp.fbox[f][3] = rel(cn.B, true);
+    jp.fbox[f][4] = rel(cn.C, false);
+    jp.fbox[f][5] = rel(cn.C, true);
+    b << "      double F" << f << "[" << nr << "][OOC_P];\n"
+      << "#pragma unroll\n      for (int r = 0; r < " << nr << "; ++r) {\n"
+      << "        const long long bb = ib0 + r + (" << F.obmin << ");\n"
+      << "        const bool rin = ia >= p.fbox[" << f << "][0] && ia < p.fbox[" << f << "][1] && bb >= p.fbox["
+      << f << "][2] && bb < p.fbox[" << f << "][3];\n"
+      << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n"
+      << "          const long long cc = cx + k * OOC_BLOCK + (" << F.oc << ");\n"
+      << "          F" << f << "[r][k] = (rin && cc >= p.fbox[" << f << "][4] && cc < p.fbox[" << f
+      << "][5]) ? __ldg(p.fp[" << f << "] + ia * p.fsA[" << f << "] + bb * p.fsB[" << f << "] + cc) : 0.0;\n"
+      << "        }\n      }\n";
+  }
+  if (loaded_values) *loaded_values = values;
+  // ---- per point: loops in order, forwarding, stores
+  b << "#pragma unroll\n      for (int q = 0; q < OOC_Q; ++q) {\n        const long long bq = ib0 + q;\n"
+    << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n          const long long c = cx + k * OOC_BLOCK;\n"
+    << "          const bool okp = bq < p.nB && c < p.nC;\n";
+  struct Writer {
+    const double* data;
+    int loop;
+    std::string sym;
+  };
+  std::vector<Writer> writers;
+  int ncst = 0, nwrite = 0;
+  for (int i = 0; i < n; ++i) {
+    const ooc_loop& L = Ls[i];
     const bool full = L.lo[0] == lo[0] && L.hi[0] == hi[0] && L.lo[1] == lo[1] &&
                       L.hi[1] == hi[1] && L.lo[2] == lo[2] && L.hi[2] == hi[2];
-    b << "      { // loop " << i << "\n        bool act[OOC_P];\n";
     if (full) {
-      b << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) act[k] = ok[k];\n";
+      b << "          const bool a" << i << " = okp;\n";
     } else {
-      if (i >= OOC_JMAX_LOOPS) return false;
       auto rel = [&](int d, bool upper) -> int {
         if (d < 0) return upper ? 1 : 0;
         return static_cast<int>((upper ? L.hi[d] : L.lo[d]) - lo[d]);
@@ -230,57 +316,32 @@ bool generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& 
       r[3] = rel(cn.B, true);
       r[4] = rel(cn.C, false);
       r[5] = rel(cn.C, true);
-      b << "        const bool inab" << i << " = ia >= p.rng[" << i << "][0] && ia < p.rng[" << i
-        << "][1] && ib >= p.rng[" << i << "][2] && ib < p.rng[" << i << "][3];\n"
-        << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) { const long long c = cx + k * OOC_BLOCK;"
-        << " act[k] = ok[k] && inab" << i << " && c >= p.rng[" << i << "][4] && c < p.rng[" << i
-        << "][5]; }\n";
+      b << "          const bool a" << i << " = okp && ia >= p.rng[" << i << "][0] && ia < p.rng[" << i
+        << "][1] && bq >= p.rng[" << i << "][2] && bq < p.rng[" << i << "][3] && c >= p.rng[" << i
+        << "][4] && c < p.rng[" << i << "][5];\n";
     }
-    // distinct reads -> loads for every point, issued before any arithmetic
-    struct Rd {
-      int arg;
-      int64_t off[3];
-      int slot;
-    };
-    std::vector<Rd> reads;
-    auto find_read = [&](const ooc_ins& in) -> int {
-      for (const Rd& r : reads)
-        if (r.arg == in.arg && r.off[0] == in.offset[0] && r.off[1] == in.offset[1] &&
-            r.off[2] == in.offset[2])
-          return r.slot;
-      return -1;
-    };
-    for (int t = 0; t < L.ntape; ++t) {
-      const ooc_ins& in = L.tape[t];
-      if (in.op != OOC_OP_READ || find_read(in) >= 0) continue;
-      if (in.arg < 0 || in.arg >= L.nargs || nread >= OOC_JMAX_READS) return false;
-      const ooc_view& v = L.args[in.arg];
-      long long delta = 0;
-      for (int d = 0; d < 3; ++d) delta += in.offset[d] * v.stride[d];
-      jp.rp[nread] = origin(v) + delta;
-      jp.rsA[nread] = stride(v, cn.A);
-      jp.rsB[nread] = stride(v, cn.B);
-      const bool coh = std::find(written.begin(), written.end(), static_cast<const double*>(v.data)) != written.end();
-      b << "        double r" << nread << "[OOC_P];\n#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) r"
-        << nread << "[k] = act[k] ? " << (coh ? "ooc_ld" : "__ldg") << "(p.rp[" << nread
-        << "] + ia * p.rsA[" << nread << "] + ib * p.rsB[" << nread << "] + cx + k * OOC_BLOCK) : 0.0;\n";
-      reads.push_back({in.arg, {in.offset[0], in.offset[1], in.offset[2]}, nread});
-      ++nread;
-    }
-    // expression bodies, one temporary per tape op, in tape order
-    b << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n";
-    const ooc_ins* t = L.tape;
     int tmp = 0;
+    auto operand = [&](const ooc_ins& in) -> std::string {
+      const ooc_view& v = L.args[in.arg];
+      const int f = family_of(v, in.offset);
+      const int64_t ob = off_of(in.offset, cn.B);
+      std::string sym = "F" + std::to_string(f) + "[q + " + std::to_string(ob - fam[f].obmin) + "][k]";
+      if (in.offset[0] == 0 && in.offset[1] == 0 && in.offset[2] == 0)
+        for (const Writer& w : writers)  // earliest first: later writers wrap outside
+          if (w.data == v.data)
+            sym = "(a" + std::to_string(w.loop) + " ? " + w.sym + " : " + sym + ")";
+      return sym;
+    };
     auto emit = [&](const ooc_ins* tape, int len, const std::string& dst) -> bool {
       std::vector<std::string> st;
-      for (int q = 0; q < len; ++q) {
-        const ooc_ins& in = tape[q];
+      for (int qd = 0; qd < len; ++qd) {
+        const ooc_ins& in = tape[qd];
         if (in.op == OOC_OP_CONST) {
           if (ncst >= OOC_JMAX_CONST) return false;
           jp.cst[ncst] = in.value;
           st.push_back("p.cst[" + std::to_string(ncst++) + "]");
         } else if (in.op == OOC_OP_READ) {
-          st.push_back("r" + std::to_string(find_read(in)) + "[k]");
+          st.push_back(operand(in));
         } else if (in.op >= OOC_OP_ADD && in.op <= OOC_OP_MAX) {
           if (st.size() < 2) return false;
           std::string y = st.back();
@@ -304,19 +365,17 @@ bool generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& 
         }
       }
       if (st.size() != 1) return false;
-      b << "          " << dst << " = " << st.back() << ";\n";
+      b << "          const double " << dst << " = " << st.back() << ";\n";
       return true;
     };
+    const ooc_ins* t = L.tape;
     for (int w = 0; w < L.nwrites; ++w) {
-      b << "          double o" << i << "_" << w << ";\n";
       if (!emit(t, L.write_len[w], "o" + std::to_string(i) + "_" + std::to_string(w))) return false;
       t += L.write_len[w];
     }
     if (L.reduce_op != OOC_RED_NONE) {
-      if (n != 1) return false;
-      b << "          double rv;\n";
       if (!emit(t, L.reduce_len, "rv")) return false;
-      b << "          if (act[k]) acc = ooc_red(p.red_op, acc, rv);\n";
+      b << "#if OOC_RED\n          if (a" << i << ") acc = ooc_red(p.red_op, acc, rv);\n#endif\n";
     }
     // the point's writes land after all of its tapes (kernel_exec.cpp:173-179)
     for (int w = 0; w < L.nwrites; ++w) {
@@ -325,30 +384,51 @@ bool generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& 
       jp.wp[nwrite] = origin(v);
       jp.wsA[nwrite] = stride(v, cn.A);
       jp.wsB[nwrite] = stride(v, cn.B);
-      b << "          if (act[k]) p.wp[" << nwrite << "][ia * p.wsA[" << nwrite << "] + ib * p.wsB["
-        << nwrite << "] + cx + k * OOC_BLOCK] = o" << i << "_" << w << ";\n";
-      written.push_back(v.data);
+      const std::string sym = "o" + std::to_string(i) + "_" + std::to_string(w);
+      b << "          if (a" << i << ") p.wp[" << nwrite << "][ia * p.wsA[" << nwrite << "] + bq * p.wsB["
+        << nwrite << "] + c] = " << sym << ";\n";
+      writers.push_back({v.data, i, sym});
       ++nwrite;
     }
-    b << "        }\n      }\n";
   }
+  b << "        }\n      }\n";
   body = b.str();
   return true;
 }
 
+// Tile shape: as many rows per thread as keeps the loaded values in registers.
+bool pick_and_generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& red_op,
+                       Shape& sh) {
+  const bool flat = Ls[0].ndim == 1;
+  static const Shape cands2d[] = {{4, 2}, {2, 2}, {1, 2}, {1, 1}};
+  static const Shape cands1d[] = {{1, 4}, {1, 2}, {1, 1}};
+  const Shape* c = flat ? cands1d : cands2d;
+  const int nc = flat ? 3 : 4;
+  for (int i = 0; i < nc; ++i) {
+    int values = 0;
+    if (!generate(Ls, n, c[i], jp, body, red_op, &values)) return false;
+    if (values <= 64 || i == nc - 1) {
+      sh = c[i];
+      return true;
+    }
+  }
+  return false;
+}
+
 // load = false: compile only (checks that the generated kernel builds for sm_100a;
 // needs NVRTC but no driver/GPU).
-bool compile(const std::string& key, int block, int P, bool red, Compiled& out, std::string& err,
-             bool load = true) {
+bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled& out,
+             std::string& err, bool load = true) {
   Api& a = api();
   if (load ? !a.ok : !a.nvrtc_ok) {
     err = a.why;
     return false;
   }
-  std::string src = "#define OOC_BLOCK " + std::to_string(block) + "\n#define OOC_P " +
+  std::string src = "#define OOC_BLOCK " + std::to_string(block) + "\n#define OOC_Q " +
+                    std::to_string(Q) + "\n#define OOC_P " +
                     std::to_string(P) + "\n#define OOC_RED " + (red ? "1" : "0") +
                     "\n#define OOC_JMAX_LOOPS " + std::to_string(OOC_JMAX_LOOPS) +
-                    "\n#define OOC_JMAX_READS " + std::to_string(OOC_JMAX_READS) +
+                    "\n#define OOC_JMAX_FAMILIES " + std::to_string(OOC_JMAX_FAMILIES) +
                     "\n#define OOC_JMAX_WRITES " + std::to_string(OOC_JMAX_WRITES) +
                     "\n#define OOC_JMAX_CONST " + std::to_string(OOC_JMAX_CONST) + "\n";
   std::string tpl = kTemplate;
@@ -391,6 +471,7 @@ bool compile(const std::string& key, int block, int P, bool red, Compiled& out, 
     return false;
   }
   out.block = block;
+  out.Q = Q;
   out.P = P;
   return true;
 }
@@ -421,13 +502,15 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   auto* jp = new JitParams;
   std::string body;
   int red_op = OOC_RED_NONE;
-  if (!generate(Ls, n, *jp, body, red_op)) {
+  Shape sh;
+  if (!pick_and_generate(Ls, n, *jp, body, red_op, sh)) {
     delete jp;
     return 1;
   }
   const bool red = red_op != OOC_RED_NONE;
-  const int block = 128, P = 4;
-  const std::string key = body + (red ? "|red" : "|nored");
+  const int block = 128;
+  const std::string key = body + "|Q" + std::to_string(sh.Q) + "P" + std::to_string(sh.P) +
+                          (red ? "|red" : "|nored");
   Compiled k;
   {
     std::lock_guard<std::mutex> lk(g_cache_mu);
@@ -437,7 +520,7 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     } else {
       std::string err;
       auto t0 = std::chrono::steady_clock::now();
-      if (!compile(body, block, P, red, k, err)) {
+      if (!compile(body, block, sh.Q, sh.P, red, k, err)) {
         delete jp;
         if (m == 2) {
           set_error("JIT: " + err);
@@ -451,7 +534,7 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
       g_cache.emplace(key, k);
     }
   }
-  const long long rows = jp->nA * jp->nB;
+  const long long rows = jp->nA * ((jp->nB + k.Q - 1) / k.Q);
   const long long xblocks = (jp->nC + k.block * k.P - 1) / (k.block * k.P);
   unsigned gx = static_cast<unsigned>(std::min<long long>(xblocks, 1 << 20)), gy;
   if (red) {
@@ -490,11 +573,12 @@ extern "C" int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, in
   auto* jp = new JitParams;
   std::string body, err;
   int red_op = OOC_RED_NONE;
-  bool ok = generate(loops, n, *jp, body, red_op);
+  Shape sh;
+  bool ok = pick_and_generate(loops, n, *jp, body, red_op, sh);
   delete jp;
   if (!ok) err = "group exceeds the kernel template's capacity";
   Compiled k;
-  if (ok) ok = compile(body, 128, 4, red_op != OOC_RED_NONE, k, err, /*load=*/false);
+  if (ok) ok = compile(body, 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
   if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", ok ? body.c_str() : err.c_str());
   return ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
 }

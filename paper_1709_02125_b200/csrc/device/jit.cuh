@@ -5,22 +5,23 @@
 #include "ooc_device.h"
 
 #define OOC_JMAX_LOOPS 8
-#define OOC_JMAX_READS 64
-#define OOC_JMAX_WRITES 32
+#define OOC_JMAX_FAMILIES 48
+#define OOC_JMAX_WRITES 24
 #define OOC_JMAX_CONST 128
 
+// A load family: one dataset view read at one (a, c) offset; its rows are loaded
+// once per thread tile and shared by every read of that view at any b offset.
 struct JitParams {
-  long long nA, nB, nC;
-  double* part;
+  long long nA, nB, nC;                    // canonical extents of the launch box (c contiguous)
+  double* part;                            // reduction block partials
   int red_op;
   int pad;
-  int rng[OOC_JMAX_LOOPS][6];
-  const double* rp[OOC_JMAX_READS];
-  long long rsA[OOC_JMAX_READS];
-  long long rsB[OOC_JMAX_READS];
+  int rng[OOC_JMAX_LOOPS][6];              // per loop: [a0,a1) [b0,b1) [c0,c1) rel. to the box
+  const double* fp[OOC_JMAX_FAMILIES];     // family base (box origin, a-offset folded in)
+  long long fsA[OOC_JMAX_FAMILIES], fsB[OOC_JMAX_FAMILIES];
+  long long fbox[OOC_JMAX_FAMILIES][6];    // safe-load bounds on (a, b, c) rel. to the box
   double* wp[OOC_JMAX_WRITES];
-  long long wsA[OOC_JMAX_WRITES];
-  long long wsB[OOC_JMAX_WRITES];
+  long long wsA[OOC_JMAX_WRITES], wsB[OOC_JMAX_WRITES];
   double cst[OOC_JMAX_CONST];
 };
 

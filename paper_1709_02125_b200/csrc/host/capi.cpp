@@ -2,6 +2,7 @@
 // types become negative status codes; messages go to a thread-local buffer.
 #include "ooc_stencil.h"
 
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -467,7 +468,7 @@ const char* ooc_rt_chain_jit_check(ooc_runtime* h, int chain, int fuse) {
                                     static_cast<int>(log.size()));
       w.begin_object().key("loops").value(static_cast<long long>(calls.size()));
       w.key("ok").value(r == OOC_OK);
-      if (r != OOC_OK) w.key("log").value(std::string(log.data()));
+      if (r != OOC_OK || std::getenv("OOC_JIT_DUMP")) w.key("log").value(std::string(log.data()));
       w.end_object();
       grp.clear();
       calls.clear();
