@@ -400,6 +400,17 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
 bool pick_and_generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& red_op,
                        Shape& sh) {
   const bool flat = Ls[0].ndim == 1;
+  static const char* forced = std::getenv("OOC_JIT_SHAPE");  // "QxP" (experiments)
+  if (forced && *forced) {
+    Shape f;
+    if (std::sscanf(forced, "%dx%d", &f.Q, &f.P) == 2 && f.Q >= 1 && f.P >= 1) {
+      if (flat) f.Q = 1;
+      int values = 0;
+      if (!generate(Ls, n, f, jp, body, red_op, &values)) return false;
+      sh = f;
+      return true;
+    }
+  }
   static const Shape cands2d[] = {{4, 2}, {2, 2}, {1, 2}, {1, 1}};
   static const Shape cands1d[] = {{1, 4}, {1, 2}, {1, 1}};
   const Shape* c = flat ? cands1d : cands2d;

@@ -23,15 +23,16 @@ for m in lm:
     k = "fieldsum" if p == 140 else "L%%d" %% (p %% 14 + 1)
     a = kinds.setdefault(k, [0, 0.0]); a[0] += m[2]; a[1] += m[3]
 d = rt.device()
-print(json.dumps({"n": n, "fuse": fuse, "jit": os.environ.get("OOC_JIT", ""), "jit_launches": d["jit_launches"], "jit_compile_ms": d["jit_compile_ms"],
+print(json.dumps({"n": n, "fuse": fuse, "jit": os.environ.get("OOC_JIT", ""), "shape": os.environ.get("OOC_JIT_SHAPE", ""), "jit_launches": d["jit_launches"], "jit_compile_ms": d["jit_compile_ms"],
                   "GBps": (r1["total_bytes"] - r0["total_bytes"]) / dt / 1e9,
                   "ms_per_step": 1e3 * dt / steps, "dev": rt.device()["kernel_launches"],
                   "per_loop_GBps": {k: round(v[0] / v[1] / 1e9) for k, v in sorted(kinds.items()) if v[1] > 0}}))
 '''
-for jit in ("1", "0"):
+shapes = sys.argv[3].split(",") if len(sys.argv) > 3 else [""]
+for shape in shapes:
     for fuse in (1, 0):
-        var = ""
-        env = dict(os.environ, OOC_JIT=jit)
+        jit = "1"
+        env = dict(os.environ, OOC_JIT=jit, OOC_JIT_SHAPE=shape)
         r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, n, steps, fuse)], env=env,
                            capture_output=True, text=True, timeout=600)
         print(r.stdout.strip() or r.stderr[-2000:], flush=True)
