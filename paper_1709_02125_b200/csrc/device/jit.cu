@@ -136,6 +136,7 @@ struct JitParams {
   const double* fp[OOC_JMAX_FAMILIES];
   long long fsA[OOC_JMAX_FAMILIES], fsB[OOC_JMAX_FAMILIES];
   long long fbox[OOC_JMAX_FAMILIES][6];
+  long long inner[6];
   double* wp[OOC_JMAX_WRITES];
   long long wsA[OOC_JMAX_WRITES], wsB[OOC_JMAX_WRITES];
   double cst[OOC_JMAX_CONST];
@@ -160,7 +161,14 @@ extern "C" __global__ void __launch_bounds__(OOC_BLOCK) ooc_jit_kernel(const __g
     const long long ib0 = (row - ia * nBq) * OOC_Q;
     for (long long xb = blockIdx.x; xb < xblocks; xb += gridDim.x) {
       const long long cx = xb * (OOC_BLOCK * OOC_P) + threadIdx.x;
+      const long long c0 = xb * (OOC_BLOCK * OOC_P);
+      // interior tile: every point active in every loop, every load in bounds
+      if (ia >= p.inner[0] && ia < p.inner[1] && ib0 >= p.inner[2] && ib0 + OOC_Q <= p.inner[3] &&
+          c0 >= p.inner[4] && c0 + OOC_BLOCK * OOC_P <= p.inner[5]) {
+<<FAST>>
+      } else {
 <<BODY>>
+      }
     }
   }
 #if OOC_RED
@@ -227,6 +235,12 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
     for (int d = 0; d < 3; ++d) off += (lo[d] - v.lo[d]) * v.stride[d];
     return v.data + off;
   };
+  // interior bounds start as the whole box; every loop range and load family shrinks them
+  long long inner[6] = {0, jp.nA, 0, jp.nB, 0, jp.nC};
+  auto shrink = [&](int k, long long lo_v, long long hi_v) {
+    inner[2 * k] = std::max(inner[2 * k], lo_v);
+    inner[2 * k + 1] = std::min(inner[2 * k + 1], hi_v);
+  };
   // ---- families over every read of every loop
   std::vector<Family> fam;
   auto family_of = [&](const ooc_view& v, const int64_t* o) -> int {
@@ -255,7 +269,7 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
     }
   }
   if (static_cast<int>(fam.size()) > OOC_JMAX_FAMILIES) return false;
-  std::ostringstream b;
+  std::ostringstream slow, fast;
   int values = 0;
   for (std::size_t f = 0; f < fam.size(); ++f) {
     const Family& F = fam[f];
@@ -269,28 +283,42 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
       if (d < 0) return upper ? 1 : 0;
       return (upper ? v.hi[d] : v.lo[d]) - lo[d];
     };
-    jp.fbox[f][0] = rel(cn.A, false) - F.oa;
-    jp.fbox[f][1] = rel(cn.A, true) - F.oa;
-    jp.fbox[f][2] = rel(cn.B, false);
-    jp.fbox[f][3] = rel(cn.B, true);
-    jp.fbox[f][4] = rel(cn.C, false);
-    jp.fbox[f][5] = rel(cn.C, true);
-    b << "      double F" << f << "[" << nr << "][OOC_P];\n"
-      << "#pragma unroll\n      for (int r = 0; r < " << nr << "; ++r) {\n"
-      << "        const long long bb = ib0 + r + (" << F.obmin << ");\n"
-      << "        const bool rin = ia >= p.fbox[" << f << "][0] && ia < p.fbox[" << f << "][1] && bb >= p.fbox["
-      << f << "][2] && bb < p.fbox[" << f << "][3];\n"
-      << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n"
-      << "          const long long cc = cx + k * OOC_BLOCK + (" << F.oc << ");\n"
-      << "          F" << f << "[r][k] = (rin && cc >= p.fbox[" << f << "][4] && cc < p.fbox[" << f
-      << "][5]) ? __ldg(p.fp[" << f << "] + ia * p.fsA[" << f << "] + bb * p.fsB[" << f << "] + cc) : 0.0;\n"
-      << "        }\n      }\n";
+    long long* fb = jp.fbox[f];
+    fb[0] = rel(cn.A, false) - F.oa;
+    fb[1] = rel(cn.A, true) - F.oa;
+    fb[2] = rel(cn.B, false);
+    fb[3] = rel(cn.B, true);
+    fb[4] = rel(cn.C, false);
+    fb[5] = rel(cn.C, true);
+    // interior: ia in fbox_a; rows ib0+obmin .. ib0+Q-1+obmax in fbox_b; cols+oc in fbox_c
+    shrink(0, fb[0], fb[1]);
+    shrink(1, fb[2] - F.obmin, fb[3] - F.obmax);
+    shrink(2, fb[4] - F.oc, fb[5] - F.oc);
+    const std::string fs = std::to_string(f);
+    slow << "      double F" << fs << "[" << nr << "][OOC_P];\n"
+         << "#pragma unroll\n      for (int r = 0; r < " << nr << "; ++r) {\n"
+         << "        const long long bb = ib0 + r + (" << F.obmin << ");\n"
+         << "        const bool rin = ia >= p.fbox[" << fs << "][0] && ia < p.fbox[" << fs << "][1] && bb >= p.fbox["
+         << fs << "][2] && bb < p.fbox[" << fs << "][3];\n"
+         << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n"
+         << "          const long long cc = cx + k * OOC_BLOCK + (" << F.oc << ");\n"
+         << "          F" << fs << "[r][k] = (rin && cc >= p.fbox[" << fs << "][4] && cc < p.fbox[" << fs
+         << "][5]) ? __ldg(p.fp[" << fs << "] + ia * p.fsA[" << fs << "] + bb * p.fsB[" << fs << "] + cc) : 0.0;\n"
+         << "        }\n      }\n";
+    fast << "      double F" << fs << "[" << nr << "][OOC_P];\n"
+         << "#pragma unroll\n      for (int r = 0; r < " << nr << "; ++r) {\n"
+         << "        const double* rp = p.fp[" << fs << "] + ia * p.fsA[" << fs << "] + (ib0 + r + (" << F.obmin
+         << ")) * p.fsB[" << fs << "] + cx + (" << F.oc << ");\n"
+         << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) F" << fs << "[r][k] = __ldg(rp + k * OOC_BLOCK);\n"
+         << "      }\n";
   }
   if (loaded_values) *loaded_values = values;
   // ---- per point: loops in order, forwarding, stores
-  b << "#pragma unroll\n      for (int q = 0; q < OOC_Q; ++q) {\n        const long long bq = ib0 + q;\n"
-    << "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n          const long long c = cx + k * OOC_BLOCK;\n"
-    << "          const bool okp = bq < p.nB && c < p.nC;\n";
+  const char* point_head =
+      "#pragma unroll\n      for (int q = 0; q < OOC_Q; ++q) {\n        const long long bq = ib0 + q;\n"
+      "#pragma unroll\n        for (int k = 0; k < OOC_P; ++k) {\n          const long long c = cx + k * OOC_BLOCK;\n";
+  slow << point_head << "          const bool okp = bq < p.nB && c < p.nC;\n";
+  fast << point_head;
   struct Writer {
     const double* data;
     int loop;
@@ -302,13 +330,17 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
     const ooc_loop& L = Ls[i];
     const bool full = L.lo[0] == lo[0] && L.hi[0] == hi[0] && L.lo[1] == lo[1] &&
                       L.hi[1] == hi[1] && L.lo[2] == lo[2] && L.hi[2] == hi[2];
+    auto rel = [&](int d, bool upper) -> int {
+      if (d < 0) return upper ? 1 : 0;
+      return static_cast<int>((upper ? L.hi[d] : L.lo[d]) - lo[d]);
+    };
+    shrink(0, rel(cn.A, false), rel(cn.A, true));
+    shrink(1, rel(cn.B, false), rel(cn.B, true));
+    shrink(2, rel(cn.C, false), rel(cn.C, true));
+    const std::string is = std::to_string(i);
     if (full) {
-      b << "          const bool a" << i << " = okp;\n";
+      slow << "          const bool a" << is << " = okp;\n";
     } else {
-      auto rel = [&](int d, bool upper) -> int {
-        if (d < 0) return upper ? 1 : 0;
-        return static_cast<int>((upper ? L.hi[d] : L.lo[d]) - lo[d]);
-      };
       int* r = jp.rng[i];
       r[0] = rel(cn.A, false);
       r[1] = rel(cn.A, true);
@@ -316,12 +348,12 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
       r[3] = rel(cn.B, true);
       r[4] = rel(cn.C, false);
       r[5] = rel(cn.C, true);
-      b << "          const bool a" << i << " = okp && ia >= p.rng[" << i << "][0] && ia < p.rng[" << i
-        << "][1] && bq >= p.rng[" << i << "][2] && bq < p.rng[" << i << "][3] && c >= p.rng[" << i
-        << "][4] && c < p.rng[" << i << "][5];\n";
+      slow << "          const bool a" << is << " = okp && ia >= p.rng[" << is << "][0] && ia < p.rng[" << is
+           << "][1] && bq >= p.rng[" << is << "][2] && bq < p.rng[" << is << "][3] && c >= p.rng[" << is
+           << "][4] && c < p.rng[" << is << "][5];\n";
     }
     int tmp = 0;
-    auto operand = [&](const ooc_ins& in) -> std::string {
+    auto operand = [&](const ooc_ins& in, bool is_fast) -> std::string {
       const ooc_view& v = L.args[in.arg];
       const int f = family_of(v, in.offset);
       const int64_t ob = off_of(in.offset, cn.B);
@@ -329,53 +361,62 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
       if (in.offset[0] == 0 && in.offset[1] == 0 && in.offset[2] == 0)
         for (const Writer& w : writers)  // earliest first: later writers wrap outside
           if (w.data == v.data)
-            sym = "(a" + std::to_string(w.loop) + " ? " + w.sym + " : " + sym + ")";
+            sym = is_fast ? w.sym : "(a" + std::to_string(w.loop) + " ? " + w.sym + " : " + sym + ")";
       return sym;
     };
     auto emit = [&](const ooc_ins* tape, int len, const std::string& dst) -> bool {
-      std::vector<std::string> st;
+      std::vector<std::string> st_s, st_f;
       for (int qd = 0; qd < len; ++qd) {
         const ooc_ins& in = tape[qd];
         if (in.op == OOC_OP_CONST) {
           if (ncst >= OOC_JMAX_CONST) return false;
           jp.cst[ncst] = in.value;
-          st.push_back("p.cst[" + std::to_string(ncst++) + "]");
+          const std::string c = "p.cst[" + std::to_string(ncst++) + "]";
+          st_s.push_back(c);
+          st_f.push_back(c);
         } else if (in.op == OOC_OP_READ) {
-          st.push_back(operand(in));
+          st_s.push_back(operand(in, false));
+          st_f.push_back(operand(in, true));
         } else if (in.op >= OOC_OP_ADD && in.op <= OOC_OP_MAX) {
-          if (st.size() < 2) return false;
-          std::string y = st.back();
-          st.pop_back();
-          std::string x = st.back();
-          st.pop_back();
-          std::string name = "t" + std::to_string(i) + "_" + std::to_string(tmp++);
-          b << "          const double " << name << " = ";
-          switch (in.op) {
-            case OOC_OP_ADD: b << x << " + " << y; break;
-            case OOC_OP_SUB: b << x << " - " << y; break;
-            case OOC_OP_MUL: b << x << " * " << y; break;
-            case OOC_OP_DIV: b << x << " / " << y; break;
-            case OOC_OP_MIN: b << "ooc_min(" << x << ", " << y << ")"; break;
-            default: b << "ooc_max(" << x << ", " << y << ")"; break;
+          if (st_s.size() < 2) return false;
+          const std::string name = "t" + std::to_string(i) + "_" + std::to_string(tmp++);
+          for (int path = 0; path < 2; ++path) {
+            auto& st = path ? st_f : st_s;
+            std::ostringstream& b = path ? fast : slow;
+            std::string y = st.back();
+            st.pop_back();
+            std::string x = st.back();
+            st.pop_back();
+            b << "          const double " << name << " = ";
+            switch (in.op) {
+              case OOC_OP_ADD: b << x << " + " << y; break;
+              case OOC_OP_SUB: b << x << " - " << y; break;
+              case OOC_OP_MUL: b << x << " * " << y; break;
+              case OOC_OP_DIV: b << x << " / " << y; break;
+              case OOC_OP_MIN: b << "ooc_min(" << x << ", " << y << ")"; break;
+              default: b << "ooc_max(" << x << ", " << y << ")"; break;
+            }
+            b << ";\n";
+            st.push_back(name);
           }
-          b << ";\n";
-          st.push_back(name);
         } else {
           return false;
         }
       }
-      if (st.size() != 1) return false;
-      b << "          const double " << dst << " = " << st.back() << ";\n";
+      if (st_s.size() != 1) return false;
+      slow << "          const double " << dst << " = " << st_s.back() << ";\n";
+      fast << "          const double " << dst << " = " << st_f.back() << ";\n";
       return true;
     };
     const ooc_ins* t = L.tape;
     for (int w = 0; w < L.nwrites; ++w) {
-      if (!emit(t, L.write_len[w], "o" + std::to_string(i) + "_" + std::to_string(w))) return false;
+      if (!emit(t, L.write_len[w], "o" + is + "_" + std::to_string(w))) return false;
       t += L.write_len[w];
     }
     if (L.reduce_op != OOC_RED_NONE) {
       if (!emit(t, L.reduce_len, "rv")) return false;
-      b << "#if OOC_RED\n          if (a" << i << ") acc = ooc_red(p.red_op, acc, rv);\n#endif\n";
+      slow << "#if OOC_RED\n          if (a" << is << ") acc = ooc_red(p.red_op, acc, rv);\n#endif\n";
+      fast << "#if OOC_RED\n          acc = ooc_red(p.red_op, acc, rv);\n#endif\n";
     }
     // the point's writes land after all of its tapes (kernel_exec.cpp:173-179)
     for (int w = 0; w < L.nwrites; ++w) {
@@ -384,15 +425,20 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
       jp.wp[nwrite] = origin(v);
       jp.wsA[nwrite] = stride(v, cn.A);
       jp.wsB[nwrite] = stride(v, cn.B);
-      const std::string sym = "o" + std::to_string(i) + "_" + std::to_string(w);
-      b << "          if (a" << i << ") p.wp[" << nwrite << "][ia * p.wsA[" << nwrite << "] + bq * p.wsB["
-        << nwrite << "] + c] = " << sym << ";\n";
+      const std::string sym = "o" + is + "_" + std::to_string(w);
+      const std::string ws = std::to_string(nwrite);
+      slow << "          if (a" << is << ") p.wp[" << ws << "][ia * p.wsA[" << ws << "] + bq * p.wsB[" << ws
+           << "] + c] = " << sym << ";\n";
+      fast << "          p.wp[" << ws << "][ia * p.wsA[" << ws << "] + bq * p.wsB[" << ws << "] + c] = " << sym
+           << ";\n";
       writers.push_back({v.data, i, sym});
       ++nwrite;
     }
   }
-  b << "        }\n      }\n";
-  body = b.str();
+  slow << "        }\n      }\n";
+  fast << "        }\n      }\n";
+  for (int k = 0; k < 6; ++k) jp.inner[k] = inner[k];
+  body = "<<SLOW>>\n" + slow.str() + "<<FAST>>\n" + fast.str();
   return true;
 }
 
@@ -443,8 +489,11 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
                     "\n#define OOC_JMAX_WRITES " + std::to_string(OOC_JMAX_WRITES) +
                     "\n#define OOC_JMAX_CONST " + std::to_string(OOC_JMAX_CONST) + "\n";
   std::string tpl = kTemplate;
-  const std::string mark = "<<BODY>>";
-  tpl.replace(tpl.find(mark), mark.size(), key);
+  const std::size_t fpos = key.find("<<FAST>>\n");
+  const std::string slow_body = key.substr(9, fpos - 9);  // after "<<SLOW>>\n"
+  const std::string fast_body = key.substr(fpos + 9);
+  tpl.replace(tpl.find("<<FAST>>"), 8, fast_body);
+  tpl.replace(tpl.find("<<BODY>>"), 8, slow_body);
   src += tpl;
   nvrtcProgram prog;
   if (a.create(&prog, src.c_str(), "ooc_par_loop.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {

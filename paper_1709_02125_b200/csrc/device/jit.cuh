@@ -20,6 +20,7 @@ struct JitParams {
   const double* fp[OOC_JMAX_FAMILIES];     // family base (box origin, a-offset folded in)
   long long fsA[OOC_JMAX_FAMILIES], fsB[OOC_JMAX_FAMILIES];
   long long fbox[OOC_JMAX_FAMILIES][6];    // safe-load bounds on (a, b, c) rel. to the box
+  long long inner[6];                      // interior tiles: a in [0,1), ib0 in [2, 3-Q], block cols in [4,5)
   double* wp[OOC_JMAX_WRITES];
   long long wsA[OOC_JMAX_WRITES], wsB[OOC_JMAX_WRITES];
   double cst[OOC_JMAX_CONST];
