@@ -170,6 +170,8 @@ int ooc_jit_config(int mode, long long min_points);
 /* Generate + NVRTC-compile (no load, no GPU needed) the specialised kernel of a
  * group; `log` receives the generated body or the compiler log. */
 int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, int len);
+/* JSON summary of the tile-shape autotuning of every specialised kernel. */
+int ooc_jit_report(char* buf, int len);
 /* "ok" or why specialisation is unavailable (NVRTC / driver not found). */
 int ooc_jit_status(char* buf, int len);
 

@@ -126,6 +126,8 @@ const char* ooc_rt_report_json(ooc_runtime* rt);
 const char* ooc_rt_chain_timings_json(ooc_runtime* rt);
 const char* ooc_rt_loop_metrics_json(ooc_runtime* rt);
 const char* ooc_rt_device_json(ooc_runtime* rt);
+/* profile_loops runs: every launch since the last call as [first_loop, nloops, bytes, s]. */
+const char* ooc_rt_launch_log_json(ooc_runtime* rt);
 int ooc_rt_num_chains(ooc_runtime* rt);
 /* Full plan of recorded chain `chain`: tiles>0 plans with that count, else
  * choose_tile_count(budget). `dump` = 1 returns the reference plan_dump_json

@@ -287,6 +287,10 @@ class Runtime:
     def loop_metrics(self):
         return self._json(_native.lib().ooc_rt_loop_metrics_json)
 
+    def launch_log(self):
+        """profile=True runs: [first_loop_id, n_loops, metric_bytes, seconds] per launch."""
+        return self._json(_native.lib().ooc_rt_launch_log_json)
+
     def device(self):
         return self._json(_native.lib().ooc_rt_device_json)
 
@@ -367,6 +371,15 @@ def set_jit(mode: int, min_points: int = -1) -> None:
     rc = dev.ooc_jit_config(mode, min_points)
     if rc != 0:
         raise OocError("ooc_jit_config failed")
+
+
+def jit_report():
+    """Autotuned tile shape of every specialised kernel (ooc_jit_report)."""
+    _native.lib()
+    dev = ctypes.CDLL(_native.device_lib_path())
+    buf = ctypes.create_string_buffer(1 << 16)
+    dev.ooc_jit_report(buf, 1 << 16)
+    return json.loads(buf.value.decode())
 
 
 def jit_status() -> str:

@@ -79,6 +79,7 @@ def lib():
         "ooc_rt_chain_timings_json": (cp, [vp]),
         "ooc_rt_loop_metrics_json": (cp, [vp]),
         "ooc_rt_device_json": (cp, [vp]),
+        "ooc_rt_launch_log_json": (cp, [vp]),
         "ooc_rt_num_chains": (i, [vp]),
         "ooc_rt_chain_plan_json": (cp, [vp, i, i, i64, i]),
         "ooc_rt_chain_plan_text": (cp, [vp, i, i]),

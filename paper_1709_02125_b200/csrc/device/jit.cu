@@ -540,6 +540,52 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
 
 namespace oocdev {
 
+// Autotuning state of one group structure: candidate tile shapes are tried on
+// successive real launches (each one a correct execution of the group), timed with
+// CUDA events, and the fastest per point is kept.
+struct Tuning {
+  std::vector<Shape> cands;
+  std::vector<float> ns_per_point;   // < 0: not measured yet
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<long long> points;
+  std::vector<char> issued;
+  int best = -1;
+};
+std::unordered_map<std::string, Tuning> g_tune;
+
+std::vector<Shape> candidates(int ndim) {
+  static const char* forced = std::getenv("OOC_JIT_SHAPE");
+  if (forced && *forced) {
+    Shape f;
+    if (std::sscanf(forced, "%dx%d", &f.Q, &f.P) == 2 && f.Q >= 1 && f.P >= 1) {
+      if (ndim == 1) f.Q = 1;
+      return {f};
+    }
+  }
+  if (ndim == 1) return {{1, 4}, {1, 8}, {1, 2}};
+  return {{1, 4}, {2, 4}, {4, 2}, {1, 8}};
+}
+
+// Resolve measured candidates (non-blocking) and pick the winner once all are in.
+void settle(Tuning& T) {
+  for (std::size_t i = 0; i < T.cands.size(); ++i) {
+    if (!T.issued[i] || T.ns_per_point[i] >= 0) continue;
+    if (cudaEventQuery(T.ev[i].second) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, T.ev[i].first, T.ev[i].second);
+    T.ns_per_point[i] = ms * 1e6f / static_cast<float>(std::max<long long>(T.points[i], 1));
+  }
+  int best = -1;
+  for (std::size_t i = 0; i < T.cands.size(); ++i) {
+    if (T.ns_per_point[i] < 0) return;
+    if (best < 0 || T.ns_per_point[i] < T.ns_per_point[best]) best = static_cast<int>(i);
+  }
+  T.best = best;
+}
+
 // Returns OOC_OK when launched, 1 when the group should go to the interpreter,
 // negative on a hard error. `blocks_out` = number of reduction partials.
 int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_out) {
@@ -562,37 +608,67 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   auto* jp = new JitParams;
   std::string body;
   int red_op = OOC_RED_NONE;
-  Shape sh;
-  if (!pick_and_generate(Ls, n, *jp, body, red_op, sh)) {
+  // the structural identity of the group = its body at the unit tile shape
+  if (!generate(Ls, n, Shape{1, 1}, *jp, body, red_op, nullptr)) {
     delete jp;
     return 1;
   }
   const bool red = red_op != OOC_RED_NONE;
   const int block = 128;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  Tuning& T = g_tune[body + (red ? "|red" : "|nored")];
+  if (T.cands.empty()) {
+    T.cands = candidates(Ls[0].ndim);
+    T.ns_per_point.assign(T.cands.size(), -1.f);
+    T.ev.resize(T.cands.size());
+    T.points.assign(T.cands.size(), 0);
+    T.issued.assign(T.cands.size(), 0);
+    if (T.cands.size() == 1) T.best = 0;
+  }
+  if (T.best < 0) settle(T);
+  int pick = T.best;
+  bool timing = false;
+  if (pick < 0) {
+    for (std::size_t i = 0; i < T.cands.size() && pick < 0; ++i)
+      if (!T.issued[i]) pick = static_cast<int>(i);
+    if (pick < 0) {
+      // all issued, some still in flight: keep using the first measured or candidate 0
+      pick = 0;
+      for (std::size_t i = 0; i < T.cands.size(); ++i)
+        if (T.ns_per_point[i] >= 0) {
+          pick = static_cast<int>(i);
+          break;
+        }
+    } else {
+      timing = true;
+    }
+  }
+  const Shape sh = T.cands[pick];
+  if (!generate(Ls, n, sh, *jp, body, red_op, nullptr)) {
+    delete jp;
+    return 1;
+  }
   const std::string key = body + "|Q" + std::to_string(sh.Q) + "P" + std::to_string(sh.P) +
                           (red ? "|red" : "|nored");
   Compiled k;
-  {
-    std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto it = g_cache.find(key);
-    if (it != g_cache.end()) {
-      k = it->second;
-    } else {
-      std::string err;
-      auto t0 = std::chrono::steady_clock::now();
-      if (!compile(body, block, sh.Q, sh.P, red, k, err)) {
-        delete jp;
-        if (m == 2) {
-          set_error("JIT: " + err);
-          return OOC_ERR_UNSUPPORTED;
-        }
-        return 1;  // toolchain unavailable: the interpreter runs the group
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) {
+    k = it->second;
+  } else {
+    std::string err;
+    auto t0 = std::chrono::steady_clock::now();
+    if (!compile(body, block, sh.Q, sh.P, red, k, err)) {
+      delete jp;
+      if (m == 2) {
+        set_error("JIT: " + err);
+        return OOC_ERR_UNSUPPORTED;
       }
-      c->stats.jit_compiles++;
-      c->stats.jit_compile_ms += static_cast<long long>(
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-      g_cache.emplace(key, k);
+      return 1;  // toolchain unavailable: the interpreter runs the group
     }
+    c->stats.jit_compiles++;
+    c->stats.jit_compile_ms += static_cast<long long>(
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    g_cache.emplace(key, k);
   }
   const long long rows = jp->nA * ((jp->nB + k.Q - 1) / k.Q);
   const long long xblocks = (jp->nC + k.block * k.P - 1) / (k.block * k.P);
@@ -606,8 +682,17 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   } else {
     gy = static_cast<unsigned>(std::min<long long>(rows, 65535));
   }
+  cudaStream_t st = c->q[q];
+  if (timing) {
+    auto& e = T.ev[pick];
+    if (!e.first) {
+      cudaEventCreate(&e.first);
+      cudaEventCreate(&e.second);
+    }
+    cudaEventRecord(e.first, st);
+  }
   void* args[] = {jp};
-  CUresult cr = api().launch(k.fn, gx, gy, 1, k.block, 1, 1, 0, reinterpret_cast<CUstream>(c->q[q]),
+  CUresult cr = api().launch(k.fn, gx, gy, 1, k.block, 1, 1, 0, reinterpret_cast<CUstream>(st),
                              args, nullptr);
   delete jp;
   if (cr != CUDA_SUCCESS) {
@@ -615,6 +700,11 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     if (api().error_string) api().error_string(cr, &s);
     set_error(std::string("JIT cuLaunchKernel: ") + s);
     return OOC_ERR_CUDA;
+  }
+  if (timing) {
+    cudaEventRecord(T.ev[pick].second, st);
+    T.issued[pick] = 1;
+    T.points[pick] = pts;
   }
   *blocks_out = static_cast<int>(gx * gy);
   c->stats.jit_launches++;
@@ -641,6 +731,30 @@ extern "C" int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, in
   if (ok) ok = compile(body, 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
   if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", ok ? body.c_str() : err.c_str());
   return ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
+}
+
+extern "C" int ooc_jit_report(char* buf, int len) {
+  // JSON: [{"loops": n, "red": 0/1, "shape": "QxP", "ns_per_point": {"QxP": t, ...}}, ...]
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  std::ostringstream o;
+  o << "[";
+  bool first = true;
+  for (const auto& [key, T] : g_tune) {
+    std::size_t nl = 0, pos = 0;
+    const std::string fast = key.substr(0, key.find("<<FAST>>"));
+    while ((pos = fast.find("const bool a", pos)) != std::string::npos) ++nl, ++pos;
+    o << (first ? "" : ",") << "{\"loops\":" << nl << ",\"red\":" << (key.find("|red") != std::string::npos)
+      << ",\"shape\":\"";
+    if (T.best >= 0) o << T.cands[T.best].Q << "x" << T.cands[T.best].P;
+    o << "\",\"ns_per_point\":{";
+    for (std::size_t i = 0; i < T.cands.size(); ++i)
+      o << (i ? "," : "") << "\"" << T.cands[i].Q << "x" << T.cands[i].P << "\":" << T.ns_per_point[i];
+    o << "}}";
+    first = false;
+  }
+  o << "]";
+  std::snprintf(buf, static_cast<size_t>(len), "%s", o.str().c_str());
+  return OOC_OK;
 }
 
 extern "C" int ooc_jit_status(char* buf, int len) {

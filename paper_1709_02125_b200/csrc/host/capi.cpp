@@ -384,6 +384,21 @@ const char* ooc_rt_loop_metrics_json(ooc_runtime* h) {
   return rc ? err_json() : out_str(s);
 }
 
+const char* ooc_rt_launch_log_json(ooc_runtime* h) {
+  std::string s;
+  int rc = guard([&] {
+    h->rt->loop_metrics();  // resolves pending launch events into the log
+    ooc::JsonWriter w;
+    w.begin_array();
+    for (const auto& r : h->rt->engine().launch_log)
+      w.begin_array().value(r.first_loop).value(r.nloops).value(r.bytes).value(r.seconds).end_array();
+    w.end_array();
+    h->rt->engine().launch_log.clear();
+    s = w.str();
+  });
+  return rc ? err_json() : out_str(s);
+}
+
 const char* ooc_rt_device_json(ooc_runtime* h) {
   std::string s;
   int rc = guard([&] {

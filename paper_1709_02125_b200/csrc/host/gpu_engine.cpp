@@ -193,11 +193,12 @@ bool GpuEngine::fusable(const ParLoop& b) const {
 void GpuEngine::flush_group(int queue) {
   if (group_.calls.empty()) return;
   if (opts_.profile_loops) {
-    PendingLoop pl{{}, fresh_timing_event(), fresh_timing_event()};
+    PendingLoop pl{{}, 0, fresh_timing_event(), fresh_timing_event()};
     double total = 0;
     for (index_t b : group_.bytes) total += static_cast<double>(b);
     for (std::size_t i = 0; i < group_.loops.size(); ++i)
       pl.weights.push_back({group_.loops[i]->id, total > 0 ? group_.bytes[i] / total : 1.0});
+    pl.bytes = static_cast<index_t>(total);
     DEV(ooc_event_record(ctx_, pl.a, queue));
     DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
     DEV(ooc_event_record(ctx_, pl.b, queue));
@@ -640,6 +641,8 @@ std::map<int, double> GpuEngine::take_loop_times() {
     float ms = 0.f;
     DEV(ooc_event_elapsed_ms(pl.a, pl.b, &ms));
     for (const auto& [id, w] : pl.weights) out[id] += w * ms * 1e-3;
+    if (!pl.weights.empty())
+      launch_log.push_back({pl.weights.front().first, static_cast<int>(pl.weights.size()), pl.bytes, ms * 1e-3});
     recycle(pl.a);
     recycle(pl.b);
   }

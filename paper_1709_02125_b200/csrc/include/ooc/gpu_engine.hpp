@@ -67,6 +67,13 @@ class GpuEngine {
   double mark_elapsed(int a, int b);
   std::vector<ChainTiming> take_timings();
   std::map<int, double> take_loop_times();
+  /// Profiled launches (profile_loops): first loop id, #loops, metric bytes, seconds.
+  struct LaunchRecord {
+    int first_loop, nloops;
+    index_t bytes;
+    double seconds;
+  };
+  std::vector<LaunchRecord> launch_log;
   ooc_ctx* ctx() { return ctx_; }
   const ooc_dev_props& props() const { return props_; }
 
@@ -85,6 +92,7 @@ class GpuEngine {
   };
   struct PendingLoop {
     std::vector<std::pair<int, double>> weights;  // loop id -> share of the launch time
+    index_t bytes = 0;                            // metric bytes of the launch
     ooc_event* a;
     ooc_event* b;
   };
