@@ -98,6 +98,22 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def profiled_traffic(group):
+    """DRAM bytes per launch of `group` from the committed ncu launch list
+    (profiles/*_traffic.json, produced from the same bench command)."""
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), reverse=True):
+        try:
+            with open(f) as fh:
+                prof = json.load(fh)
+        except Exception:
+            continue
+        for k in prof.get("kernels", []):
+            if k.get("group", "").split(" ")[0] == group:
+                return k["dram_bytes_per_launch"], os.path.relpath(f, ROOT)
+    return None, None
+
+
 def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -273,6 +289,7 @@ def main():
     dom = max(kinds, key=lambda k: kinds[k]["seconds"]) if kinds else None
     achieved = (kinds[dom]["bytes"] / kinds[dom]["seconds"] / 1e9) if dom else None
     total_k = sum(k["seconds"] for k in kinds.values())
+    traffic, traffic_src = profiled_traffic(dom) if dom else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
@@ -285,7 +302,15 @@ def main():
                    "l2": "inputs (18.9 GB) >> L2 (126 MB); no flush needed",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "dram_GBps": (traffic / (kinds[dom]["seconds"] / kinds[dom]["launches"]) / 1e9
+                                   if traffic and dom else None),
+                     "dram_frac": (traffic / (kinds[dom]["seconds"] / kinds[dom]["launches"]) / 1e9 / peak
+                                   if traffic and dom else None),
+                     "note": "achieved counts the reference's metric bytes of every loop fused into the "
+                             "kernel (proj/src/metrics.cpp:10-12); traffic/dram_* are the DRAM bytes the "
+                             "fused kernel really moves (ncu)",
                      "peak_source": peak_kind,
                      "kernel": f"ooc_jit_kernel [{dom}] (fused sm_100a par_loop kernel)",
                      "kernel_share_of_step": kinds[dom]["seconds"] / total_k if dom else None,
