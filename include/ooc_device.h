@@ -180,6 +180,25 @@ int ooc_reduce_reset(ooc_ctx* ctx, int queue, int slot, int op);
 /* Asynchronous device->host read of a slot into page-locked `dst` on `queue`. */
 int ooc_reduce_fetch(ooc_ctx* ctx, int queue, int slot, double* dst);
 
+/* ------------------------------------------------------------ multi-GPU (NCCL) */
+/* Slab decomposition plumbing (new; the reference is single-device).
+ * ooc_comm_unique_id fills 128 opaque bytes on one rank; every rank passes them to
+ * ooc_comm_init. Exchanges are grouped NCCL send/recv of contiguous device ranges
+ * (whole rows of the outermost dimension), enqueued on `queue`. */
+typedef struct {
+  int peer;
+  const double* send;
+  int64_t send_count; /* doubles */
+  double* recv;
+  int64_t recv_count;
+} ooc_xfer;
+int ooc_comm_unique_id(void* out128);
+int ooc_comm_init(ooc_ctx* ctx, int rank, int world, const void* id128);
+int ooc_comm_exchange(ooc_ctx* ctx, int queue, const ooc_xfer* xfers, int n);
+/* All-reduce of one reduction accumulator across the communicator (sum/min/max). */
+int ooc_reduce_allreduce(ooc_ctx* ctx, int queue, int slot, int op);
+void ooc_comm_release(ooc_ctx* ctx);
+
 /* ------------------------------------------------------------ statistics */
 typedef struct {
   long long kernel_launches;
@@ -188,6 +207,7 @@ typedef struct {
   long long h2d_bytes, d2h_bytes, d2d_bytes;
   long long copy_calls;
   long long jit_launches, jit_compiles, jit_compile_ms;
+  long long comm_bytes;
 } ooc_dev_stats;
 int ooc_stats(ooc_ctx* ctx, ooc_dev_stats* out);
 int ooc_stats_reset(ooc_ctx* ctx);

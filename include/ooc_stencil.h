@@ -69,6 +69,10 @@ typedef struct {
   int profile_loops;
   int arena_fill;            /* debug: 0 none, 1 zero, 2 NaN */
   int no_fuse;               /* 1: one launch per par_loop (disable loop fusion) */
+  /* slab decomposition (new; the reference is single-device): this rank owns rows
+   * [own_lo, own_hi) of dimension 0 and recomputes `ghost` rows each side */
+  int dist_rank, dist_world;
+  long long own_lo, own_hi, ghost;
 } ooc_runtime_options;
 
 void ooc_rt_default_options(ooc_runtime_options* o);
@@ -135,6 +139,12 @@ int ooc_rt_num_chains(ooc_runtime* rt);
 const char* ooc_rt_chain_plan_json(ooc_runtime* rt, int chain, int tiles, int64_t budget,
                                    int dump);
 const char* ooc_rt_chain_plan_text(ooc_runtime* rt, int chain, int tiles);
+/* Slab decomposition: join the NCCL communicator (id from ooc_comm_unique_id in
+ * ooc_device.h); export a recorded chain's (window-clipped) loops; its ghost depth
+ * and the ghost-band exchange it triggers. */
+int ooc_rt_comm_init(ooc_runtime* rt, const void* unique_id128);
+const char* ooc_rt_chain_export_json(ooc_runtime* rt, int chain);
+const char* ooc_rt_dist_plan_json(ooc_runtime* rt, int chain);
 /* Group recorded chain `chain` as the engine would (fuse = 1: loop fusion) and
  * generate + NVRTC-compile each group's specialised sm_100a kernel (no GPU needed). */
 const char* ooc_rt_chain_jit_check(ooc_runtime* rt, int chain, int fuse);

@@ -100,7 +100,7 @@ class Runtime:
 
     def __init__(self, executor="resident", tiles=0, capacity=16_000_000_000, resident_budget=0,
                  prefetch=False, record=False, gpu=0, profile=False, arena_fill=0, tiled_dim=0,
-                 fuse=True):
+                 fuse=True, dist=(0, 1), own=None, ghost=0):
         L = _native.lib()
         o = _native.Options()
         L.ooc_rt_default_options(ctypes.byref(o))
@@ -115,6 +115,10 @@ class Runtime:
         o.profile_loops = int(profile)
         o.arena_fill = arena_fill
         o.no_fuse = 0 if fuse else 1
+        o.dist_rank, o.dist_world = int(dist[0]), int(dist[1])
+        if own is not None:
+            o.own_lo, o.own_hi = int(own[0]), int(own[1])
+        o.ghost = int(ghost)
         h = ctypes.c_void_p()
         _check(L.ooc_rt_create(ctypes.byref(o), ctypes.byref(h)))
         self._h = h
@@ -302,6 +306,19 @@ class Runtime:
 
     def chain_plan_text(self, chain, tiles):
         return _native.lib().ooc_rt_chain_plan_text(self._h, chain, tiles).decode()
+
+    # ---------------------------------------------------------------- slab decomposition
+    def comm_init(self, unique_id: bytes):
+        """Join the NCCL communicator of the slab decomposition (128-byte id)."""
+        _check(_native.lib().ooc_rt_comm_init(self._h, unique_id))
+
+    def chain_export(self, chain):
+        """A recorded chain's loops as this rank runs them (window-clipped)."""
+        return self._json(_native.lib().ooc_rt_chain_export_json, chain)
+
+    def dist_plan(self, chain):
+        """Ghost depth the chain needs and the ghost-band exchange it triggers."""
+        return self._json(_native.lib().ooc_rt_dist_plan_json, chain)
 
     def chain_jit_check(self, chain, fuse=True):
         """Compile (NVRTC, sm_100a, no GPU needed) the specialised kernels of a recorded chain."""

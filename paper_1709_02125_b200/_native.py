@@ -30,6 +30,11 @@ class Options(ctypes.Structure):
         ("profile_loops", ctypes.c_int),
         ("arena_fill", ctypes.c_int),
         ("no_fuse", ctypes.c_int),
+        ("dist_rank", ctypes.c_int),
+        ("dist_world", ctypes.c_int),
+        ("own_lo", ctypes.c_longlong),
+        ("own_hi", ctypes.c_longlong),
+        ("ghost", ctypes.c_longlong),
     ]
 
 
@@ -84,6 +89,9 @@ def lib():
         "ooc_rt_chain_plan_json": (cp, [vp, i, i, i64, i]),
         "ooc_rt_chain_plan_text": (cp, [vp, i, i]),
         "ooc_rt_chain_jit_check": (cp, [vp, i, i]),
+        "ooc_rt_comm_init": (i, [vp, ctypes.c_char_p]),
+        "ooc_rt_chain_export_json": (cp, [vp, i]),
+        "ooc_rt_dist_plan_json": (cp, [vp, i]),
         "ooc_rt_chain_oracle_json": (cp, [vp, i, i]),
     }
     for name, (res, args) in sig.items():

@@ -50,4 +50,7 @@ struct ooc_ctx {
   double* red_part[OOC_NUM_QUEUES] = {nullptr, nullptr, nullptr};
   int red_part_cap = 0;
   ooc_dev_stats stats{};
+  // multi-GPU (comm.cu): NCCL communicator of the slab decomposition
+  void* comm = nullptr;
+  int rank = 0, world = 1;
 };

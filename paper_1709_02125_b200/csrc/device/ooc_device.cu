@@ -128,6 +128,7 @@ int ooc_ctx_destroy(ooc_ctx* c) {
   if (!c) return OOC_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  ooc_comm_release(c);
   for (auto& [p, sz] : c->allocs) cudaFree(p);
   cudaFree(c->red_acc);
   for (int q = 0; q < OOC_NUM_QUEUES; ++q) {

@@ -138,6 +138,11 @@ int ooc_rt_create(const ooc_runtime_options* o, ooc_runtime** out) {
     ro.profile_loops = o->profile_loops != 0;
     ro.arena_fill = o->arena_fill;
     ro.fuse = o->no_fuse == 0;
+    ro.dist_rank = o->dist_rank;
+    ro.dist_world = o->dist_world > 0 ? o->dist_world : 1;
+    ro.own_lo = o->own_lo;
+    ro.own_hi = o->own_hi;
+    ro.ghost = o->ghost;
     auto* h = new ooc_runtime;
     h->rt = std::make_unique<ooc::Runtime>(ro);
     *out = h;
@@ -517,6 +522,74 @@ const char* ooc_rt_chain_jit_check(ooc_runtime* h, int chain, int fuse) {
     }
     flush();
     w.end_array();
+    s = w.str();
+  });
+  return rc ? err_json() : out_str(s);
+}
+
+int ooc_rt_comm_init(ooc_runtime* h, const void* unique_id) {
+  return guard([&] { h->rt->comm_init(unique_id); });
+}
+
+const char* ooc_rt_chain_export_json(ooc_runtime* h, int chain) {
+  std::string s;
+  int rc = guard([&] {
+    const ooc::LoopChain& c = h->rt->chain_log().at(static_cast<std::size_t>(chain));
+    const ooc::Mesh& m = h->rt->mesh();
+    ooc::JsonWriter w;
+    w.begin_array();
+    for (const ooc::ParLoop& l : c.loops) {
+      w.begin_object();
+      w.key("id").value(l.id);
+      w.key("lo").begin_array();
+      for (int d = 0; d < l.range.ndim; ++d) w.value(l.range.lo[d]);
+      w.end_array();
+      w.key("hi").begin_array();
+      for (int d = 0; d < l.range.ndim; ++d) w.value(l.range.hi[d]);
+      w.end_array();
+      w.key("args").begin_array();
+      for (const ooc::LoopArg& a : l.args) {
+        w.begin_object().key("dataset").value(m[a.dataset].name).key("mode").value(ooc::access_name(a.mode));
+        w.key("offsets").begin_array();
+        for (const ooc::Point& o : a.stencil.offsets) w.begin_array().value(o[0]).value(o[1]).value(o[2]).end_array();
+        w.end_array().end_object();
+      }
+      w.end_array();
+      w.key("writes").begin_object();
+      for (const auto& wr : l.kernel.writes) w.key(std::to_string(wr.arg)).value(ooc::expr_to_string(wr.expr));
+      w.end_object();
+      if (l.has_reduction()) {
+        const char* op = l.kernel.reduce == ooc::ReduceOp::sum ? "SUM" : l.kernel.reduce == ooc::ReduceOp::min ? "MIN" : "MAX";
+        w.key("reduction").begin_object().key("op").value(op).key("expr").value(ooc::expr_to_string(l.kernel.reduce_expr))
+            .key("name").value(l.kernel.reduce_name).end_object();
+      }
+      w.end_object();
+    }
+    w.end_array();
+    s = w.str();
+  });
+  return rc ? err_json() : out_str(s);
+}
+
+const char* ooc_rt_dist_plan_json(ooc_runtime* h, int chain) {
+  std::string s;
+  int rc = guard([&] {
+    const ooc::LoopChain& c = h->rt->chain_log().at(static_cast<std::size_t>(chain));
+    const ooc::Mesh& m = h->rt->mesh();
+    ooc::JsonWriter w;
+    w.begin_object();
+    w.key("depth").value(h->rt->dependency_depth(c));
+    w.key("ghost").value(h->rt->options().ghost);
+    w.key("halos").begin_array();
+    for (const ooc::HaloXfer& x : h->rt->halo_plan(c)) {
+      w.begin_object().key("dataset").value(m[x.dataset].name);
+      const std::pair<const char*, const ooc::index_t*> f[] = {
+          {"send_left", x.send_left}, {"recv_left", x.recv_left}, {"send_right", x.send_right}, {"recv_right", x.recv_right}};
+      for (const auto& [k, v] : f) w.key(k).begin_array().value(v[0]).value(v[1]).end_array();
+      w.end_object();
+    }
+    w.end_array();
+    w.end_object();
     s = w.str();
   });
   return rc ? err_json() : out_str(s);

@@ -532,7 +532,8 @@ void GpuEngine::forget_resident(DatasetId d) {
 }
 
 void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan* plan,
-                             const Footprints* fp, ChainOut& out) {
+                             const Footprints* fp, ChainOut& out,
+                             const std::vector<HaloXfer>* halos) {
   (void)fp;
   PendingChain pc;
   pc.start = fresh_timing_event();
@@ -585,8 +586,37 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
   flush_group(OOC_Q_COMPUTE);
+  if (halos && comm_ready_) {
+    // slab decomposition: refresh every ghost band from the neighbours' owned rows,
+    // then combine the ranks' reductions — both stream-ordered after the kernels
+    std::vector<ooc_xfer> xs;
+    for (const HaloXfer& h : *halos) {
+      const Resident& r = res_[static_cast<std::size_t>(h.dataset)];
+      const Extent a = mesh[h.dataset].alloc();
+      const index_t row = r.layout.stride[0];
+      auto at = [&](index_t r0) { return r.dev + (r0 - a.lo[0]) * row; };
+      if (rank_ > 0)
+        xs.push_back({rank_ - 1, at(h.send_left[0]), (h.send_left[1] - h.send_left[0]) * row,
+                      at(h.recv_left[0]), (h.recv_left[1] - h.recv_left[0]) * row});
+      if (rank_ + 1 < world_)
+        xs.push_back({rank_ + 1, at(h.send_right[0]), (h.send_right[1] - h.send_right[0]) * row,
+                      at(h.recv_right[0]), (h.recv_right[1] - h.recv_right[0]) * row});
+    }
+    if (!xs.empty()) DEV(ooc_comm_exchange(ctx_, OOC_Q_COMPUTE, xs.data(), static_cast<int>(xs.size())));
+    for (const ParLoop& l : chain.loops)
+      if (l.has_reduction())
+        DEV(ooc_reduce_allreduce(ctx_, OOC_Q_COMPUTE, out.reduction_slot.at(l.id),
+                                 lower_loop(l).reduce_op));
+  }
   for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
   finish_chain(chain, out.reduction_slot, pc);
+}
+
+void GpuEngine::comm_init(int rank, int world, const void* id) {
+  DEV(ooc_comm_init(ctx_, rank, world, id));
+  rank_ = rank;
+  world_ = world;
+  comm_ready_ = true;
 }
 
 double GpuEngine::reduction_value(int slot) {

@@ -20,7 +20,54 @@ GpuEngine& Runtime::engine() {
   return *gpu_;
 }
 
+Extent Runtime::window_core(const Extent& core) const {
+  if (!windowed()) return core;
+  Extent c = core;
+  c.lo[0] = std::max(core.lo[0], opts_.own_lo - opts_.ghost);
+  c.hi[0] = std::min(core.hi[0], opts_.own_hi + opts_.ghost);
+  if (c.lo[0] >= c.hi[0])
+    throw ValidationError("dataset core " + core.str() + " lies outside this rank's rows [" +
+                          std::to_string(opts_.own_lo - opts_.ghost) + "," +
+                          std::to_string(opts_.own_hi + opts_.ghost) + ")");
+  return c;
+}
+
 void Runtime::enqueue_loop(ParLoop loop) {  // runtime.cpp:5-11
+  if (windowed()) {
+    // owned rows carry the metric (so ranks sum to the global metric); reductions
+    // fold only owned rows; every other loop runs on the whole window
+    Extent owned = loop.range;
+    owned.lo[0] = std::max(owned.lo[0], opts_.own_lo);
+    owned.hi[0] = std::min(owned.hi[0], opts_.own_hi);
+    Extent run = owned;
+    if (!loop.has_reduction()) {
+      run = loop.range;
+      run.lo[0] = std::max(run.lo[0], opts_.own_lo - opts_.ghost);
+      run.hi[0] = std::min(run.hi[0], opts_.own_hi + opts_.ghost);
+      // near the window edge a loop shrinks by its own stencil reach (rows it cannot
+      // read locally); dependency_depth() <= ghost keeps the owned rows exact
+      for (const LoopArg& a : loop.args) {
+        if (a.dataset < 0 || a.dataset >= static_cast<int>(mesh_.datasets.size())) continue;
+        const Dataset& ds = mesh_[a.dataset];
+        if (access_reads(a.mode)) {
+          auto [slo, shi] = stencil_extents(a.stencil);
+          run.lo[0] = std::max(run.lo[0], ds.alloc().lo[0] - slo[0]);
+          run.hi[0] = std::min(run.hi[0], ds.alloc().hi[0] - shi[0]);
+        }
+        if (access_writes(a.mode)) {
+          run.lo[0] = std::max(run.lo[0], ds.core.lo[0]);
+          run.hi[0] = std::min(run.hi[0], ds.core.hi[0]);
+        }
+      }
+    }
+    if (run.empty() || owned.empty())
+      throw ValidationError("loop range " + loop.range.str() +
+                            " does not reach this rank's owned rows (slab too thin)");
+    loop.range = run;
+    validate_loop(mesh_, loop);
+    loop.id = next_loop_id_;
+    owned_bytes_[loop.id] = owned.size() * loop_bytes_per_point(mesh_, loop);
+  }
   validate_loop(mesh_, loop);
   loop.id = next_loop_id_++;
   const bool reduces = loop.has_reduction();
@@ -110,7 +157,8 @@ void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
     LoopMetric m;
     m.loop_id = l.id;
     m.points = l.range.size();
-    m.bytes = l.range.size() * loop_bytes_per_point(mesh_, l);
+    auto ob = owned_bytes_.find(l.id);
+    m.bytes = ob != owned_bytes_.end() ? ob->second : l.range.size() * loop_bytes_per_point(mesh_, l);
     metric_index_[l.id] = loop_metrics_.size();
     loop_metrics_.push_back(m);
   }
@@ -119,6 +167,8 @@ void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
     last_tiles_ = e.plan.tile_count;
     return;
   }
+  if (windowed() && opts_.executor == ExecutorKind::tiled_explicit)
+    throw ValidationError("the slab decomposition runs with the resident executor");
   GpuEngine& g = engine();
   GpuEngine::ChainOut out;
   if (opts_.executor == ExecutorKind::tiled_explicit) {
@@ -139,6 +189,15 @@ void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
       const PlanCache::Entry& e = plan_for(chain);
       last_tiles_ = e.plan.tile_count;
       g.run_resident(mesh_, chain, &e.plan, &e.footprints, out);
+    } else if (windowed() && g.comm_ready()) {
+      last_tiles_ = 1;
+      const index_t depth = dependency_depth(chain);
+      if (depth > opts_.ghost)
+        throw ValidationError("chain " + std::to_string(chain.chain_id) + " needs " +
+                              std::to_string(depth) + " ghost rows; the slab has " +
+                              std::to_string(opts_.ghost));
+      const std::vector<HaloXfer> halos = halo_plan(chain);
+      g.run_resident(mesh_, chain, nullptr, nullptr, out, &halos);
     } else {
       last_tiles_ = 1;
       g.run_resident(mesh_, chain, nullptr, nullptr, out);
@@ -152,6 +211,66 @@ void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
     downloaded_ += r.downloaded;
     d2d_ += r.d2d;
   }
+}
+
+// Rows of dimension 0 each dataset must be correct beyond the owned rows at the
+// start of the chain so the owned rows are exact at its end: a backward sweep like
+// the planner's (tiler.cpp:100-134) — a loop that must produce rows owned+-e reads
+// its stencil's reach beyond that.
+index_t Runtime::dependency_depth(const LoopChain& chain) const {
+  std::vector<index_t> need(mesh_.datasets.size(), 0);
+  for (std::size_t jj = chain.loops.size(); jj-- > 0;) {
+    const ParLoop& l = chain.loops[jj];
+    index_t e = 0;
+    for (const LoopArg& a : l.args)
+      if (access_writes(a.mode)) e = std::max(e, need[static_cast<std::size_t>(a.dataset)]);
+    for (const LoopArg& a : l.args) {
+      if (!access_reads(a.mode)) continue;
+      auto [lo, hi] = stencil_extents(a.stencil);
+      const index_t reach = e + std::max(-lo[0], hi[0]);
+      auto& n = need[static_cast<std::size_t>(a.dataset)];
+      n = std::max(n, reach);
+    }
+  }
+  index_t d = 0;
+  for (index_t v : need) d = std::max(d, v);
+  return d;
+}
+
+std::vector<HaloXfer> Runtime::halo_plan(const LoopChain& chain) {
+  std::vector<HaloXfer> out;
+  std::vector<char> written(mesh_.datasets.size(), 0);
+  for (const ParLoop& l : chain.loops)
+    for (const LoopArg& a : l.args)
+      if (access_writes(a.mode)) written[static_cast<std::size_t>(a.dataset)] = 1;
+  const index_t lo = opts_.own_lo, hi = opts_.own_hi;
+  const bool left = opts_.dist_rank > 0, right = opts_.dist_rank + 1 < opts_.dist_world;
+  for (std::size_t d = 0; d < written.size(); ++d) {
+    if (!written[d]) continue;  // untouched data keeps its (globally correct) values
+    const Dataset& ds = mesh_[static_cast<DatasetId>(d)];
+    const Extent a = ds.alloc();
+    const index_t band = opts_.ghost + ds.halo[0];
+    auto clip = [&](index_t r0, index_t r1, index_t* dst) {
+      dst[0] = std::max(r0, a.lo[0]);
+      dst[1] = std::max(dst[0], std::min(r1, a.hi[0]));
+    };
+    HaloXfer h{};
+    h.dataset = static_cast<DatasetId>(d);
+    if (left) {
+      clip(lo, lo + band, h.send_left);
+      clip(lo - band, lo, h.recv_left);
+    }
+    if (right) {
+      clip(hi - band, hi, h.send_right);
+      clip(hi, hi + band, h.recv_right);
+    }
+    out.push_back(h);
+  }
+  return out;
+}
+
+void Runtime::comm_init(const void* unique_id) {
+  engine().comm_init(opts_.dist_rank, opts_.dist_world, unique_id);
 }
 
 const std::vector<ChainTiming>& Runtime::chain_timings() {

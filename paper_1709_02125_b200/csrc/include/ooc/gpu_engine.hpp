@@ -52,7 +52,13 @@ class GpuEngine {
   void run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan& plan,
                     const Footprints& fp, bool cyclic, ChainOut& out);
   void run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan* plan,
-                    const Footprints* fp, ChainOut& out);
+                    const Footprints* fp, ChainOut& out,
+                    const std::vector<HaloXfer>* halos = nullptr);
+  /// Join the NCCL communicator of the slab decomposition.
+  void comm_init(int rank, int world, const void* unique_id);
+  int rank() const { return rank_; }
+  int world() const { return world_; }
+  bool comm_ready() const { return comm_ready_; }
 
   /// Resident mode: newest values of `d` are on the device (host copy stale).
   bool host_outdated(DatasetId d) const;
@@ -135,6 +141,8 @@ class GpuEngine {
   std::vector<PendingLoop> pending_loops_;
   std::vector<ooc_event*> marks_;
   Group group_;
+  int rank_ = 0, world_ = 1;
+  bool comm_ready_ = false;
 };
 
 }  // namespace ooc

@@ -90,6 +90,20 @@ struct RuntimeOptions {
   bool profile_loops = false;       // per-launch CUDA events -> per-loop device time
   int arena_fill = 0;               // debug: 0 none, 1 zero (reference behaviour), 2 NaN poison
   bool fuse = true;                 // run point-wise-dependent consecutive loops in one launch
+  // ---- slab decomposition (multi-GPU, one runtime per GPU): this rank owns rows
+  // [own_lo, own_hi) of dimension 0 and recomputes `ghost` rows on each side. Any
+  // program runs unchanged: declared datasets and loop ranges are clipped to the
+  // rank's window, ghost bands are exchanged after each chain, reductions fold the
+  // owned rows and are all-reduced. own_hi <= own_lo: no decomposition.
+  int dist_rank = 0, dist_world = 1;
+  index_t own_lo = 0, own_hi = 0;
+  index_t ghost = 0;
+};
+
+/// Ghost-band exchange of one dataset after a chain (rows of dimension 0).
+struct HaloXfer {
+  DatasetId dataset;
+  index_t send_left[2], recv_left[2], send_right[2], recv_right[2];  // [lo, hi) rows
 };
 
 struct FlushRecord {
@@ -155,12 +169,24 @@ class Runtime {
 
   DatasetId declare(const std::string& name, const Extent& core, Point halo, index_t elem_bytes,
                     double fill) {
-    return declare_dataset(mesh_, name, core, halo, elem_bytes, fill);
+    return declare_dataset(mesh_, name, window_core(core), halo, elem_bytes, fill);
   }
   DatasetId declare(const std::string& name, const Extent& core, Point halo, index_t elem_bytes,
                     const std::function<double(Point)>& fill) {
-    return declare_dataset(mesh_, name, core, halo, elem_bytes, fill);
+    return declare_dataset(mesh_, name, window_core(core), halo, elem_bytes, fill);
   }
+
+  // ---- slab decomposition
+  bool windowed() const { return opts_.own_hi > opts_.own_lo; }
+  /// The part of a global core this rank stores (owned rows +- ghost rows).
+  Extent window_core(const Extent& core) const;
+  /// Rows of dimension 0 a chain needs correct beyond the owned rows at its start
+  /// (backward sweep of the stencil extents); must not exceed `ghost`.
+  index_t dependency_depth(const LoopChain& chain) const;
+  /// Ghost-band exchanges after `chain` (datasets it writes that are not write-first).
+  std::vector<HaloXfer> halo_plan(const LoopChain& chain);
+  /// Join the NCCL communicator of the slab decomposition (128-byte unique id).
+  void comm_init(const void* unique_id);
 
   void enqueue_loop(ParLoop loop);
   std::vector<double> fetch_dataset(DatasetId d);
@@ -215,6 +241,7 @@ class Runtime {
   std::optional<LoopChain> last_chain_;
   std::vector<LoopChain> chain_log_;
   std::map<std::string, int> red_slot_;  // reduction name -> device accumulator slot
+  std::map<int, index_t> owned_bytes_;   // windowed runs: metric bytes of the owned rows
   std::vector<ChainTiming> timings_;
   std::unique_ptr<GpuEngine> gpu_;
 };

@@ -234,3 +234,19 @@ def test_specialised_medium_apps(fuse, jit_always):
         assert not compare(want, got), (app, fuse)
         dev = B.Runtime("resident").device()
         assert dev["jit_launches"] == 0  # fresh context; counters are per runtime
+
+
+def test_slab_runtime_with_nccl_single_rank():
+    """The multi-GPU path on one GPU: a 1-rank NCCL communicator, a dim-0 window with
+    ghost rows, all-reduce of the fieldsum — same bits / same reduction as plain."""
+    from paper_1709_02125_b200 import dist as D
+    n, iters = 96, 20
+    ghost = D.chain_depth("miniflow2d", iters)
+    a = B.Runtime("resident", dist=(0, 1), own=(0, n), ghost=ghost)
+    a.comm_init(D.unique_id())
+    a.run_app("miniflow2d", n, n, 0, iters)
+    b = B.Runtime("resident")
+    b.run_app("miniflow2d", n, n, 0, iters)
+    for d in range(b.num_datasets):
+        assert np.array_equal(a.fetch_dataset(d).view(np.uint64), b.fetch_dataset(d).view(np.uint64))
+    assert a.fetch_reduction("fieldsum") == b.fetch_reduction("fieldsum")
