@@ -217,10 +217,11 @@ def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, wor
     return out
 
 
-def run_e2e(B, n, steps, warmup, gpu, ratio=3.0, cyclic=True):
+def run_e2e(B, n, steps, warmup, gpu, ratio=3.0, cyclic=True, prefetch=True):
     pb = B.problem_bytes("miniflow2d", n, n)
     cap = int(pb / ratio)
-    rt = B.Runtime("explicit", capacity=cap, gpu=gpu)
+    # speculative prefetch of the next chain's first tile (reference ExecOptions::prefetch)
+    rt = B.Runtime("explicit", capacity=cap, gpu=gpu, prefetch=prefetch)
     rt.declare_app("miniflow2d", n, n)
     rt.app_iterations("miniflow2d", n, n, 0, 0, ITERS_PER_STEP * warmup, cyclic=False)
     if cyclic:
@@ -284,14 +285,17 @@ def main():
     gpu = local if world > 1 else 0
     n = args.n
     barrier(dist)
-    inc = run_incore(B, n, args.steps, args.warmup, bool(args.profile), gpu, rank=rank, world=world)
+    # at least 5 untimed warm-up chains: the first sight of every fused-kernel structure
+    # compiles its tile-shape candidates and the next launches time them
+    warm = max(args.warmup, 5)
+    inc = run_incore(B, n, args.steps, warm, bool(args.profile), gpu, rank=rank, world=world)
     dt = max_over_ranks(inc["seconds"], dist, local)
     # every rank's metric counts only its owned rows, so the job total is their sum
     value = world * inc["bytes"] / dt / 1e9
     e2e = None
     if not args.no_e2e:
         barrier(dist)
-        e2e = run_e2e(B, n, args.steps, args.warmup, gpu)
+        e2e = run_e2e(B, n, args.steps, warm, gpu)
         e2e_wall = max_over_ranks(e2e["wall"], dist, local)
     if rank != 0:
         return
@@ -305,7 +309,7 @@ def main():
     traffic, traffic_src = profiled_traffic(dom) if dom else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "warmup": warm, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference closed-form fills, proj/src/apps.cpp:61-67)",
         "config": {"workload": f"miniflow2d {n}x{n} fp64 in-core (CloverLeaf-2D analogue, "

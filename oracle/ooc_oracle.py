@@ -791,7 +791,10 @@ class Runtime:
     stale bookkeeping (explicit_exec.cpp:233-258), reductions folded in tile
     order == row-major order (explicit_exec.cpp:159-162)."""
 
-    def __init__(self, executor="reference", tiles=0, capacity=16000000000, record=False):
+    def __init__(self, executor="reference", tiles=0, capacity=16000000000, record=False,
+                 prefetch=False):
+        self.prefetch = prefetch
+        self.staged = {}  # dataset -> region staged for the next chain (DeviceState::staged)
         self.executor = executor
         self.tiles = tiles
         self.capacity = capacity
@@ -866,6 +869,7 @@ class Runtime:
         ds = self.mesh[d]
         if ds.host_stale:
             raise StaleDataError(ds.name, ds.stale_chain)
+        self.staged.pop(d, None)  # returned data may change before the next chain (:17)
         return ds.host.copy()
 
     def fetch_reduction(self, name):  # runtime.cpp:21-26
@@ -936,16 +940,39 @@ class Runtime:
 
         # uploads: tile-0 full footprint on q0, right footprints of t+1 on q1
         # (explicit_exec.cpp:174-186; write-first never travels up, :86)
+        dim = plan.tiled_dim
         for d in used:
             pd = fp.per_dataset[d]
             eb = self.mesh[d].elem_bytes
             if pd.write_first:
                 continue
-            if not pd.full[0].empty():
-                row(d, 0)[2] += pd.full[0].size() * eb
+            region = pd.full[0]
+            if not region.empty():
+                # tile-0 upload consumes a speculative stage when it only differs along
+                # the tiled dimension (explicit_exec.cpp:135-157)
+                st = self.staged.get(d)
+                common = region.intersect(st) if st is not None else Ext.none(region.ndim)
+                splits = not common.empty() and all(
+                    k == dim or (common.lo[k] == region.lo[k] and common.hi[k] == region.hi[k])
+                    for k in range(3))
+                if splits:
+                    if region.lo[dim] < common.lo[dim]:
+                        row(d, 0)[2] += region.with_dim(dim, region.lo[dim], common.lo[dim]).size() * eb
+                    if common.hi[dim] < region.hi[dim]:
+                        row(d, 0)[2] += region.with_dim(dim, common.hi[dim], region.hi[dim]).size() * eb
+                else:
+                    row(d, 0)[2] += region.size() * eb
             for t in range(1, T):
                 if not pd.right_fp[t].empty():
                     row(d, t)[2] += pd.right_fp[t].size() * eb
+        self.staged = {}  # anything not consumed is for a chain that never came (:178)
+        if self.prefetch:  # stage this chain's first tile for the next chain (:188-204, 260-271)
+            for d in used:
+                pd = fp.per_dataset[d]
+                if pd.write_first or pd.full[0].empty():
+                    continue
+                row(d, T)[2] += pd.full[0].size() * self.mesh[d].elem_bytes
+                self.staged[d] = pd.full[0]
         # device-to-device edge carry (:230-231)
         for t in range(T - 1):
             for d in used:

@@ -553,7 +553,9 @@ struct Tuning {
 };
 std::unordered_map<std::string, Tuning> g_tune;
 
-std::vector<Shape> candidates(int ndim) {
+// Candidate tile shapes; shapes whose column block (128*P) wastes more than 20 %
+// of a short contiguous row (3-D grids) are replaced by narrower ones.
+std::vector<Shape> candidates(int ndim, long long nC) {
   static const char* forced = std::getenv("OOC_JIT_SHAPE");
   if (forced && *forced) {
     Shape f;
@@ -563,7 +565,16 @@ std::vector<Shape> candidates(int ndim) {
     }
   }
   if (ndim == 1) return {{1, 4}, {1, 8}, {1, 2}};
-  return {{1, 4}, {2, 4}, {4, 2}, {1, 8}};
+  auto waste = [&](int P) {
+    const long long w = 128LL * P;
+    return static_cast<double>((nC + w - 1) / w * w) / static_cast<double>(nC) - 1.0;
+  };
+  std::vector<Shape> out;
+  for (Shape s : {Shape{1, 4}, Shape{2, 4}, Shape{4, 2}, Shape{1, 8}, Shape{2, 2}, Shape{4, 1},
+                  Shape{8, 1}})
+    if (waste(s.P) <= 0.2 && out.size() < 4) out.push_back(s);
+  if (out.empty()) out = {{4, 1}, {8, 1}, {2, 1}};
+  return out;
 }
 
 // Resolve measured candidates (non-blocking) and pick the winner once all are in.
@@ -584,6 +595,32 @@ void settle(Tuning& T) {
     if (best < 0 || T.ns_per_point[i] < T.ns_per_point[best]) best = static_cast<int>(i);
   }
   T.best = best;
+}
+
+// Generate the group's kernel for tile shape `sh` (filling `jp`) and fetch or
+// compile its binary. Caller holds g_cache_mu.
+bool compiled_for(ooc_ctx* c, const ooc_loop* Ls, int n, const Shape& sh, bool red, JitParams& jp,
+                  Compiled& k, std::string& err) {
+  std::string body;
+  int red_op = OOC_RED_NONE;
+  if (!generate(Ls, n, sh, jp, body, red_op, nullptr)) {
+    err = "group exceeds the kernel template's capacity";
+    return false;
+  }
+  const std::string key = body + "|Q" + std::to_string(sh.Q) + "P" + std::to_string(sh.P) +
+                          (red ? "|red" : "|nored");
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) {
+    k = it->second;
+    return true;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  if (!compile(body, 128, sh.Q, sh.P, red, k, err)) return false;
+  c->stats.jit_compiles++;
+  c->stats.jit_compile_ms += static_cast<long long>(
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  g_cache.emplace(key, k);
+  return true;
 }
 
 // Returns OOC_OK when launched, 1 when the group should go to the interpreter,
@@ -618,12 +655,19 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   std::lock_guard<std::mutex> lk(g_cache_mu);
   Tuning& T = g_tune[body + (red ? "|red" : "|nored")];
   if (T.cands.empty()) {
-    T.cands = candidates(Ls[0].ndim);
+    T.cands = candidates(Ls[0].ndim, jp->nC);
     T.ns_per_point.assign(T.cands.size(), -1.f);
     T.ev.resize(T.cands.size());
     T.points.assign(T.cands.size(), 0);
     T.issued.assign(T.cands.size(), 0);
     if (T.cands.size() == 1) T.best = 0;
+    // compile every candidate now (first sight of this structure, normally a
+    // warm-up chain) so later launches never wait for NVRTC
+    for (const Shape& cs : T.cands) {
+      Compiled kk;
+      std::string e2;
+      compiled_for(c, Ls, n, cs, red, *jp, kk, e2);
+    }
   }
   if (T.best < 0) settle(T);
   int pick = T.best;
@@ -644,31 +688,15 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     }
   }
   const Shape sh = T.cands[pick];
-  if (!generate(Ls, n, sh, *jp, body, red_op, nullptr)) {
-    delete jp;
-    return 1;
-  }
-  const std::string key = body + "|Q" + std::to_string(sh.Q) + "P" + std::to_string(sh.P) +
-                          (red ? "|red" : "|nored");
   Compiled k;
-  auto it = g_cache.find(key);
-  if (it != g_cache.end()) {
-    k = it->second;
-  } else {
-    std::string err;
-    auto t0 = std::chrono::steady_clock::now();
-    if (!compile(body, block, sh.Q, sh.P, red, k, err)) {
-      delete jp;
-      if (m == 2) {
-        set_error("JIT: " + err);
-        return OOC_ERR_UNSUPPORTED;
-      }
-      return 1;  // toolchain unavailable: the interpreter runs the group
+  std::string err;
+  if (!compiled_for(c, Ls, n, sh, red, *jp, k, err)) {
+    delete jp;
+    if (m == 2) {
+      set_error("JIT: " + err);
+      return OOC_ERR_UNSUPPORTED;
     }
-    c->stats.jit_compiles++;
-    c->stats.jit_compile_ms += static_cast<long long>(
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-    g_cache.emplace(key, k);
+    return 1;  // toolchain unavailable: the interpreter runs the group
   }
   const long long rows = jp->nA * ((jp->nB + k.Q - 1) / k.Q);
   const long long xblocks = (jp->nC + k.block * k.P - 1) / (k.block * k.P);

@@ -110,10 +110,13 @@ GpuEngine::~GpuEngine() {
     for (auto* e : v) ooc_event_destroy(ctx_, e);
     v.clear();
   };
-  drop(ev_h2d_);
-  drop(ev_k_);
-  drop(ev_q0_);
-  drop(ev_d2h_);
+  for (int p = 0; p < 2; ++p) {
+    drop(ev_h2d_[p]);
+    drop(ev_k_[p]);
+    drop(ev_q0_[p]);
+    drop(ev_d2h_[p]);
+    if (chain_done_[p]) ooc_event_destroy(ctx_, chain_done_[p]);
+  }
   drop(free_timing_);
   for (auto& pc : pending_chains_) {
     ooc_event_destroy(ctx_, pc.start);
@@ -257,7 +260,7 @@ void GpuEngine::ensure_pool(index_t elems) {
 }
 
 void GpuEngine::finish_chain(const LoopChain& chain, const std::map<int, int>& red,
-                             PendingChain pc) {
+                             PendingChain pc, int end_queue) {
   // reductions: one 8-byte D2H per reducing loop, on the compute queue after its kernels
   if (!red.empty()) {
     for (const auto& [loop_id, slot] : red) {
@@ -267,7 +270,7 @@ void GpuEngine::finish_chain(const LoopChain& chain, const std::map<int, int>& r
       DEV(ooc_event_record(ctx_, e, OOC_Q_COMPUTE));
     }
   }
-  DEV(ooc_event_record(ctx_, pc.end, OOC_Q_COMPUTE));
+  DEV(ooc_event_record(ctx_, pc.end, end_queue));
   pc.t.chain_id = chain.chain_id;
   pc.t.loops = static_cast<int>(chain.loops.size());
   pending_chains_.push_back(pc);
@@ -278,12 +281,16 @@ void GpuEngine::finish_chain(const LoopChain& chain, const std::map<int, int>& r
 void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan& plan,
                              const Footprints& fp, bool cyclic, ChainOut& out) {
   const int T = plan.tile_count;
+  const int dim = plan.tiled_dim;
   if (3 * fp.slot_bytes > opts_.device.capacity_bytes)  // explicit_exec.cpp:61-62
     throw CapacityError(3 * fp.slot_bytes, opts_.device.capacity_bytes);
 
   std::vector<DatasetId> used;
   for (std::size_t d = 0; d < fp.per_dataset.size(); ++d)
     if (fp.per_dataset[d].accessed) used.push_back(static_cast<DatasetId>(d));
+  auto P = [&](DatasetId d) -> const Footprints::PerDataset& {
+    return fp.per_dataset[static_cast<std::size_t>(d)];
+  };
 
   // Slot layout: every dataset gets a region able to hold its largest tile box
   // (per-dim max over tiles of full[t]); rows padded to 128 B.
@@ -291,9 +298,8 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
   std::vector<index_t> off(mesh.datasets.size(), 0);
   index_t slot_elems = 0;
   for (DatasetId d : used) {
-    const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
     Extent big = Extent::none(mesh[d].core.ndim);
-    for (const Extent& f : pd.full)
+    for (const Extent& f : P(d).full)
       if (!f.empty()) {
         if (big.empty()) {
           big = f;
@@ -312,11 +318,12 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
   }
   ensure_pool(3 * std::max<index_t>(slot_elems, 32));
 
+  const int par = static_cast<int>(chain_count_ & 1);  // this chain's event pools
+  auto E = [&](std::vector<ooc_event*>* pools, int t) { return ev(pools[par], static_cast<std::size_t>(t)); };
   auto slot_of = [&](int t) { return (slot_cursor_ + t) % 3; };
   auto arena = [&](DatasetId d, int t) {
-    const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
     return view_at(pool_ + static_cast<index_t>(slot_of(t)) * slot_elems + off[static_cast<std::size_t>(d)],
-                   pd.full[t], lay[static_cast<std::size_t>(d)].stride);
+                   P(d).full[t], lay[static_cast<std::size_t>(d)].stride);
   };
   std::map<std::pair<DatasetId, int>, AuditRow> audit;
   auto row = [&](DatasetId d, int t) -> AuditRow& {
@@ -337,22 +344,36 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     if (!opts_.arena_fill) return;
     const double v = opts_.arena_fill == 2 ? std::nan("") : 0.0;
     for (DatasetId d : used) {
-      const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
-      if (pd.full[t].empty()) continue;
+      if (P(d).full[t].empty()) continue;
       ooc_view a = arena(d, t);
       DEV(ooc_fill_box(ctx_, q, &a, v));
     }
   };
+  // A queue about to write slot s waits for the slot's previous users (kernels and
+  // edge carry on the compute queue, the download) — possibly of the previous chain.
+  auto wait_slot_free = [&](int q, int s) {
+    if (slot_q0_[s]) DEV(ooc_queue_wait(ctx_, q, slot_q0_[s]));
+    if (slot_d2h_[s]) DEV(ooc_queue_wait(ctx_, q, slot_d2h_[s]));
+  };
+  // Host read-after-write across chains: an upload of rows `r` of dataset d waits
+  // for the previous chain's download of those rows (latest intersecting tile).
+  auto wait_host_rows = [&](DatasetId d, const Extent& r) {
+    const auto& downs = prev_down_[static_cast<std::size_t>(d)];
+    int last = -1;
+    for (const auto& [box, t] : downs)
+      if (!box.intersect(r).empty()) last = std::max(last, t);
+    if (last >= 0) DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, ev(ev_d2h_[1 - par], static_cast<std::size_t>(last))));
+  };
+  if (prev_down_.size() < mesh.datasets.size()) prev_down_.resize(mesh.datasets.size());
 
   PendingChain pc;
   pc.start = fresh_timing_event();
   pc.end = fresh_timing_event();
   pc.t.tiles = T;
-  // Chain start on the compute queue; the H2D / D2H queues follow it, so nothing of
-  // this chain overtakes the previous chain's downloads (host RAW) or slot use.
   DEV(ooc_event_record(ctx_, pc.start, OOC_Q_COMPUTE));
-  DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, pc.start));
-  DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, pc.start));
+  // chains older than the previous one are fully downloaded before this one uploads
+  // (the previous chain is tracked row by row in wait_host_rows)
+  if (chain_done_[par]) DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, chain_done_[par]));
 
   // reduction accumulators (explicit_exec.cpp:159-162)
   for (const ParLoop& l : chain.loops)
@@ -367,45 +388,67 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     down_hull[static_cast<std::size_t>(d)] = Extent::none(mesh[d].alloc().ndim);
     skip_hull[static_cast<std::size_t>(d)] = Extent::none(mesh[d].alloc().ndim);
   }
+  std::vector<std::vector<std::pair<Extent, int>>> this_down(mesh.datasets.size());
   // tapes are lowered once per chain; ooc_launch_loop copies them into kernel params
   std::vector<LoweredLoop> lowered_store(chain.loops.size());
-  std::vector<const LoweredLoop*> lowered(chain.loops.size());
-  for (std::size_t j = 0; j < chain.loops.size(); ++j) {
-    lowered_store[j] = lower_loop(chain.loops[j]);
-    lowered[j] = &lowered_store[j];
-  }
+  for (std::size_t j = 0; j < chain.loops.size(); ++j) lowered_store[j] = lower_loop(chain.loops[j]);
   std::vector<ooc_view> hviews(mesh.datasets.size());
   for (DatasetId d : used) hviews[static_cast<std::size_t>(d)] = host_view(mesh[d]);
 
   for (int t = 0; t < T; ++t) {
     if (t == 0) {
+      wait_slot_free(OOC_Q_H2D, slot_of(0));
       fill_tile(0, OOC_Q_H2D);
       for (DatasetId d : used) {
-        const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+        const auto& pd = P(d);
         if (pd.write_first || pd.full[0].empty()) continue;
-        copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), pd.full[0]);
-        row(d, 0).uploaded += pd.full[0].size() * mesh[d].elem_bytes;
+        const Extent& region = pd.full[0];
+        const index_t eb = mesh[d].elem_bytes;
+        // consume what the previous chain staged speculatively when it only differs
+        // along the tiled dimension (explicit_exec.cpp:135-157)
+        auto st = staged_.find(d);
+        bool splits = false;
+        Extent common;
+        if (st != staged_.end()) {
+          common = region.intersect(st->second.region);
+          splits = !common.empty();
+          for (int k = 0; k < 3 && splits; ++k)
+            if (k != dim && (common.lo[k] != region.lo[k] || common.hi[k] != region.hi[k])) splits = false;
+        }
+        if (splits) {
+          copy(OOC_Q_H2D, OOC_COPY_D2D, st->second.view, arena(d, 0), common);
+          Extent lo_part = region.with_dim(dim, region.lo[dim], common.lo[dim]);
+          Extent hi_part = region.with_dim(dim, common.hi[dim], region.hi[dim]);
+          for (const Extent& part : {lo_part, hi_part})
+            if (part.lo[dim] < part.hi[dim]) {
+              wait_host_rows(d, part);
+              copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), part);
+              row(d, 0).uploaded += part.size() * eb;
+            }
+        } else {
+          wait_host_rows(d, region);
+          copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), region);
+          row(d, 0).uploaded += region.size() * eb;
+        }
       }
-      DEV(ooc_event_record(ctx_, ev(ev_h2d_, 0), OOC_Q_H2D));
+      staged_.clear();  // anything not consumed is for a chain that never came (:178)
+      DEV(ooc_event_record(ctx_, E(ev_h2d_, 0), OOC_Q_H2D));
     }
     if (t + 1 < T) {
-      if (t >= 2) {  // slot(t+1) == slot(t-2): its readers must be done
-        DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, ev(ev_q0_, t - 2)));
-        DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, ev(ev_d2h_, t - 2)));
-      }
+      wait_slot_free(OOC_Q_H2D, slot_of(t + 1));
       fill_tile(t + 1, OOC_Q_H2D);
       for (DatasetId d : used) {
-        const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+        const auto& pd = P(d);
         if (pd.write_first || pd.right_fp[t + 1].empty()) continue;
-        copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, t + 1),
-             pd.right_fp[t + 1]);
+        wait_host_rows(d, pd.right_fp[t + 1]);
+        copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, t + 1), pd.right_fp[t + 1]);
         row(d, t + 1).uploaded += pd.right_fp[t + 1].size() * mesh[d].elem_bytes;
       }
-      DEV(ooc_event_record(ctx_, ev(ev_h2d_, t + 1), OOC_Q_H2D));
+      DEV(ooc_event_record(ctx_, E(ev_h2d_, t + 1), OOC_Q_H2D));
     }
 
     // kernels of tile t wait for tile t's upload (missing from the reference model)
-    DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, ev(ev_h2d_, t)));
+    DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, E(ev_h2d_, t)));
     for (std::size_t j = 0; j < chain.loops.size(); ++j) {
       const ParLoop& loop = chain.loops[j];
       const Extent sub = plan.subrange(static_cast<int>(j), t);
@@ -417,26 +460,28 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
         if (access_writes(a.mode)) mesh[a.dataset].ever_written = true;
       }
       auto rs = out.reduction_slot.find(loop.id);
-      launch(OOC_Q_COMPUTE, loop, *lowered[j], sub, views,
+      launch(OOC_Q_COMPUTE, loop, lowered_store[j], sub, views,
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
     flush_group(OOC_Q_COMPUTE);
-    DEV(ooc_event_record(ctx_, ev(ev_k_, t), OOC_Q_COMPUTE));
+    DEV(ooc_event_record(ctx_, E(ev_k_, t), OOC_Q_COMPUTE));
 
     if (t + 1 < T) {
-      if (t >= 2) DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, ev(ev_d2h_, t - 2)));
+      // the edge carry writes slot(t+1): its previous download must be done
+      if (slot_d2h_[slot_of(t + 1)]) DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, slot_d2h_[slot_of(t + 1)]));
       for (DatasetId d : used) {
-        const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+        const auto& pd = P(d);
         if (pd.right_edge[t].empty()) continue;
         copy(OOC_Q_COMPUTE, OOC_COPY_D2D, arena(d, t), arena(d, t + 1), pd.right_edge[t]);
         row(d, t + 1).d2d += pd.right_edge[t].size() * mesh[d].elem_bytes;
       }
     }
-    DEV(ooc_event_record(ctx_, ev(ev_q0_, t), OOC_Q_COMPUTE));
+    DEV(ooc_event_record(ctx_, E(ev_q0_, t), OOC_Q_COMPUTE));
+    slot_q0_[slot_of(t)] = E(ev_q0_, t);
 
-    DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, ev(ev_k_, t)));
+    DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, E(ev_k_, t)));
     for (DatasetId d : used) {
-      const auto& pd = fp.per_dataset[static_cast<std::size_t>(d)];
+      const auto& pd = P(d);
       if (!pd.written_any) continue;  // read-only data never travels back
       if (cyclic && pd.write_first) {  // cyclic: temporaries are dropped
         skip_hull[static_cast<std::size_t>(d)] = skip_hull[static_cast<std::size_t>(d)].hull(pd.left_fp[t]);
@@ -445,12 +490,43 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
       if (!pd.left_fp[t].empty()) {
         copy(OOC_Q_D2H, OOC_COPY_D2H, arena(d, t), hviews[static_cast<std::size_t>(d)], pd.left_fp[t]);
         row(d, t).downloaded += pd.left_fp[t].size() * mesh[d].elem_bytes;
+        this_down[static_cast<std::size_t>(d)].push_back({pd.left_fp[t], t});
       }
       down_hull[static_cast<std::size_t>(d)] = down_hull[static_cast<std::size_t>(d)].hull(pd.left_fp[t]);
     }
-    DEV(ooc_event_record(ctx_, ev(ev_d2h_, t), OOC_Q_D2H));
+    DEV(ooc_event_record(ctx_, E(ev_d2h_, t), OOC_Q_D2H));
+    slot_d2h_[slot_of(t)] = E(ev_d2h_, t);
   }
-  DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, ev(ev_d2h_, T - 1)));
+
+  // speculative upload of this chain's first tile for the next chain
+  // (explicit_exec.cpp:188-204, 260-271): issued once every download that writes
+  // those host rows has landed, into a staging region outside the three slots
+  if (opts_.prefetch) {
+    index_t need = 0;
+    std::vector<std::pair<DatasetId, BoxLayout>> st_lay;
+    for (DatasetId d : used) {
+      const auto& pd = P(d);
+      if (pd.write_first || pd.full[0].empty()) continue;
+      st_lay.push_back({d, padded_layout(pd.full[0])});
+      need += (st_lay.back().second.elems + 31) / 32 * 32;
+    }
+    ensure_staging(need);
+    index_t at = 0;
+    for (const auto& [d, L] : st_lay) {
+      const Extent& region = P(d).full[0];
+      int last = -1;
+      for (const auto& [box, t] : this_down[static_cast<std::size_t>(d)])
+        if (!box.intersect(region).empty()) last = std::max(last, t);
+      if (last >= 0) DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, E(ev_d2h_, last)));
+      Staged s;
+      s.region = region;
+      s.view = view_at(staging_ + at, region, L.stride);
+      at += (L.elems + 31) / 32 * 32;
+      copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], s.view, region);
+      row(d, T).uploaded += region.size() * mesh[d].elem_bytes;
+      staged_[d] = s;
+    }
+  }
 
   // host staleness bookkeeping (explicit_exec.cpp:245-258)
   for (DatasetId d : used) {
@@ -468,6 +544,13 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     }
   }
   slot_cursor_ = (slot_cursor_ + T) % 3;
+  for (std::size_t d = 0; d < prev_down_.size(); ++d)
+    prev_down_[d] = d < this_down.size() ? std::move(this_down[d]) : std::vector<std::pair<Extent, int>>{};
+  // everything of this chain has landed in host memory once this event completes
+  ooc_event*& done = chain_done_[par];
+  if (!done) DEV(ooc_event_create(ctx_, 0, &done));
+  DEV(ooc_event_record(ctx_, done, OOC_Q_D2H));
+  ++chain_count_;
 
   for (auto& [k, r] : audit) {
     out.audit.push_back(r);
@@ -476,8 +559,26 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     pc.t.d2d += r.d2d;
   }
   for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
-  finish_chain(chain, out.reduction_slot, pc);
+  // the chain ends when its last download has landed; the compute queue does not
+  // wait for it, so the next chain's first tiles overlap this chain's last downloads
+  DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, E(ev_q0_, T - 1)));
+  finish_chain(chain, out.reduction_slot, pc, OOC_Q_D2H);
 }
+
+void GpuEngine::ensure_staging(index_t elems) {
+  if (elems <= staging_elems_) return;
+  if (staging_) {
+    DEV(ooc_ctx_sync(ctx_));
+    DEV(ooc_mem_free(ctx_, staging_));
+    staging_ = nullptr;
+  }
+  void* p = nullptr;
+  DEV(ooc_mem_alloc(ctx_, static_cast<std::size_t>(elems) * sizeof(double), &p));
+  staging_ = static_cast<double*>(p);
+  staging_elems_ = elems;
+}
+
+void GpuEngine::invalidate_staged(DatasetId d) { staged_.erase(d); }
 
 // ---------------------------------------------------------------- resident executor
 

@@ -97,6 +97,7 @@ void Runtime::fetch_dataset_into(DatasetId d, double* dst, std::size_t n) {
       gpu_->download_resident(mesh_, d);
     else
       gpu_->sync();  // streamed downloads of earlier chains must have landed
+    gpu_->invalidate_staged(d);  // runtime.cpp:17
   }
   std::copy(ds.host.begin(), ds.host.end(), dst);
 }

@@ -64,6 +64,9 @@ class GpuEngine {
   bool host_outdated(DatasetId d) const;
   void download_resident(Mesh& mesh, DatasetId d);
   void forget_resident(DatasetId d);
+  /// A fetched dataset's staged first tile may be modified before the next chain
+  /// (reference Runtime::fetch_dataset, proj/src/runtime.cpp:17).
+  void invalidate_staged(DatasetId d);
   /// Block until the reduction written to `slot` has reached host memory.
   double reduction_value(int slot);
   void sync();
@@ -120,7 +123,8 @@ class GpuEngine {
   index_t loop_bytes_per_point_views(const ParLoop& loop) const;
   void ensure_pool(index_t elems);
   void ensure_resident(Mesh& mesh, DatasetId d);
-  void finish_chain(const LoopChain& chain, const std::map<int, int>& red, PendingChain pc);
+  void finish_chain(const LoopChain& chain, const std::map<int, int>& red, PendingChain pc,
+                    int end_queue = OOC_Q_COMPUTE);
 
   RuntimeOptions opts_;
   ooc_ctx* ctx_ = nullptr;
@@ -129,7 +133,25 @@ class GpuEngine {
   double* pool_ = nullptr;
   index_t pool_elems_ = 0;
   int slot_cursor_ = 0;
-  std::vector<ooc_event*> ev_h2d_, ev_k_, ev_q0_, ev_d2h_;
+  // per-tile events, double-buffered by chain parity so the next chain can wait on
+  // the previous chain's downloads while recording its own
+  std::vector<ooc_event*> ev_h2d_[2], ev_k_[2], ev_q0_[2], ev_d2h_[2];
+  ooc_event* chain_done_[2] = {nullptr, nullptr};
+  long long chain_count_ = 0;
+  // last users of each slot (may belong to the previous chain)
+  ooc_event* slot_q0_[3] = {nullptr, nullptr, nullptr};
+  ooc_event* slot_d2h_[3] = {nullptr, nullptr, nullptr};
+  // host rows the previous chain downloaded, per dataset: (box, tile)
+  std::vector<std::vector<std::pair<Extent, int>>> prev_down_;
+  // speculative first-tile stages for the next chain (reference DeviceState::staged)
+  struct Staged {
+    Extent region;
+    ooc_view view;
+  };
+  std::map<DatasetId, Staged> staged_;
+  double* staging_ = nullptr;
+  index_t staging_elems_ = 0;
+  void ensure_staging(index_t elems);
   // resident buffers by dataset id
   std::vector<Resident> res_;
   // reductions: device accumulator slot -> pinned host mirror

@@ -20,7 +20,7 @@ WORK = {
 }
 
 
-def run(app_key, executor, steps=3, warmup=2, **kw):
+def run(app_key, executor, steps=3, warmup=5, **kw):
     app, nx, ny, nz, per, span = WORK[app_key]
     rt = B.Runtime(executor, **kw)
     t0 = time.perf_counter()

@@ -40,12 +40,15 @@ def reduction_names(prog):
                    if op["op"] == "loop" and "reduction" in op.get("kernel", {})})
 
 
-def run_record(prog, executor, tiles=0, capacity=1 << 40, cyclic=False, extra=False):
+def run_record(prog, executor, tiles=0, capacity=1 << 40, cyclic=False, extra=False,
+               prefetch=False):
     pr = json.loads(json.dumps(prog))
     if cyclic:
         pr["ops"].insert(0, {"op": "cyclic", "on": True})
-    ref = refo.RefRuntime(executor, tiles=tiles, capacity=capacity, record=True)
+    ref = refo.RefRuntime(executor, tiles=tiles, capacity=capacity, record=True, prefetch=prefetch)
     rec = {"executor": executor, "tiles": tiles, "capacity": capacity, "cyclic": cyclic}
+    if prefetch:
+        rec["prefetch"] = True
     try:
         ref.load_program(pr)
     except refo.RefError as e:
@@ -125,6 +128,7 @@ def main():
         for T in (1, 3):
             for cyc in (False, True):
                 runs.append(run_record(prog, "explicit", tiles=T, cyclic=cyc))
+        runs.append(run_record(prog, "explicit", tiles=3, prefetch=True))
         cases.append({"seed": seed, "kwargs": RANDOM_KW, "program_sha": sha(prog), "runs": runs,
                       "plans": plan_records(prog)})
     with open(os.path.join(HERE, "random_programs.json"), "w") as f:
@@ -138,7 +142,8 @@ def main():
         runs = [run_record(prog, "reference"),
                 run_record(prog, "explicit", tiles=3, extra=True),
                 run_record(prog, "explicit", capacity=pb // 3, extra=True),
-                run_record(prog, "explicit", capacity=pb // 3, cyclic=True, extra=True)]
+                run_record(prog, "explicit", capacity=pb // 3, cyclic=True, extra=True),
+                run_record(prog, "explicit", tiles=3, prefetch=True)]
         apps.append({"app": name, "case": [name, dict(APP_CASES[len(apps)][1])],
                      "program_sha": sha(prog), "problem_bytes": pb, "runs": runs})
     with open(os.path.join(HERE, "apps.json"), "w") as f:

@@ -29,8 +29,8 @@ def with_cyclic(prog, cyclic):
     return pr
 
 
-def oracle_record(prog, executor, tiles=0, capacity=1 << 40, cyclic=False):
-    rt = O.Runtime(executor, tiles=tiles, capacity=capacity, record=True)
+def oracle_record(prog, executor, tiles=0, capacity=1 << 40, cyclic=False, prefetch=False):
+    rt = O.Runtime(executor, tiles=tiles, capacity=capacity, record=True, prefetch=prefetch)
     rec = {}
     try:
         O.load_program(rt, with_cyclic(prog, cyclic))

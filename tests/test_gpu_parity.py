@@ -22,7 +22,7 @@ def test_random_programs_vs_reference_golden(golden_random):
         prog = P.random_program(case["seed"], **case["kwargs"])
         for want in case["runs"]:
             got = product_record(prog, EXEC_OF[want["executor"]], want["tiles"], want["capacity"],
-                                 want["cyclic"])
+                                 want["cyclic"], prefetch=want.get("prefetch", False))
             got.pop("_rt", None)
             # the reference executor moves no bytes; only explicit runs carry an audit
             diff = compare(want, got, check_audit=want["executor"] == "explicit",
@@ -40,7 +40,7 @@ def test_apps_vs_reference_golden(golden_apps):
         prog = P.app_program(name, kw.pop("nx"), kw.pop("ny"), kw.pop("nz", 0), **kw)
         for want in case["runs"]:
             got = product_record(prog, EXEC_OF[want["executor"]], want["tiles"], want["capacity"],
-                                 want["cyclic"])
+                                 want["cyclic"], prefetch=want.get("prefetch", False))
             got.pop("_rt", None)
             diff = compare(want, got, check_audit=want["executor"] == "explicit",
                            check_totals=want["executor"] == "explicit")
@@ -199,7 +199,7 @@ def test_specialised_kernels_vs_golden(golden_random, golden_apps, jit_always):
         prog = P.random_program(case["seed"], **case["kwargs"])
         for want in case["runs"]:
             got = product_record(prog, EXEC_OF[want["executor"]], want["tiles"], want["capacity"],
-                                 want["cyclic"])
+                                 want["cyclic"], prefetch=want.get("prefetch", False))
             got.pop("_rt", None)
             diff = compare(want, got, check_audit=want["executor"] == "explicit",
                            check_totals=want["executor"] == "explicit")
@@ -211,7 +211,7 @@ def test_specialised_kernels_vs_golden(golden_random, golden_apps, jit_always):
         prog = P.app_program(name, kw.pop("nx"), kw.pop("ny"), kw.pop("nz", 0), **kw)
         for want in case["runs"][:2]:
             got = product_record(prog, EXEC_OF[want["executor"]], want["tiles"], want["capacity"],
-                                 want["cyclic"])
+                                 want["cyclic"], prefetch=want.get("prefetch", False))
             got.pop("_rt", None)
             diff = compare(want, got, check_audit=want["executor"] == "explicit",
                            check_totals=want["executor"] == "explicit")

@@ -19,7 +19,7 @@ def test_random_programs_match_reference_golden(golden_random):
         assert sha(prog) == case["program_sha"], "random program generator drifted"
         for want in case["runs"]:
             got = oracle_record(prog, want["executor"], want["tiles"], want["capacity"],
-                                want["cyclic"])
+                                want["cyclic"], prefetch=want.get("prefetch", False))
             diff = compare(want, got, exact_reductions=True)
             if diff:
                 bad.append((case["seed"], want["executor"], want["tiles"], want["cyclic"], diff))
@@ -58,7 +58,7 @@ def test_apps_match_reference_golden(golden_apps):
         assert sha(prog) == case["program_sha"]
         for want in case["runs"]:
             got = oracle_record(prog, want["executor"], want["tiles"], want["capacity"],
-                                want["cyclic"])
+                                want["cyclic"], prefetch=want.get("prefetch", False))
             diff = compare(want, got, exact_reductions=True)
             if diff:
                 bad.append((name, want["executor"], want["tiles"], want["cyclic"], diff))
