@@ -73,6 +73,7 @@ typedef struct {
    * [own_lo, own_hi) of dimension 0 and recomputes `ghost` rows each side */
   int dist_rank, dist_world;
   long long own_lo, own_hi, ghost;
+  int timeline;              /* 1: record a real event timeline (CUDA events per command) */
 } ooc_runtime_options;
 
 void ooc_rt_default_options(ooc_runtime_options* o);
@@ -133,6 +134,17 @@ const char* ooc_rt_device_json(ooc_runtime* rt);
 /* profile_loops runs: every launch since the last call as [first_loop, nloops, bytes, s]. */
 const char* ooc_rt_launch_log_json(ooc_runtime* rt);
 int ooc_rt_num_chains(ooc_runtime* rt);
+/* CSV exports in the reference's schemas; NULL on error (see ooc_rt_last_error).
+ * report: proj/src/metrics.cpp:46-60 (report_csv_header + report_csv_row)
+ * loops:  proj/src/metrics.cpp:62-70 (loops_csv; with timeline=1 loop times come
+ *         from the real timeline, attributed as attribute_loop_times, metrics.cpp:14-32)
+ * audit:  proj/src/metrics.cpp:72-79 (audit_csv)
+ * timeline: proj/src/command.cpp:160-168 (timeline_csv; rows are measured CUDA
+ *         events, seconds from the first recorded command, not a simulation) */
+const char* ooc_rt_report_csv(ooc_runtime* rt, const char* app, const char* size, int iters);
+const char* ooc_rt_loops_csv(ooc_runtime* rt);
+const char* ooc_rt_audit_csv(ooc_runtime* rt);
+const char* ooc_rt_timeline_csv(ooc_runtime* rt);
 /* Full plan of recorded chain `chain`: tiles>0 plans with that count, else
  * choose_tile_count(budget). `dump` = 1 returns the reference plan_dump_json
  * schema instead of the full footprint record. */

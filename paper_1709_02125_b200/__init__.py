@@ -100,7 +100,7 @@ class Runtime:
 
     def __init__(self, executor="resident", tiles=0, capacity=16_000_000_000, resident_budget=0,
                  prefetch=False, record=False, gpu=0, profile=False, arena_fill=0, tiled_dim=0,
-                 fuse=True, dist=(0, 1), own=None, ghost=0):
+                 fuse=True, dist=(0, 1), own=None, ghost=0, timeline=False):
         L = _native.lib()
         o = _native.Options()
         L.ooc_rt_default_options(ctypes.byref(o))
@@ -119,6 +119,7 @@ class Runtime:
         if own is not None:
             o.own_lo, o.own_hi = int(own[0]), int(own[1])
         o.ghost = int(ghost)
+        o.timeline = int(timeline)
         h = ctypes.c_void_p()
         _check(L.ooc_rt_create(ctypes.byref(o), ctypes.byref(h)))
         self._h = h
@@ -284,6 +285,29 @@ class Runtime:
 
     def report(self):
         return self._json(_native.lib().ooc_rt_report_json)
+
+    def _csv(self, fn, *args):
+        s = fn(self._h, *args)
+        if s is None:
+            msg = _native.lib().ooc_rt_last_error().decode()
+            raise {"ValidationError": ValidationError, "InfeasibleError": InfeasibleError,
+                   "CapacityError": CapacityError, "DeviceError": DeviceError,
+                   "StaleDataError": StaleDataError}.get(msg.split(":", 1)[0], OocError)(msg)
+        return s.decode()
+
+    def report_csv(self, app="", size="", iters=0):
+        """proj/src/metrics.cpp:46-60 schema (#oocstencil-report-v1)."""
+        return self._csv(_native.lib().ooc_rt_report_csv, app.encode(), str(size).encode(), int(iters))
+
+    def loops_csv(self):
+        return self._csv(_native.lib().ooc_rt_loops_csv)
+
+    def audit_csv(self):
+        return self._csv(_native.lib().ooc_rt_audit_csv)
+
+    def timeline_csv(self):
+        """Measured command timeline (timeline=True runs), proj/src/command.cpp:160-168 schema."""
+        return self._csv(_native.lib().ooc_rt_timeline_csv)
 
     def chain_timings(self):
         return self._json(_native.lib().ooc_rt_chain_timings_json)

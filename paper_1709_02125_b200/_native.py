@@ -35,6 +35,7 @@ class Options(ctypes.Structure):
         ("own_lo", ctypes.c_longlong),
         ("own_hi", ctypes.c_longlong),
         ("ghost", ctypes.c_longlong),
+        ("timeline", ctypes.c_int),
     ]
 
 
@@ -81,6 +82,10 @@ def lib():
         "ooc_rt_flush_log_json": (cp, [vp]),
         "ooc_rt_audit_json": (cp, [vp]),
         "ooc_rt_report_json": (cp, [vp]),
+        "ooc_rt_report_csv": (cp, [vp, cp, cp, ctypes.c_int]),
+        "ooc_rt_loops_csv": (cp, [vp]),
+        "ooc_rt_audit_csv": (cp, [vp]),
+        "ooc_rt_timeline_csv": (cp, [vp]),
         "ooc_rt_chain_timings_json": (cp, [vp]),
         "ooc_rt_loop_metrics_json": (cp, [vp]),
         "ooc_rt_device_json": (cp, [vp]),

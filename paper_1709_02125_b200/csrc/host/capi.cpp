@@ -143,6 +143,7 @@ int ooc_rt_create(const ooc_runtime_options* o, ooc_runtime** out) {
     ro.own_lo = o->own_lo;
     ro.own_hi = o->own_hi;
     ro.ghost = o->ghost;
+    ro.timeline = o->timeline != 0;
     auto* h = new ooc_runtime;
     h->rt = std::make_unique<ooc::Runtime>(ro);
     *out = h;
@@ -329,6 +330,30 @@ const char* ooc_rt_audit_json(ooc_runtime* h) {
     w.begin_array().value(r.dataset).value(r.tile).value(r.uploaded).value(r.downloaded).value(r.d2d).end_array();
   w.end_array();
   return out_str(w.str());
+}
+
+const char* ooc_rt_report_csv(ooc_runtime* h, const char* app, const char* size, int iters) {
+  std::string s;
+  int rc = guard([&] { s = h->rt->report_csv(app ? app : "", size ? size : "", iters); });
+  return rc ? nullptr : out_str(s);
+}
+
+const char* ooc_rt_loops_csv(ooc_runtime* h) {
+  std::string s;
+  int rc = guard([&] { s = h->rt->loops_csv(); });
+  return rc ? nullptr : out_str(s);
+}
+
+const char* ooc_rt_audit_csv(ooc_runtime* h) {
+  std::string s;
+  int rc = guard([&] { s = h->rt->audit_csv(); });
+  return rc ? nullptr : out_str(s);
+}
+
+const char* ooc_rt_timeline_csv(ooc_runtime* h) {
+  std::string s;
+  int rc = guard([&] { s = h->rt->timeline_csv(); });
+  return rc ? nullptr : out_str(s);
 }
 
 const char* ooc_rt_report_json(ooc_runtime* h) {

@@ -195,7 +195,17 @@ bool GpuEngine::fusable(const ParLoop& b) const {
 
 void GpuEngine::flush_group(int queue) {
   if (group_.calls.empty()) return;
-  if (opts_.profile_loops) {
+  if (opts_.timeline) {
+    std::vector<std::pair<int, index_t>> loops;
+    index_t total = 0;
+    for (std::size_t i = 0; i < group_.loops.size(); ++i) {
+      loops.push_back({group_.loops[i]->id, group_.bytes[i]});
+      total += group_.bytes[i];
+    }
+    timeline_cmd(3, queue, total, -1, cur_tile_, std::move(loops), [&] {
+      DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
+    });
+  } else if (opts_.profile_loops) {
     PendingLoop pl{{}, 0, fresh_timing_event(), fresh_timing_event()};
     double total = 0;
     for (index_t b : group_.bytes) total += static_cast<double>(b);
@@ -332,13 +342,16 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     r.tile = t;
     return r;
   };
-  auto copy = [&](int q, int kind, const ooc_view& s, const ooc_view& dv, const Extent& region) {
+  auto copy = [&](int q, int kind, const ooc_view& s, const ooc_view& dv, const Extent& region,
+                  DatasetId d, int tile) {
     int64_t lo[3], hi[3];
     for (int k = 0; k < 3; ++k) {
       lo[k] = region.lo[k];
       hi[k] = region.hi[k];
     }
-    DEV(ooc_copy_box(ctx_, q, kind, &s, &dv, lo, hi));
+    const int cmd = kind == OOC_COPY_H2D ? 0 : kind == OOC_COPY_D2H ? 1 : 2;  // CmdKind order
+    timeline_cmd(cmd, q, region.size() * mesh[d].elem_bytes, d, tile, {},
+                 [&] { DEV(ooc_copy_box(ctx_, q, kind, &s, &dv, lo, hi)); });
   };
   auto fill_tile = [&](int t, int q) {
     if (!opts_.arena_fill) return;
@@ -416,18 +429,18 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
             if (k != dim && (common.lo[k] != region.lo[k] || common.hi[k] != region.hi[k])) splits = false;
         }
         if (splits) {
-          copy(OOC_Q_H2D, OOC_COPY_D2D, st->second.view, arena(d, 0), common);
+          copy(OOC_Q_H2D, OOC_COPY_D2D, st->second.view, arena(d, 0), common, d, 0);
           Extent lo_part = region.with_dim(dim, region.lo[dim], common.lo[dim]);
           Extent hi_part = region.with_dim(dim, common.hi[dim], region.hi[dim]);
           for (const Extent& part : {lo_part, hi_part})
             if (part.lo[dim] < part.hi[dim]) {
               wait_host_rows(d, part);
-              copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), part);
+              copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), part, d, 0);
               row(d, 0).uploaded += part.size() * eb;
             }
         } else {
           wait_host_rows(d, region);
-          copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), region);
+          copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), region, d, 0);
           row(d, 0).uploaded += region.size() * eb;
         }
       }
@@ -441,12 +454,14 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
         const auto& pd = P(d);
         if (pd.write_first || pd.right_fp[t + 1].empty()) continue;
         wait_host_rows(d, pd.right_fp[t + 1]);
-        copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, t + 1), pd.right_fp[t + 1]);
+        copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, t + 1), pd.right_fp[t + 1], d,
+             t + 1);
         row(d, t + 1).uploaded += pd.right_fp[t + 1].size() * mesh[d].elem_bytes;
       }
       DEV(ooc_event_record(ctx_, E(ev_h2d_, t + 1), OOC_Q_H2D));
     }
 
+    cur_tile_ = t;
     // kernels of tile t wait for tile t's upload (missing from the reference model)
     DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, E(ev_h2d_, t)));
     for (std::size_t j = 0; j < chain.loops.size(); ++j) {
@@ -472,7 +487,7 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
       for (DatasetId d : used) {
         const auto& pd = P(d);
         if (pd.right_edge[t].empty()) continue;
-        copy(OOC_Q_COMPUTE, OOC_COPY_D2D, arena(d, t), arena(d, t + 1), pd.right_edge[t]);
+        copy(OOC_Q_COMPUTE, OOC_COPY_D2D, arena(d, t), arena(d, t + 1), pd.right_edge[t], d, t + 1);
         row(d, t + 1).d2d += pd.right_edge[t].size() * mesh[d].elem_bytes;
       }
     }
@@ -488,7 +503,7 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
         continue;
       }
       if (!pd.left_fp[t].empty()) {
-        copy(OOC_Q_D2H, OOC_COPY_D2H, arena(d, t), hviews[static_cast<std::size_t>(d)], pd.left_fp[t]);
+        copy(OOC_Q_D2H, OOC_COPY_D2H, arena(d, t), hviews[static_cast<std::size_t>(d)], pd.left_fp[t], d, t);
         row(d, t).downloaded += pd.left_fp[t].size() * mesh[d].elem_bytes;
         this_down[static_cast<std::size_t>(d)].push_back({pd.left_fp[t], t});
       }
@@ -522,7 +537,7 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
       s.region = region;
       s.view = view_at(staging_ + at, region, L.stride);
       at += (L.elems + 31) / 32 * 32;
-      copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], s.view, region);
+      copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], s.view, region, d, T);
       row(d, T).uploaded += region.size() * mesh[d].elem_bytes;
       staged_[d] = s;
     }
@@ -563,6 +578,56 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
   // wait for it, so the next chain's first tiles overlap this chain's last downloads
   DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, E(ev_q0_, T - 1)));
   finish_chain(chain, out.reduction_slot, pc, OOC_Q_D2H);
+}
+
+// Real event timeline (replaces the reference's simulated one, command.cpp:35-126):
+// every command bracketed by timing events on its queue; fused launches are split
+// into per-loop sub-intervals in proportion to their metric bytes.
+void GpuEngine::timeline_cmd(int kind, int queue, index_t bytes, DatasetId d, int tile,
+                             std::vector<std::pair<int, index_t>> loops,
+                             const std::function<void()>& issue) {
+  if (!opts_.timeline) {
+    issue();
+    return;
+  }
+  if (!tl_base_) {
+    DEV(ooc_event_create(ctx_, 1, &tl_base_));
+    DEV(ooc_event_record(ctx_, tl_base_, OOC_Q_COMPUTE));
+    tl_host0_ = std::chrono::steady_clock::now();
+  }
+  TLPending p{kind, queue, bytes, d, tile, std::move(loops), 0.0, fresh_timing_event(),
+              fresh_timing_event()};
+  p.issue = std::chrono::duration<double>(std::chrono::steady_clock::now() - tl_host0_).count();
+  DEV(ooc_event_record(ctx_, p.a, queue));
+  issue();
+  DEV(ooc_event_record(ctx_, p.b, queue));
+  tl_pending_.push_back(std::move(p));
+}
+
+std::vector<TimelineRow> GpuEngine::take_timeline() {
+  std::vector<TimelineRow> out;
+  for (TLPending& p : tl_pending_) {
+    DEV(ooc_event_sync(ctx_, p.b));
+    float a = 0.f, b = 0.f;
+    DEV(ooc_event_elapsed_ms(tl_base_, p.a, &a));
+    DEV(ooc_event_elapsed_ms(tl_base_, p.b, &b));
+    const double s = a * 1e-3, e = b * 1e-3;
+    if (p.loops.empty()) {
+      out.push_back({next_cmd_++, p.kind, p.queue, p.bytes, p.issue, s, e, p.dataset, p.tile, -1});
+    } else {
+      double t = s;
+      for (const auto& [loop, lb] : p.loops) {
+        const double span = p.bytes > 0 ? (e - s) * static_cast<double>(lb) / p.bytes
+                                        : (e - s) / p.loops.size();
+        out.push_back({next_cmd_++, p.kind, p.queue, lb, p.issue, t, t + span, -1, p.tile, loop});
+        t += span;
+      }
+    }
+    recycle(p.a);
+    recycle(p.b);
+  }
+  tl_pending_.clear();
+  return out;
 }
 
 void GpuEngine::ensure_staging(index_t elems) {
@@ -607,7 +672,9 @@ void GpuEngine::ensure_resident(Mesh& mesh, DatasetId d) {
   if (!r.dev_valid) {
     ooc_view hv = host_view(ds);
     ooc_view dv = view_at(r.dev, ds.alloc(), r.layout.stride);
-    DEV(ooc_copy_box(ctx_, OOC_Q_COMPUTE, OOC_COPY_H2D, &hv, &dv, hv.lo, hv.hi));
+    timeline_cmd(0, OOC_Q_COMPUTE, ds.alloc().size() * ds.elem_bytes, d, 0, {}, [&] {
+      DEV(ooc_copy_box(ctx_, OOC_Q_COMPUTE, OOC_COPY_H2D, &hv, &dv, hv.lo, hv.hi));
+    });
     r.dev_valid = true;
     r.host_outdated = false;
   }
@@ -683,6 +750,8 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
       const Extent sub = plan ? plan->subrange(static_cast<int>(j), t) : l.range;
       if (sub.empty()) continue;
       auto rs = out.reduction_slot.find(l.id);
+      if (!fusable(l)) flush_group(OOC_Q_COMPUTE);
+      cur_tile_ = t;
       launch(OOC_Q_COMPUTE, l, *lowered[j], sub, views[j],
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }

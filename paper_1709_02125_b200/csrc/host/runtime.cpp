@@ -2,6 +2,9 @@
 // B200 engine.
 #include "ooc/runtime.hpp"
 
+#include <algorithm>
+#include <sstream>
+
 #include "ooc/gpu_engine.hpp"
 
 namespace ooc {
@@ -281,7 +284,9 @@ const std::vector<ChainTiming>& Runtime::chain_timings() {
 }
 
 const std::vector<LoopMetric>& Runtime::loop_metrics() {
-  if (gpu_) {
+  if (gpu_ && opts_.timeline) {
+    timeline();
+  } else if (gpu_) {
     for (const auto& [id, s] : gpu_->take_loop_times()) {
       auto it = metric_index_.find(id);
       if (it == metric_index_.end()) continue;
@@ -291,6 +296,82 @@ const std::vector<LoopMetric>& Runtime::loop_metrics() {
     }
   }
   return loop_metrics_;
+}
+
+// Real-timeline loop attribution (restates proj/src/metrics.cpp:14-32 over measured
+// rows): kernel rows sorted by (start, command_id); each gets max(0, end - prev_end).
+const std::vector<TimelineRow>& Runtime::timeline() {
+  if (!gpu_) return timeline_;
+  std::vector<TimelineRow> rows = gpu_->take_timeline();
+  std::vector<const TimelineRow*> k;
+  for (const TimelineRow& r : rows)
+    if (r.kind == 3) k.push_back(&r);
+  std::sort(k.begin(), k.end(), [](const TimelineRow* a, const TimelineRow* b) {
+    if (a->start != b->start) return a->start < b->start;
+    return a->command_id < b->command_id;
+  });
+  for (const TimelineRow* e : k) {
+    const double span = std::max(0.0, e->end - last_kernel_end_);
+    if (e->end > last_kernel_end_) last_kernel_end_ = e->end;
+    auto it = metric_index_.find(e->loop);
+    if (it == metric_index_.end()) continue;
+    LoopMetric& m = loop_metrics_[it->second];
+    m.time_s += span;
+    m.bandwidth = m.time_s > 0 ? static_cast<double>(m.bytes) / m.time_s : 0.0;
+  }
+  timeline_.insert(timeline_.end(), rows.begin(), rows.end());
+  return timeline_;
+}
+
+static const char* kind_name(int k) {
+  static const char* n[] = {"h2d", "d2h", "d2d", "kernel"};
+  return k >= 0 && k < 4 ? n[k] : "unknown";
+}
+
+std::string Runtime::timeline_csv() {
+  std::ostringstream os;  // proj/src/command.cpp:160-168
+  os << "command_id,kind,queue,bytes,issue,start,end\n";
+  os.precision(12);
+  for (const TimelineRow& e : timeline())
+    os << e.command_id << "," << kind_name(e.kind) << "," << e.queue << "," << e.bytes << ","
+       << e.issue << "," << e.start << "," << e.end << "\n";
+  return os.str();
+}
+
+std::string Runtime::report_csv(const std::string& app, const std::string& size, int iters) {
+  RunReport r = report();  // proj/src/metrics.cpp:46-60
+  r.app = app;
+  r.size = size;
+  r.iters = iters;
+  std::ostringstream os;
+  os << "#oocstencil-report-v1\n"
+        "app,size,iters,mode,tiles,capacity,average_bandwidth,total_bytes,total_time,"
+        "makespan,uploaded,downloaded,d2d,efficiency,hit_rate,faults,error\n";
+  os.precision(12);
+  os << r.app << "," << r.size << "," << r.iters << "," << r.mode << "," << r.tiles << ","
+     << r.capacity << "," << r.average_bandwidth << "," << r.total_bytes << "," << r.total_time
+     << "," << r.makespan << "," << r.uploaded << "," << r.downloaded << "," << r.d2d << ","
+     << r.efficiency << "," << r.hit_rate << "," << r.faults << "," << r.error << "\n";
+  return os.str();
+}
+
+std::string Runtime::loops_csv() {
+  std::ostringstream os;  // proj/src/metrics.cpp:62-70
+  os << "#oocstencil-report-v1\nloop,points,bytes,time,bandwidth\n";
+  os.precision(12);
+  for (const LoopMetric& l : loop_metrics())
+    os << l.loop_id << "," << l.points << "," << l.bytes << "," << l.time_s << "," << l.bandwidth
+       << "\n";
+  return os.str();
+}
+
+std::string Runtime::audit_csv() const {
+  std::ostringstream os;  // proj/src/metrics.cpp:72-79
+  os << "dataset,tile,uploaded,downloaded,d2d\n";
+  for (const AuditRow& r : audit_)
+    os << mesh_[r.dataset].name << "," << r.tile << "," << r.uploaded << "," << r.downloaded << ","
+       << r.d2d << "\n";
+  return os.str();
 }
 
 RunReport Runtime::report() {

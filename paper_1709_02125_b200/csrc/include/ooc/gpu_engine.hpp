@@ -4,6 +4,8 @@
 // ABI in include/ooc_device.h.
 #pragma once
 
+#include <chrono>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -83,6 +85,8 @@ class GpuEngine {
     double seconds;
   };
   std::vector<LaunchRecord> launch_log;
+  /// Resolve the real event timeline recorded so far (RuntimeOptions::timeline).
+  std::vector<TimelineRow> take_timeline();
   ooc_ctx* ctx() { return ctx_; }
   const ooc_dev_props& props() const { return props_; }
 
@@ -152,6 +156,23 @@ class GpuEngine {
   double* staging_ = nullptr;
   index_t staging_elems_ = 0;
   void ensure_staging(index_t elems);
+  struct TLPending {
+    int kind, queue;
+    index_t bytes;
+    DatasetId dataset;
+    int tile;
+    std::vector<std::pair<int, index_t>> loops;
+    double issue;
+    ooc_event* a;
+    ooc_event* b;
+  };
+  void timeline_cmd(int kind, int queue, index_t bytes, DatasetId d, int tile,
+                    std::vector<std::pair<int, index_t>> loops, const std::function<void()>& issue);
+  std::vector<TLPending> tl_pending_;
+  ooc_event* tl_base_ = nullptr;
+  std::chrono::steady_clock::time_point tl_host0_;
+  int next_cmd_ = 0;
+  int cur_tile_ = 0;
   // resident buffers by dataset id
   std::vector<Resident> res_;
   // reductions: device accumulator slot -> pinned host mirror

@@ -90,6 +90,7 @@ struct RuntimeOptions {
   bool profile_loops = false;       // per-launch CUDA events -> per-loop device time
   int arena_fill = 0;               // debug: 0 none, 1 zero (reference behaviour), 2 NaN poison
   bool fuse = true;                 // run point-wise-dependent consecutive loops in one launch
+  bool timeline = false;            // record a real event timeline of every command
   // ---- slab decomposition (multi-GPU, one runtime per GPU): this rank owns rows
   // [own_lo, own_hi) of dimension 0 and recomputes `ghost` rows on each side. Any
   // program runs unchanged: declared datasets and loop ranges are clipped to the
@@ -125,6 +126,19 @@ struct LoopMetric {
   index_t bytes = 0;
   double time_s = 0.0;
   double bandwidth = 0.0;
+};
+
+/// One command of the real event timeline (schema of the reference's simulated
+/// Timeline, proj/include/ooc/command.hpp:93-108). kind: 0 h2d, 1 d2h, 2 d2d, 3 kernel.
+struct TimelineRow {
+  int command_id;
+  int kind;
+  int queue;
+  index_t bytes;
+  double issue, start, end;  // seconds from the first recorded command
+  DatasetId dataset;
+  int tile;
+  int loop;
 };
 
 /// One executed chain as measured on the device (CUDA events).
@@ -220,6 +234,13 @@ class Runtime {
   const std::vector<ChainTiming>& chain_timings();
   RunReport report();
   GpuEngine& engine();
+  /// Real event timeline rows resolved so far (RuntimeOptions::timeline).
+  const std::vector<TimelineRow>& timeline();
+  // CSVs in the reference's schemas (proj/src/metrics.cpp:46-79, command.cpp:160-168)
+  std::string report_csv(const std::string& app = "", const std::string& size = "", int iters = 0);
+  std::string loops_csv();
+  std::string audit_csv() const;
+  std::string timeline_csv();
 
  private:
   void execute(LoopChain&& chain);
@@ -243,6 +264,8 @@ class Runtime {
   std::map<std::string, int> red_slot_;  // reduction name -> device accumulator slot
   std::map<int, index_t> owned_bytes_;   // windowed runs: metric bytes of the owned rows
   std::vector<ChainTiming> timings_;
+  std::vector<TimelineRow> timeline_;
+  double last_kernel_end_ = 0.0;
   std::unique_ptr<GpuEngine> gpu_;
 };
 

@@ -203,3 +203,19 @@ def test_specialised_kernels_compile_for_sm100a(app, kw):
     groups = rt.chain_jit_check(rt.num_chains() - 1, fuse=True)
     assert groups and all(g["ok"] for g in groups), [g.get("log", "")[:500] for g in groups if not g["ok"]]
     assert max(g["loops"] for g in groups) > 1  # fusion happened
+
+
+def test_report_csv_schemas_match_reference():
+    """proj/src/metrics.cpp:46-79 / command.cpp:160-168 headers; one loops row per loop."""
+    prog = P.app_program("heat2d", 32, 32, 0, iters=2)
+    rt = plan_only(prog)
+    rep = rt.report_csv("heat2d", "32x32", 2).splitlines()
+    assert rep[0] == "#oocstencil-report-v1"
+    assert rep[1] == ("app,size,iters,mode,tiles,capacity,average_bandwidth,total_bytes,"
+                      "total_time,makespan,uploaded,downloaded,d2d,efficiency,hit_rate,faults,error")
+    assert rep[2].startswith("heat2d,32x32,2,plan_only,1,")
+    loops = rt.loops_csv().splitlines()
+    assert loops[:2] == ["#oocstencil-report-v1", "loop,points,bytes,time,bandwidth"]
+    assert [l.split(",")[0] for l in loops[2:]] == ["0", "1"]
+    assert rt.audit_csv() == "dataset,tile,uploaded,downloaded,d2d\n"
+    assert rt.timeline_csv() == "command_id,kind,queue,bytes,issue,start,end\n"
