@@ -98,6 +98,44 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def measure_link(gpu, nbytes=1 << 30, reps=4):
+    """Pinned host<->device copy bandwidth, both directions at once (the streaming
+    engine's H2D and D2H queues overlap), timed with CUDA events on each copy stream.
+    torch is only the measuring tape here; the engine's copies are its own."""
+    import torch
+    dev = torch.device(f"cuda:{gpu}")
+    h_up = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_dn = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_up = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    d_dn = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s_up, s_dn = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    out = {}
+    for mode in ("alone", "concurrent"):
+        res = {}
+        for name, s, dst, src in (("h2d", s_up, d_up, h_up), ("d2h", s_dn, h_dn, d_dn)):
+            with torch.cuda.stream(s):
+                dst.copy_(src, non_blocking=True)  # warm
+        torch.cuda.synchronize(dev)
+        pairs = (((s_up, d_up, h_up, "h2d"), (s_dn, h_dn, d_dn, "d2h")),) if mode == "concurrent" \
+            else (((s_up, d_up, h_up, "h2d"),), ((s_dn, h_dn, d_dn, "d2h"),))
+        for group in pairs:
+            ev = {}
+            for s, dst, src, name in group:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(s):
+                    a.record(s)
+                    for _ in range(reps):
+                        dst.copy_(src, non_blocking=True)
+                    b.record(s)
+                ev[name] = (a, b)
+            torch.cuda.synchronize(dev)
+            for name, (a, b) in ev.items():
+                res[name] = reps * nbytes / (a.elapsed_time(b) * 1e-3) / 1e9
+        out[mode] = res
+    del h_up, h_dn, d_up, d_dn
+    return out
+
+
 def profiled_traffic(group):
     """DRAM bytes per launch of `group` from the committed ncu launch list
     (profiles/*_traffic.json, produced from the same bench command)."""
@@ -297,6 +335,12 @@ def main():
         barrier(dist)
         e2e = run_e2e(B, n, args.steps, warm, gpu)
         e2e_wall = max_over_ranks(e2e["wall"], dist, local)
+    link = None
+    if e2e:
+        try:
+            link = measure_link(gpu)
+        except Exception as ex:  # noqa: BLE001
+            link = {"error": str(ex)}
     if rank != 0:
         return
     peak, peak_kind = measured_peaks()
@@ -355,7 +399,22 @@ def main():
                                 "their own host link" if world > 1 else ""),
                        "device_s": e2e["device_s"], "wall_s": e2e["wall"],
                        "ooc_over_incore": e2e_val / value, "launches": e2e["launches"],
-                       "clocks": e2e["clocks"]}
+                       "clocks": e2e["clocks"],
+                       "link_GBps": {"h2d": e2e["uploaded"] / e2e["wall"] / 1e9,
+                                     "d2h": e2e["downloaded"] / e2e["wall"] / 1e9}}
+        if link and "concurrent" in link:
+            # SURVEY §8(d) out-of-core roofline: min(in-core, BW_h2d·metric/up, BW_d2h·metric/down)
+            # with the pinned-copy bandwidths measured concurrently on this box
+            bw = link["concurrent"]
+            lim = {"incore": value / world,
+                   "h2d": bw["h2d"] * e2e["bytes"] / max(e2e["uploaded"], 1),
+                   "d2h": bw["d2h"] * e2e["bytes"] / max(e2e["downloaded"], 1)}
+            bound = min(lim, key=lim.get)
+            line["e2e"]["roofline"] = {"bound": bound, "limit": lim[bound] * world, "unit": UNIT,
+                                       "frac": e2e_val / (lim[bound] * world), "limits": lim,
+                                       "pinned_copy_GBps": link}
+        elif link:
+            line["e2e"]["roofline"] = link
     if not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_reference(1, n_sample=1920, warmup=0)
