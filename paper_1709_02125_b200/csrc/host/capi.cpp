@@ -519,9 +519,12 @@ const char* ooc_rt_chain_jit_check(ooc_runtime* h, int chain, int fuse) {
       calls.clear();
       tape = 0;
     };
+    std::vector<std::size_t> tape_len(c.loops.size());
+    for (std::size_t j = 0; j < c.loops.size(); ++j) tape_len[j] = low[j].tape.size();
+    const std::vector<char> starts = ooc::plan_fusion(m, c.loops, tape_len, fuse != 0);
     for (std::size_t j = 0; j < c.loops.size(); ++j) {
       const ooc::ParLoop& l = c.loops[j];
-      if (!ooc::can_fuse(grp, tape, l, fuse != 0)) flush();
+      if (starts[j] || !ooc::can_fuse(grp, tape, l, fuse != 0)) flush();
       ooc_loop L{};
       L.ndim = l.range.ndim;
       for (int d = 0; d < 3; ++d) {

@@ -15,6 +15,8 @@
 // omits (kernels of tile t wait for the H2D of tile t).
 #include "ooc/gpu_engine.hpp"
 
+#include <map>
+
 #include <cmath>
 #include <cstring>
 
@@ -189,6 +191,64 @@ bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, 
   return true;
 }
 
+std::vector<char> plan_fusion(const Mesh& mesh, const std::vector<ParLoop>& loops,
+                              const std::vector<std::size_t>& tape_len, bool enabled) {
+  const std::size_t L = loops.size();
+  std::vector<char> starts(L, 1);
+  if (!enabled || L < 2) return starts;
+  // longest legal group from each start (exactly the engine's incremental check)
+  std::vector<std::size_t> maxj(L);
+  for (std::size_t i = 0; i < L; ++i) {
+    std::vector<const ParLoop*> g{&loops[i]};
+    std::size_t tape = tape_len[i], j = i + 1;
+    if (!loops[i].has_reduction())
+      for (; j < L && can_fuse(g, tape, loops[j], true); ++j) {
+        g.push_back(&loops[j]);
+        tape += tape_len[j];
+      }
+    maxj[i] = j;
+  }
+  // estimated DRAM bytes of a group: each dataset read once if its first access in
+  // the group reads it, written once if any loop writes it; plus a launch cost
+  constexpr double kLaunchBytes = 24e6;  // ~4 us of HBM time per extra launch
+  auto cost = [&](std::size_t i, std::size_t j) {
+    std::map<DatasetId, std::pair<int, index_t>> m;  // dataset -> (reads+writes, points)
+    std::map<DatasetId, bool> seen, wrote;
+    for (std::size_t k = i; k < j; ++k)
+      for (const LoopArg& a : loops[k].args) {
+        auto& e = m[a.dataset];
+        if (!seen[a.dataset]) {
+          seen[a.dataset] = true;
+          e.first += access_reads(a.mode) ? 1 : 0;
+        }
+        if (access_writes(a.mode) && !wrote[a.dataset]) {
+          wrote[a.dataset] = true;
+          e.first += 1;
+        }
+        e.second = std::max(e.second, loops[k].range.size());
+      }
+    double b = kLaunchBytes;
+    for (const auto& [d, e] : m) b += static_cast<double>(e.first) * e.second * mesh[d].elem_bytes;
+    return b;
+  };
+  std::vector<double> best(L + 1, 1e300);
+  std::vector<std::size_t> from(L + 1, 0);
+  best[0] = 0;
+  for (std::size_t j = 1; j <= L; ++j)
+    for (std::size_t i = j; i-- > 0;) {
+      if (j - i > 8) break;
+      if (maxj[i] < j) continue;
+      const double c = best[i] + cost(i, j);
+      if (c < best[j]) {
+        best[j] = c;
+        from[j] = i;
+      }
+    }
+  std::fill(starts.begin(), starts.end(), 0);
+  for (std::size_t j = L; j > 0; j = from[j]) starts[from[j]] = 1;
+  return starts;
+}
+
 bool GpuEngine::fusable(const ParLoop& b) const {
   return can_fuse(group_.loops, group_.tape_len, b, opts_.fuse);
 }
@@ -222,9 +282,11 @@ void GpuEngine::flush_group(int queue) {
   group_ = Group{};
 }
 
-void GpuEngine::launch(int queue, const ParLoop& loop, const LoweredLoop& lw, const Extent& sub,
+void GpuEngine::launch(int queue, bool group_start, int tile, const ParLoop& loop,
+                       const LoweredLoop& lw, const Extent& sub,
                        const std::vector<ooc_view>& views, int red_slot) {
-  if (!fusable(loop)) flush_group(queue);
+  if (group_start || !fusable(loop)) flush_group(queue);
+  cur_tile_ = tile;
   ooc_loop L{};
   L.ndim = sub.ndim;
   for (int d = 0; d < 3; ++d) {
@@ -405,6 +467,9 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
   // tapes are lowered once per chain; ooc_launch_loop copies them into kernel params
   std::vector<LoweredLoop> lowered_store(chain.loops.size());
   for (std::size_t j = 0; j < chain.loops.size(); ++j) lowered_store[j] = lower_loop(chain.loops[j]);
+  std::vector<std::size_t> tape_len(chain.loops.size());
+  for (std::size_t j = 0; j < chain.loops.size(); ++j) tape_len[j] = lowered_store[j].tape.size();
+  const std::vector<char> starts = plan_fusion(mesh, chain.loops, tape_len, opts_.fuse);
   std::vector<ooc_view> hviews(mesh.datasets.size());
   for (DatasetId d : used) hviews[static_cast<std::size_t>(d)] = host_view(mesh[d]);
 
@@ -461,7 +526,6 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
       DEV(ooc_event_record(ctx_, E(ev_h2d_, t + 1), OOC_Q_H2D));
     }
 
-    cur_tile_ = t;
     // kernels of tile t wait for tile t's upload (missing from the reference model)
     DEV(ooc_queue_wait(ctx_, OOC_Q_COMPUTE, E(ev_h2d_, t)));
     for (std::size_t j = 0; j < chain.loops.size(); ++j) {
@@ -475,7 +539,7 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
         if (access_writes(a.mode)) mesh[a.dataset].ever_written = true;
       }
       auto rs = out.reduction_slot.find(loop.id);
-      launch(OOC_Q_COMPUTE, loop, lowered_store[j], sub, views,
+      launch(OOC_Q_COMPUTE, starts[j] != 0, t, loop, lowered_store[j], sub, views,
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
     flush_group(OOC_Q_COMPUTE);
@@ -743,6 +807,9 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
       }
     }
   }
+  std::vector<std::size_t> tape_len(chain.loops.size());
+  for (std::size_t j = 0; j < chain.loops.size(); ++j) tape_len[j] = lowered_store[j].tape.size();
+  const std::vector<char> starts = plan_fusion(mesh, chain.loops, tape_len, opts_.fuse);
   const int T = plan ? plan->tile_count : 1;
   for (int t = 0; t < T; ++t)
     for (std::size_t j = 0; j < chain.loops.size(); ++j) {
@@ -750,9 +817,7 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
       const Extent sub = plan ? plan->subrange(static_cast<int>(j), t) : l.range;
       if (sub.empty()) continue;
       auto rs = out.reduction_slot.find(l.id);
-      if (!fusable(l)) flush_group(OOC_Q_COMPUTE);
-      cur_tile_ = t;
-      launch(OOC_Q_COMPUTE, l, *lowered[j], sub, views[j],
+      launch(OOC_Q_COMPUTE, starts[j] != 0, t, l, *lowered[j], sub, views[j],
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
   flush_group(OOC_Q_COMPUTE);

@@ -31,6 +31,14 @@ LoweredLoop lower_loop(const ParLoop& loop);
 bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, const ParLoop& b,
               bool enabled);
 
+/// Fusion partition of a chain into consecutive launch groups: starts[j] = 1 where a
+/// launch begins. Among all partitions whose groups pass `can_fuse` (as the engine
+/// checks them, prefix by prefix) it picks the one with the least estimated DRAM
+/// traffic plus a per-launch cost — greedy first-fit can strand loops in extra
+/// launches that re-read what the previous launch just wrote.
+std::vector<char> plan_fusion(const Mesh& mesh, const std::vector<ParLoop>& loops,
+                              const std::vector<std::size_t>& tape_len, bool enabled);
+
 /// Dense (optionally row-padded) device layout of a box.
 struct BoxLayout {
   Extent box;       // the largest box the layout must hold (per-dim max lengths)
@@ -120,7 +128,8 @@ class GpuEngine {
   ooc_event* fresh_timing_event();
   void recycle(ooc_event* e);
   int alloc_red_slot();
-  void launch(int queue, const ParLoop& loop, const LoweredLoop& lw, const Extent& sub,
+  void launch(int queue, bool group_start, int tile, const ParLoop& loop, const LoweredLoop& lw,
+              const Extent& sub,
               const std::vector<ooc_view>& views, int red_slot);
   bool fusable(const ParLoop& b) const;
   void flush_group(int queue);

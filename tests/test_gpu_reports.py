@@ -66,3 +66,35 @@ def test_timeline_off_records_nothing():
     rt = B.Runtime("resident")
     rt.run_app("heat2d", 64, 64, 0, 4)
     assert rt.timeline_csv() == "command_id,kind,queue,bytes,issue,start,end\n"
+
+
+def _prefetch_kat():
+    """proj/tests/test_device_sim.cpp:316-368: c pure input, a = c, b = a(-1); 3 tiles."""
+    p = P.Prog()
+    p.declare("c", (0,), (12,), (1,), "(* 0.125 i)")
+    p.declare("a", (0,), (12,), (1,), 0.0)
+    p.declare("b", (0,), (12,), (1,), 0.0)
+    for _ in range(2):
+        p.loop((0,), (12,), [("c", P.POINT, P.R), ("a", P.POINT, P.W)], {1: P.r(0)})
+        p.loop((0,), (12,), [("a", [(-1, 0, 0), (0, 0, 0)], P.R), ("b", P.POINT, P.W)],
+               {1: P.r(0, -1)})
+        p.flush()
+    p.finish()
+    return p.to_json()
+
+
+def test_prefetch_kat_second_chain_skips_tile0_upload():
+    prog = _prefetch_kat()
+    want = oracle_record(prog, "explicit", tiles=3, prefetch=True)
+    got = product_record(prog, "explicit", tiles=3, prefetch=True, timeline=True)
+    rt = got.pop("_rt")
+    want.pop("_rt", None)
+    assert not compare(want, got)
+    audit = rt.audit()  # rows [dataset, tile, up, down, d2d] of both chains in order
+    cut = next(i for i in range(1, len(audit)) if audit[i][0] < audit[i - 1][0])
+    second = audit[cut:]
+    assert sum(r[2] for r in audit[:cut] if r[1] == 0) == 72
+    assert sum(r[2] for r in second if r[1] == 0) == 0
+    plain = product_record(prog, "explicit", tiles=3)
+    plain.pop("_rt")
+    assert plain["buffers"] == got["buffers"]
