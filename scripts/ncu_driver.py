@@ -1,12 +1,32 @@
-"""Small, deterministic driver for ncu captures: miniflow2d resident (one warm-up
-chain + one measured chain of 10 iterations)."""
-import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_1709_02125_b200 as B
+"""Small, deterministic driver for ncu captures: miniflow2d resident, `chains`
+10-iteration chains (the first ones compile + tune every fused kernel). Writes the
+launch sequence of the last chain — (first loop position, loops) per launch — to
+gpurun_out/ncu_seq.json so scripts/ncu_summarize.py can label ncu's launch list.
+
+    python scripts/ncu_driver.py [n] [fuse] [chains] [app]
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1709_02125_b200 as B  # noqa: E402
+
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 15360
 fuse = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-rt = B.Runtime("resident", fuse=bool(fuse))
-rt.declare_app("miniflow2d", n, n)
-rt.app_iterations("miniflow2d", n, n, 0, 0, 20)
-rt.sync()
+chains = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+app = sys.argv[4] if len(sys.argv) > 4 else "miniflow2d"
+nz = n if app.endswith("3d") else 0
+rt = B.Runtime("resident", fuse=bool(fuse), profile=True)
+rt.declare_app(app, n, n, nz)
+for c in range(chains):
+    first_id = max((m[0] for m in rt.loop_metrics()), default=-1) + 1
+    rt.app_iterations(app, n, n, nz, 10 * c, 10 * (c + 1))
+    rt.sync()
+    log = rt.launch_log()
+seq = [[first - first_id, nl, nbytes] for first, nl, nbytes, _ in log]
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+with open(os.path.join(ROOT, "gpurun_out", "ncu_seq.json"), "w") as f:
+    json.dump({"app": app, "n": n, "fuse": fuse, "chains": chains, "last_chain": seq}, f)
 print(rt.device())
