@@ -24,6 +24,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <map>
+#include <tuple>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -268,6 +271,73 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
       fam[f].obmax = std::max(fam[f].obmax, ob);
     }
   }
+  // ---- row recompute: a read at a B-only (row) offset of a value written earlier in
+  // the group is evaluated in-thread by re-running the writer's tape on the shifted
+  // row (recursively through earlier writers); the host's can_fuse admits such groups
+  // only when no loop of the group rewrites the recomputation's inputs.
+  auto tape_of = [&](int i, int w) {
+    const ooc_ins* t = Ls[i].tape;
+    for (int k = 0; k < w; ++k) t += Ls[i].write_len[k];
+    return t;
+  };
+  auto last_writer = [&](const double* data, int before, int* wout) -> int {
+    for (int i = before - 1; i >= 0; --i)
+      for (int w = 0; w < Ls[i].nwrites; ++w)
+        if (Ls[i].args[Ls[i].write_arg[w]].data == data) {
+          *wout = w;
+          return i;
+        }
+    return -1;
+  };
+  auto zero = [](const int64_t* o) { return o[0] == 0 && o[1] == 0 && o[2] == 0; };
+  auto b_only = [&](const int64_t* o) {
+    for (int d = 0; d < 3; ++d)
+      if (d != cn.B && o[d] != 0) return false;
+    return cn.B >= 0;
+  };
+  auto extend = [&](const ooc_view& v, const int64_t* o, int64_t ob) {
+    const int f = family_of(v, o);
+    fam[f].obmin = std::min(fam[f].obmin, ob);
+    fam[f].obmax = std::max(fam[f].obmax, ob);
+  };
+  std::vector<std::vector<std::vector<char>>> dem;  // [loop][write][shift + 64]
+  dem.assign(n, {});
+  for (int i = 0; i < n; ++i) dem[i].assign(Ls[i].nwrites, std::vector<char>(129, 0));
+  std::function<bool(int, int, int)> demand = [&](int a, int w, int s) -> bool {
+    if (s < -64 || s > 64) return false;
+    const ooc_view& X = Ls[a].args[Ls[a].write_arg[w]];
+    const int64_t ox[3] = {cn.B == 0 ? s : 0, cn.B == 1 ? s : 0, cn.B == 2 ? s : 0};
+    extend(X, ox, s);  // snapshot where the writer is inactive (slow path)
+    if (s == 0) return true;  // the writer's own value at this point: forwarded
+    if (dem[a][w][s + 64]) return true;
+    dem[a][w][s + 64] = 1;
+    const ooc_ins* t = tape_of(a, w);
+    for (int k = 0; k < Ls[a].write_len[w]; ++k) {
+      const ooc_ins& in = t[k];
+      if (in.op != OOC_OP_READ) continue;
+      const ooc_view& v = Ls[a].args[in.arg];
+      int vw = 0;
+      const int src = last_writer(v.data, a, &vw);
+      const int64_t ob = s + off_of(in.offset, cn.B);
+      if (src >= 0) {
+        if (!b_only(in.offset) && !zero(in.offset)) return false;
+        if (!demand(src, vw, static_cast<int>(ob))) return false;
+      } else {
+        extend(v, in.offset, ob);
+      }
+    }
+    return true;
+  };
+  for (int j = 0; j < n; ++j)
+    for (int t = 0; t < Ls[j].ntape; ++t) {
+      const ooc_ins& in = Ls[j].tape[t];
+      if (in.op != OOC_OP_READ || zero(in.offset)) continue;
+      int w = 0;
+      const int a = last_writer(Ls[j].args[in.arg].data, j, &w);
+      if (a < 0) continue;
+      if (!b_only(in.offset)) return false;
+      if (!demand(a, w, static_cast<int>(off_of(in.offset, cn.B)))) return false;
+    }
   if (static_cast<int>(fam.size()) > OOC_JMAX_FAMILIES) return false;
   std::ostringstream slow, fast;
   int values = 0;
@@ -326,6 +396,88 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
   };
   std::vector<Writer> writers;
   int ncst = 0, nwrite = 0;
+  std::vector<std::vector<std::vector<int>>> cst_idx(n);  // constants of each write tape
+  for (int i = 0; i < n; ++i) cst_idx[i].resize(Ls[i].nwrites);
+  std::map<std::tuple<int, int, int>, std::pair<std::string, std::string>> rc_memo;
+  int rc_count = 0;
+  auto active_at = [&](int a, int s) -> std::string {  // slow-path: loop a active at row bq+s
+    const std::string as = std::to_string(a), bs = "(bq + (" + std::to_string(s) + "))";
+    return "(ia >= p.rng[" + as + "][0] && ia < p.rng[" + as + "][1] && " + bs + " >= p.rng[" + as +
+           "][2] && " + bs + " < p.rng[" + as + "][3] && c >= p.rng[" + as + "][4] && c < p.rng[" + as +
+           "][5])";
+  };
+  auto fam_sym = [&](const ooc_view& v, const int64_t* o, int64_t ob) {
+    const int f = family_of(v, o);
+    return "F" + std::to_string(f) + "[q + " + std::to_string(ob - fam[f].obmin) + "][k]";
+  };
+  // value of loop a's write w at row bq+s: {slow-path symbol, fast-path symbol}
+  std::function<std::pair<std::string, std::string>(int, int, int)> rc =
+      [&](int a, int w, int s) -> std::pair<std::string, std::string> {
+    auto key = std::make_tuple(a, w, s);
+    auto it = rc_memo.find(key);
+    if (it != rc_memo.end()) return it->second;
+    if (s == 0) {  // computed at this very point earlier in the launch: forward it
+      const std::string o = "o" + std::to_string(a) + "_" + std::to_string(w);
+      const int64_t z[3] = {0, 0, 0};
+      const ooc_view& X = Ls[a].args[Ls[a].write_arg[w]];
+      return rc_memo[key] = {"(a" + std::to_string(a) + " ? " + o + " : " + fam_sym(X, z, 0) + ")", o};
+    }
+    const std::string tag = "r" + std::to_string(rc_count++) + "_";
+    std::vector<std::string> st_s, st_f;
+    const ooc_ins* t = tape_of(a, w);
+    std::size_t ci = 0;
+    int tmp = 0;
+    for (int k = 0; k < Ls[a].write_len[w]; ++k) {
+      const ooc_ins& in = t[k];
+      if (in.op == OOC_OP_CONST) {
+        const std::string c = "p.cst[" + std::to_string(cst_idx[a][w].at(ci++)) + "]";
+        st_s.push_back(c);
+        st_f.push_back(c);
+      } else if (in.op == OOC_OP_READ) {
+        const ooc_view& v = Ls[a].args[in.arg];
+        int vw = 0;
+        const int src = last_writer(v.data, a, &vw);
+        const int64_t ob = s + off_of(in.offset, cn.B);
+        if (src >= 0) {
+          auto sub = rc(src, vw, static_cast<int>(ob));
+          st_s.push_back(sub.first);
+          st_f.push_back(sub.second);
+        } else {
+          st_s.push_back(fam_sym(v, in.offset, ob));
+          st_f.push_back(st_s.back());
+        }
+      } else {
+        const std::string name = tag + std::to_string(tmp++);
+        for (int path = 0; path < 2; ++path) {
+          auto& st = path ? st_f : st_s;
+          std::ostringstream& b = path ? fast : slow;
+          std::string y = st.back();
+          st.pop_back();
+          std::string x = st.back();
+          st.pop_back();
+          b << "          const double " << name << " = ";
+          switch (in.op) {
+            case OOC_OP_ADD: b << x << " + " << y; break;
+            case OOC_OP_SUB: b << x << " - " << y; break;
+            case OOC_OP_MUL: b << x << " * " << y; break;
+            case OOC_OP_DIV: b << x << " / " << y; break;
+            case OOC_OP_MIN: b << "ooc_min(" << x << ", " << y << ")"; break;
+            default: b << "ooc_max(" << x << ", " << y << ")"; break;
+          }
+          b << ";\n";
+          st.push_back(name);
+        }
+      }
+    }
+    // inactive writer at that row: the value memory held before the launch
+    const ooc_view& X = Ls[a].args[Ls[a].write_arg[w]];
+    const int64_t ox[3] = {cn.B == 0 ? s : 0, cn.B == 1 ? s : 0, cn.B == 2 ? s : 0};
+    const std::string res = tag + "v";
+    slow << "          const double " << res << " = " << active_at(a, s) << " ? " << st_s.back() << " : "
+         << fam_sym(X, ox, s) << ";\n";
+    fast << "          const double " << res << " = " << st_f.back() << ";\n";
+    return rc_memo[key] = {res, res};
+  };
   for (int i = 0; i < n; ++i) {
     const ooc_loop& L = Ls[i];
     const bool full = L.lo[0] == lo[0] && L.hi[0] == hi[0] && L.lo[1] == lo[1] &&
@@ -338,6 +490,18 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
     shrink(1, rel(cn.B, false), rel(cn.B, true));
     shrink(2, rel(cn.C, false), rel(cn.C, true));
     const std::string is = std::to_string(i);
+    {
+      int* r = jp.rng[i];
+      r[0] = rel(cn.A, false);
+      r[1] = rel(cn.A, true);
+      r[2] = rel(cn.B, false);
+      r[3] = rel(cn.B, true);
+      r[4] = rel(cn.C, false);
+      r[5] = rel(cn.C, true);
+      for (int w = 0; w < L.nwrites; ++w)  // interior tiles: recomputed rows in range too
+        for (int sh = -64; sh <= 64; ++sh)
+          if (dem[i][w][sh + 64]) shrink(1, r[2] - sh, r[3] - sh);
+    }
     if (full) {
       slow << "          const bool a" << is << " = okp;\n";
     } else {
@@ -355,6 +519,14 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
     int tmp = 0;
     auto operand = [&](const ooc_ins& in, bool is_fast) -> std::string {
       const ooc_view& v = L.args[in.arg];
+      if (!zero(in.offset)) {
+        int w = 0;
+        const int src = last_writer(v.data, i, &w);
+        if (src >= 0) {
+          auto r = rc(src, w, static_cast<int>(off_of(in.offset, cn.B)));
+          return is_fast ? r.second : r.first;
+        }
+      }
       const int f = family_of(v, in.offset);
       const int64_t ob = off_of(in.offset, cn.B);
       std::string sym = "F" + std::to_string(f) + "[q + " + std::to_string(ob - fam[f].obmin) + "][k]";
@@ -364,12 +536,13 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
             sym = is_fast ? w.sym : "(a" + std::to_string(w.loop) + " ? " + w.sym + " : " + sym + ")";
       return sym;
     };
-    auto emit = [&](const ooc_ins* tape, int len, const std::string& dst) -> bool {
+    auto emit = [&](const ooc_ins* tape, int len, const std::string& dst, int wi) -> bool {
       std::vector<std::string> st_s, st_f;
       for (int qd = 0; qd < len; ++qd) {
         const ooc_ins& in = tape[qd];
         if (in.op == OOC_OP_CONST) {
           if (ncst >= OOC_JMAX_CONST) return false;
+          if (wi >= 0) cst_idx[i][wi].push_back(ncst);
           jp.cst[ncst] = in.value;
           const std::string c = "p.cst[" + std::to_string(ncst++) + "]";
           st_s.push_back(c);
@@ -410,11 +583,11 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
     };
     const ooc_ins* t = L.tape;
     for (int w = 0; w < L.nwrites; ++w) {
-      if (!emit(t, L.write_len[w], "o" + is + "_" + std::to_string(w))) return false;
+      if (!emit(t, L.write_len[w], "o" + is + "_" + std::to_string(w), w)) return false;
       t += L.write_len[w];
     }
     if (L.reduce_op != OOC_RED_NONE) {
-      if (!emit(t, L.reduce_len, "rv")) return false;
+      if (!emit(t, L.reduce_len, "rv", -1)) return false;
       slow << "#if OOC_RED\n          if (a" << is << ") acc = ooc_red(p.red_op, acc, rv);\n#endif\n";
       fast << "#if OOC_RED\n          acc = ooc_red(p.red_op, acc, rv);\n#endif\n";
     }
@@ -577,6 +750,23 @@ std::vector<Shape> candidates(int ndim, long long nC) {
   return out;
 }
 
+const std::unordered_map<std::size_t, Shape>& preset_shapes() {
+  static std::unordered_map<std::size_t, Shape> m;
+  static bool loaded = false;
+  if (loaded) return m;
+  loaded = true;
+  const char* f = std::getenv("OOC_JIT_TUNE");
+  if (!f || !*f) return m;
+  FILE* fp = std::fopen(f, "r");
+  if (!fp) return m;
+  char hex[64];
+  Shape sh;
+  while (std::fscanf(fp, "%63s %dx%d", hex, &sh.Q, &sh.P) == 3)
+    m[static_cast<std::size_t>(std::strtoull(hex, nullptr, 16))] = sh;
+  std::fclose(fp);
+  return m;
+}
+
 // Resolve measured candidates (non-blocking) and pick the winner once all are in.
 void settle(Tuning& T) {
   for (std::size_t i = 0; i < T.cands.size(); ++i) {
@@ -661,6 +851,13 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     T.points.assign(T.cands.size(), 0);
     T.issued.assign(T.cands.size(), 0);
     if (T.cands.size() == 1) T.best = 0;
+    // replayed tuning (OOC_JIT_TUNE=file of "key QxP" lines from ooc_jit_report):
+    // profilers see the shapes an unprofiled run picked, not their own timing
+    const auto& pre = preset_shapes();
+    auto ps = pre.find(std::hash<std::string>{}(body + (red ? "|red" : "|nored")));
+    if (ps != pre.end())
+      for (std::size_t i = 0; i < T.cands.size(); ++i)
+        if (T.cands[i].Q == ps->second.Q && T.cands[i].P == ps->second.P) T.best = static_cast<int>(i);
     // compile every candidate now (first sight of this structure, normally a
     // warm-up chain) so later launches never wait for NVRTC
     for (const Shape& cs : T.cands) {
@@ -772,7 +969,7 @@ extern "C" int ooc_jit_report(char* buf, int len) {
     const std::string fast = key.substr(0, key.find("<<FAST>>"));
     while ((pos = fast.find("const bool a", pos)) != std::string::npos) ++nl, ++pos;
     o << (first ? "" : ",") << "{\"loops\":" << nl << ",\"red\":" << (key.find("|red") != std::string::npos)
-      << ",\"shape\":\"";
+      << ",\"key\":\"" << std::hex << std::hash<std::string>{}(key) << std::dec << "\",\"shape\":\"";
     if (T.best >= 0) o << T.cands[T.best].Q << "x" << T.cands[T.best].P;
     o << "\",\"ns_per_point\":{";
     for (std::size_t i = 0; i < T.cands.size(); ++i)

@@ -633,6 +633,24 @@ int ooc_launch_group(ooc_ctx* c, int q, const ooc_loop* loops, int n) {
     if (live.size() > 1) ++c->stats.special_launches;
     return OOC_OK;
   }
+  // The interpreter forwards values only at the point itself: a group that relies on
+  // row recompute (a neighbour read of a value written earlier in the group) runs
+  // loop by loop — the sequential semantics the fused launch reproduces.
+  for (std::size_t j = 1; j < live.size(); ++j)
+    for (int t = 0; t < live[j].ntape; ++t) {
+      const ooc_ins& in = live[j].tape[t];
+      if (in.op != OOC_OP_READ || (in.offset[0] == 0 && in.offset[1] == 0 && in.offset[2] == 0)) continue;
+      const double* d = live[j].args[in.arg].data;
+      for (std::size_t i = 0; i < j; ++i)
+        for (int w = 0; w < live[i].nwrites; ++w)
+          if (live[i].args[live[i].write_arg[w]].data == d) {
+            for (const ooc_loop& L : live) {
+              int rc = ooc_launch_group(c, q, &L, 1);
+              if (rc) return rc;
+            }
+            return OOC_OK;
+          }
+    }
   if (total <= 64) return launch_cap<64>(c, q, live.data(), static_cast<int>(live.size()));
   OOC_ARG_CHECK(total <= 1000, "ooc_launch_group: program too long");
   return launch_cap<1000>(c, q, live.data(), static_cast<int>(live.size()));

@@ -168,10 +168,64 @@ int GpuEngine::alloc_red_slot() {
   return s;
 }
 
-// Loop fusion: consecutive loops run in one launch when every cross-loop access is
-// point-wise, i.e. a point only ever consumes values its own thread produced
-// earlier in the launch (RAW), and no loop overwrites what an earlier loop of the
-// group reads at a neighbour (WAR). Reducing loops always run alone.
+// Loop fusion: consecutive loops run in one launch when every value a point consumes
+// is either (a) read from memory that no loop of the launch writes at another point,
+// or (b) produced earlier in the launch by the same thread — at the point itself
+// (forwarded in registers) or, for reads at row (B = dim ndim-2) offsets, by
+// re-evaluating the unique earlier writer's expression on the shifted row from inputs
+// no loop of the launch rewrites ("row recompute"). The matching WAR rule: no loop
+// overwrites what an earlier loop reads at a neighbour, directly or through a
+// recomputation. Reducing loops always run alone.
+namespace {
+
+bool row_only(const Stencil& st, int ndim) {
+  const int b = ndim - 2;
+  if (b < 0) return false;
+  for (const Point& o : st.offsets)
+    for (int d = 0; d < 3; ++d)
+      if (d != b && o[d] != 0) return false;
+  return true;
+}
+
+bool writes_dataset(const ParLoop& l, DatasetId d) {
+  for (const LoopArg& a : l.args)
+    if (a.dataset == d && access_writes(a.mode)) return true;
+  return false;
+}
+
+// Datasets the recomputation of dataset d before position `pos` reads from memory;
+// false when it cannot be recomputed (several writers, non-row offsets, or an input
+// that some loop from the writer on rewrites).
+bool recompute_inputs(const std::vector<const ParLoop*>& all, DatasetId d, std::size_t pos,
+                      std::vector<DatasetId>& inputs, int depth = 0) {
+  if (depth > 8) return false;
+  std::size_t x = all.size();
+  int nw = 0;
+  for (std::size_t k = 0; k < pos; ++k)
+    if (writes_dataset(*all[k], d)) {
+      x = k;
+      ++nw;
+    }
+  if (nw != 1) return false;
+  const ParLoop& w = *all[x];
+  for (const LoopArg& a : w.args) {
+    if (!access_reads(a.mode)) continue;
+    bool earlier = false;
+    for (std::size_t k = 0; k < x; ++k) earlier = earlier || writes_dataset(*all[k], a.dataset);
+    if (earlier) {
+      if (!a.stencil.is_point() && !row_only(a.stencil, w.range.ndim)) return false;
+      if (!recompute_inputs(all, a.dataset, x, inputs, depth + 1)) return false;
+      continue;
+    }
+    for (std::size_t k = x; k < all.size(); ++k)
+      if (writes_dataset(*all[k], a.dataset)) return false;
+    inputs.push_back(a.dataset);
+  }
+  return true;
+}
+
+}  // namespace
+
 bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, const ParLoop& b,
               bool enabled) {
   if (group.empty()) return true;
@@ -179,15 +233,36 @@ bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, 
   std::size_t tape = group_tape;
   for (const auto& t : b.write_tapes) tape += t.ins.size();
   if (tape > 200) return false;
+  std::vector<const ParLoop*> all(group);
+  all.push_back(&b);
   for (const ParLoop* a : group) {
     if (a->has_reduction() || a->range.ndim != b.range.ndim) return false;
     for (const LoopArg& x : a->args)
       for (const LoopArg& y : b.args) {
         if (x.dataset != y.dataset) continue;
-        if (access_writes(x.mode) && access_reads(y.mode) && !y.stencil.is_point()) return false;
         if (access_reads(x.mode) && access_writes(y.mode) && !x.stencil.is_point()) return false;
       }
   }
+  // b's neighbour reads of values written in the launch: row recompute only
+  for (const LoopArg& y : b.args) {
+    if (!access_reads(y.mode) || y.stencil.is_point()) continue;
+    bool written = false;
+    for (const ParLoop* a : group) written = written || writes_dataset(*a, y.dataset);
+    if (!written) continue;
+    if (!row_only(y.stencil, b.range.ndim) || writes_dataset(b, y.dataset)) return false;
+    std::vector<DatasetId> in;
+    if (!recompute_inputs(all, y.dataset, group.size(), in)) return false;
+  }
+  // b must not overwrite an input of a recomputation an earlier loop relies on
+  for (std::size_t j = 0; j < group.size(); ++j)
+    for (const LoopArg& y : group[j]->args) {
+      if (!access_reads(y.mode) || y.stencil.is_point()) continue;
+      bool written = false;
+      for (std::size_t k = 0; k < j; ++k) written = written || writes_dataset(*group[k], y.dataset);
+      if (!written) continue;
+      std::vector<DatasetId> in;
+      if (!recompute_inputs(all, y.dataset, j, in)) return false;
+    }
   return true;
 }
 

@@ -27,6 +27,11 @@ for c in range(chains):
     log = rt.launch_log()
 seq = [[first - first_id, nl, nbytes] for first, nl, nbytes, _ in log]
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-with open(os.path.join(ROOT, "gpurun_out", "ncu_seq.json"), "w") as f:
+seq_name = "ncu_seq.json" if not os.environ.get("OOC_JIT_TUNE") else "ncu_seq_replay.json"
+with open(os.path.join(ROOT, "gpurun_out", seq_name), "w") as f:
     json.dump({"app": app, "n": n, "fuse": fuse, "chains": chains, "last_chain": seq}, f)
+with open(os.path.join(ROOT, "gpurun_out", "ncu_tune.txt"), "w") as f:
+    for k in B.jit_report():  # replay these shapes under ncu: OOC_JIT_TUNE=gpurun_out/ncu_tune.txt
+        if k["shape"]:
+            f.write(f"{k['key']} {k['shape']}\n")
 print(rt.device())

@@ -23,8 +23,9 @@ def main(csv_path, seq_path, out_path):
         e = rows.setdefault(int(r["ID"]), {"kernel": r["Kernel Name"], "grid": r["Grid Size"]})
         v = float(r["Metric Value"].replace(",", ""))
         unit = r["Metric Unit"]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-                 "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(unit, 1)
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3,
+                 "MB": 1e6, "GB": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+                 "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "second": 1, "s": 1}[unit]
         e[r["Metric Name"]] = v * scale
     seq = json.load(open(seq_path))
     last = seq["last_chain"]

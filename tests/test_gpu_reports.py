@@ -80,7 +80,7 @@ def _prefetch_kat():
                {1: P.r(0, -1)})
         p.flush()
     p.finish()
-    return p.to_json()
+    return p.to_dict()
 
 
 def test_prefetch_kat_second_chain_skips_tile0_upload():

@@ -219,3 +219,17 @@ def test_report_csv_schemas_match_reference():
     assert [l.split(",")[0] for l in loops[2:]] == ["0", "1"]
     assert rt.audit_csv() == "dataset,tile,uploaded,downloaded,d2d\n"
     assert rt.timeline_csv() == "command_id,kind,queue,bytes,issue,start,end\n"
+
+
+def test_fusion_plan_miniflow2d():
+    """Least-traffic legal partition: per iteration [L1-L6] (stencil reads of rho/e/v)
+    and [L7-L14] (L14's row-offset read of t3 recomputed from L10/L11 in-thread);
+    the fieldsum reduction runs alone. Unfused: one launch per loop."""
+    rt = B.Runtime("plan_only", record=True, tiles=1)
+    rt.run_app("miniflow2d", 64, 48, 0, 22)
+    c = rt.num_chains() - 2  # iterations 10..19: a full 10-iteration chain
+    fused = [g["loops"] for g in rt.chain_jit_check(c, fuse=True)] if B.jit_status() in (
+        "ok", "libcuda.so.1 (driver) not available") else None
+    if fused is not None:
+        assert fused == [6, 8] * 10 + [1]
+    assert [g["loops"] for g in rt.chain_jit_check(c, fuse=False)][:3] == [1, 1, 1]
