@@ -414,6 +414,11 @@ def set_jit(mode: int, min_points: int = -1) -> None:
         raise OocError("ooc_jit_config failed")
 
 
+def set_row_recompute(on: bool) -> None:
+    """Process-wide fusion policy (ooc_rt_set_row_recompute)."""
+    _native.lib().ooc_rt_set_row_recompute(int(bool(on)))
+
+
 def jit_report():
     """Autotuned tile shape of every specialised kernel (ooc_jit_report)."""
     _native.lib()

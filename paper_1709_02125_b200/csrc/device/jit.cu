@@ -674,8 +674,17 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
     return false;
   }
   const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17",
-                        "--prec-div=true", "--prec-sqrt=true", "--ftz=false", "-lineinfo"};
-  nvrtcResult rc = a.compile(prog, 7, opts);
+                        "--prec-div=true", "--prec-sqrt=true", "--ftz=false", "-lineinfo",
+                        "--ptxas-options=-v"};
+  static const bool verbose = std::getenv("OOC_JIT_VERBOSE") != nullptr;
+  nvrtcResult rc = a.compile(prog, verbose ? 8 : 7, opts);
+  if (verbose && rc == NVRTC_SUCCESS) {  // ptxas register / spill report (compile checks)
+    size_t n = 0;
+    a.log_size(prog, &n);
+    std::string log(n, '\0');
+    a.log(prog, log.data());
+    err = log;
+  }
   if (rc != NVRTC_SUCCESS) {
     size_t n = 0;
     a.log_size(prog, &n);
@@ -954,6 +963,7 @@ extern "C" int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, in
   if (!ok) err = "group exceeds the kernel template's capacity";
   Compiled k;
   if (ok) ok = compile(body, 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
+  if (ok && std::getenv("OOC_JIT_VERBOSE")) body = err + "\n" + body;
   if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", ok ? body.c_str() : err.c_str());
   return ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
 }

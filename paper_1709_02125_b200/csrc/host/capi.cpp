@@ -332,6 +332,8 @@ const char* ooc_rt_audit_json(ooc_runtime* h) {
   return out_str(w.str());
 }
 
+void ooc_rt_set_row_recompute(int on) { ooc::set_row_recompute(on != 0); }
+
 const char* ooc_rt_report_csv(ooc_runtime* h, const char* app, const char* size, int iters) {
   std::string s;
   int rc = guard([&] { s = h->rt->report_csv(app ? app : "", size ? size : "", iters); });

@@ -15,6 +15,7 @@
 // omits (kernels of tile t wait for the H2D of tile t).
 #include "ooc/gpu_engine.hpp"
 
+#include <cstdlib>
 #include <map>
 
 #include <cmath>
@@ -178,9 +179,21 @@ int GpuEngine::alloc_red_slot() {
 // recomputation. Reducing loops always run alone.
 namespace {
 
+// Row recompute trades DRAM bytes for registers; with the register-staged kernel
+// template the extra live values spill (8-loop miniflow2d group: 226-255 regs), so it
+// is opt-in (OOC_ROW_RECOMPUTE=1) until operands are staged in shared memory.
+int g_row_recompute = -1;  // -1: from the environment
+bool row_recompute_enabled() {
+  if (g_row_recompute < 0) {
+    const char* e = std::getenv("OOC_ROW_RECOMPUTE");
+    g_row_recompute = e && std::atoi(e) != 0;
+  }
+  return g_row_recompute != 0;
+}
+
 bool row_only(const Stencil& st, int ndim) {
   const int b = ndim - 2;
-  if (b < 0) return false;
+  if (b < 0 || !row_recompute_enabled()) return false;
   for (const Point& o : st.offsets)
     for (int d = 0; d < 3; ++d)
       if (d != b && o[d] != 0) return false;
@@ -225,6 +238,8 @@ bool recompute_inputs(const std::vector<const ParLoop*>& all, DatasetId d, std::
 }
 
 }  // namespace
+
+void set_row_recompute(bool on) { g_row_recompute = on ? 1 : 0; }
 
 bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, const ParLoop& b,
               bool enabled) {

@@ -31,6 +31,9 @@ LoweredLoop lower_loop(const ParLoop& loop);
 bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, const ParLoop& b,
               bool enabled);
 
+/// Process-wide: admit row-recompute fusion (default: OOC_ROW_RECOMPUTE env, off).
+void set_row_recompute(bool on);
+
 /// Fusion partition of a chain into consecutive launch groups: starts[j] = 1 where a
 /// launch begins. Among all partitions whose groups pass `can_fuse` (as the engine
 /// checks them, prefix by prefix) it picks the one with the least estimated DRAM

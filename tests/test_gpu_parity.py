@@ -236,6 +236,40 @@ def test_specialised_medium_apps(fuse, jit_always):
         assert dev["jit_launches"] == 0  # fresh context; counters are per runtime
 
 
+@pytest.fixture
+def row_recompute():
+    B.set_row_recompute(True)
+    yield
+    B.set_row_recompute(False)
+
+
+def test_row_recompute_fusion_parity(golden_random, row_recompute, jit_always):
+    """Groups fused through row recompute (neighbour reads of values written earlier in
+    the launch, re-evaluated in-thread) give the reference's bits — specialised
+    kernels, and the interpreter's loop-by-loop fallback."""
+    bad = []
+    for app, nx, ny, nz, iters in [("miniflow2d", 300, 256, 0, 12), ("miniflow3d", 40, 36, 30, 10)]:
+        prog = P.app_program(app, nx, ny, nz, iters=iters)
+        pb = B.problem_bytes(app, nx, ny, nz)
+        for kw in (dict(capacity=pb // 2), dict(tiles=1)):
+            want = oracle_record(prog, "explicit", **kw)
+            got = product_record(prog, "explicit", **kw)
+            want.pop("_rt", None)
+            got.pop("_rt", None)
+            if compare(want, got):
+                bad.append((app, kw))
+    B.set_jit(0, 1 << 18)  # interpreter: row-recompute groups run loop by loop
+    for case in golden_random[:30]:
+        prog = P.random_program(case["seed"], **case["kwargs"])
+        want = [w for w in case["runs"] if w["executor"] == "explicit"][0]
+        got = product_record(prog, "explicit", want["tiles"], want["capacity"], want["cyclic"],
+                             prefetch=want.get("prefetch", False))
+        got.pop("_rt", None)
+        if compare(want, got):
+            bad.append(case["seed"])
+    assert not bad, bad
+
+
 def test_slab_runtime_with_nccl_single_rank():
     """The multi-GPU path on one GPU: a 1-rank NCCL communicator, a dim-0 window with
     ghost rows, all-reduce of the fieldsum — same bits / same reduction as plain."""
