@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -29,6 +30,7 @@
 #include <tuple>
 #include <mutex>
 #include <sstream>
+#include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -59,6 +61,11 @@ struct Api {
   CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                      unsigned, CUstream, void**, void**) = nullptr;
   CUresult (*error_string)(CUresult, const char**) = nullptr;
+  CUresult (*func_set_attr)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*encode_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                           CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill) = nullptr;
 };
 
 Api& api() {
@@ -87,6 +94,9 @@ Api& api() {
     BIND(cu, get_function, "cuModuleGetFunction");
     BIND(cu, launch, "cuLaunchKernel");
     BIND(cu, error_string, "cuGetErrorString");
+    BIND(cu, func_set_attr, "cuFuncSetAttribute");
+    BIND(cu, occupancy, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+    BIND(cu, encode_tiled, "cuTensorMapEncodeTiled");
   }
 #undef BIND
   a.nvrtc_ok = a.create && a.compile && a.log_size && a.log && a.cubin_size && a.cubin && a.destroy;
@@ -115,6 +125,8 @@ struct Compiled {
   int block = 128;
   int Q = 1;
   int P = 4;
+  long long smem = 0;  // TMA template: dynamic shared memory per CTA (0: register template)
+  int occ = 1;         // TMA template: resident CTAs per SM
 };
 std::unordered_map<std::string, Compiled> g_cache;
 std::mutex g_cache_mu;
@@ -129,7 +141,7 @@ std::mutex g_cache_mu;
 // rows per Q outputs instead of 3 per output; then each point evaluates the loops
 // in order with values produced earlier in the launch forwarded in registers, and
 // stores.
-const char* kTemplate = R"CUDA(
+const char* kCommon = R"CUDA(
 struct JitParams {
   long long nA, nB, nC;
   double* part;
@@ -143,6 +155,7 @@ struct JitParams {
   double* wp[OOC_JMAX_WRITES];
   long long wsA[OOC_JMAX_WRITES], wsB[OOC_JMAX_WRITES];
   double cst[OOC_JMAX_CONST];
+  int tv_org[OOC_JMAX_VIEWS][3];
 };
 __device__ __forceinline__ double ooc_min(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double ooc_max(double a, double b) { return a < b ? b : a; }
@@ -151,6 +164,9 @@ __device__ __forceinline__ double ooc_red(int op, double acc, double v) {
   if (op == 2) return v < acc ? v : acc;
   return acc < v ? v : acc;
 }
+)CUDA";
+
+const char* kRegKernel = R"CUDA(
 extern "C" __global__ void __launch_bounds__(OOC_BLOCK) ooc_jit_kernel(const __grid_constant__ JitParams p) {
   const long long nBq = (p.nB + OOC_Q - 1) / OOC_Q;
   const long long rows = p.nA * nBq;
@@ -189,6 +205,105 @@ extern "C" __global__ void __launch_bounds__(OOC_BLOCK) ooc_jit_kernel(const __g
 }
 )CUDA";
 
+// The shared-memory-staged kernel (B200 TMA path). Persistent CTAs walk the tiles
+// of the launch box (OOC_TB rows x OOC_TC columns of one plane); for every dataset
+// view the group reads, one thread issues a TMA tensor load of the tile's box
+// widened by the view's stencil reach (zero-filled outside the view, exactly the
+// register template's out-of-bounds rule) into an OOC_STAGES-deep ring of shared
+// memory stages, completing on an mbarrier — so DRAM streams while the previous
+// tile computes and no thread holds operands in registers. Each thread then
+// evaluates the loops point by point from shared memory (same tape order, same
+// forwarding and row recompute as the register template) and stores its outputs.
+const char* kTmaKernel = R"CUDA(
+struct __align__(64) TmaMaps { unsigned long long t[OOC_JMAX_VIEWS][16]; };
+__device__ __forceinline__ unsigned ooc_smem(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ooc_mbar_wait(unsigned bar, unsigned phase) {
+  asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n"
+               " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               " @!P1 bra WAIT_%=;\n}\n" :: "r"(bar), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void ooc_tma(unsigned dst, const void* map, int x, int y, int z, unsigned bar) {
+#if OOC_RANK == 1
+  asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2}], [%3];" :: "r"(dst), "l"(map), "r"(x), "r"(bar) : "memory");
+#elif OOC_RANK == 2
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3}], [%4];" :: "r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar) : "memory");
+#else
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+               " [%0], [%1, {%2, %3, %4}], [%5];" :: "r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+               : "memory");
+#endif
+}
+extern "C" __global__ void __launch_bounds__(OOC_THREADS) ooc_jit_kernel(const __grid_constant__ JitParams p,
+                                                                       const __grid_constant__ TmaMaps m) {
+  extern __shared__ __align__(128) unsigned char ooc_sm[];
+  __shared__ __align__(8) unsigned long long bar[OOC_STAGES];
+  const long long tC = (p.nC + OOC_TC - 1) / OOC_TC, tB = (p.nB + OOC_TB - 1) / OOC_TB;
+  const long long ntiles = p.nA * tB * tC;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OOC_STAGES; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(ooc_smem(&bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](long long tile, int s) {
+    const long long ia = tile / (tB * tC), rem = tile - ia * tB * tC;
+    const int ib0 = static_cast<int>((rem / tC) * OOC_TB), c0 = static_cast<int>((rem % tC) * OOC_TC);
+    const int a0 = static_cast<int>(ia);
+    const unsigned b = ooc_smem(&bar[s]);
+    const unsigned base = ooc_smem(ooc_sm) + s * OOC_STAGE_BYTES;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(OOC_STAGE_BYTES) : "memory");
+<<ISSUE>>
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < OOC_STAGES; ++s) {
+      const long long t = blockIdx.x + static_cast<long long>(s) * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+#if OOC_RED
+  double acc = p.red_op == 2 ? __longlong_as_double(0x7ff0000000000000LL)
+             : p.red_op == 3 ? __longlong_as_double(0xfff0000000000000LL) : 0.0;
+#endif
+  int k = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = k % OOC_STAGES;
+    ooc_mbar_wait(ooc_smem(&bar[s]), static_cast<unsigned>((k / OOC_STAGES) & 1));
+    const double* S = reinterpret_cast<const double*>(ooc_sm + s * OOC_STAGE_BYTES);
+    const long long ia = tile / (tB * tC), rem = tile - ia * tB * tC;
+    const long long ib0 = (rem / tC) * OOC_TB, c0 = (rem % tC) * OOC_TC;
+    const int lc = threadIdx.x % OOC_TC;
+#pragma unroll 1
+    for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
+      const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
+      const long long bq = ib0 + lr, c = c0 + lc;
+      const bool okp = bq < p.nB && c < p.nC;
+<<BODY>>
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long nt = tile + static_cast<long long>(OOC_STAGES) * gridDim.x;
+      if (nt < ntiles) issue(nt, s);
+    }
+  }
+#if OOC_RED
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = ooc_red(p.red_op, acc, __shfl_down_sync(0xffffffffu, acc, o));
+  __shared__ double warp_part[OOC_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = warp_part[0];
+    for (int i = 1; i < OOC_THREADS / 32; ++i) b = ooc_red(p.red_op, b, warp_part[i]);
+    p.part[blockIdx.x] = b;
+  }
+#endif
+}
+)CUDA";
+
 struct Canon {
   int A, B, C;
 };
@@ -204,7 +319,39 @@ struct Family {
 
 struct Shape {
   int Q = 1, P = 4;
+  int tb = 0, tc = 0;  // > 0: shared-memory-staged TMA template with OOC_TB x OOC_TC tiles
+  bool tma() const { return tb > 0; }
+  std::string name() const {
+    return tma() ? "t" + std::to_string(tb) + "x" + std::to_string(tc)
+                 : std::to_string(Q) + "x" + std::to_string(P);
+  }
 };
+
+// Host-side plan of the TMA template: one staged box per dataset view read.
+struct TmaView {
+  const ooc_view* v;
+  int64_t omin[3], omax[3];  // canonical (A, B, C) offset reach, including recompute shifts
+  int box[3];                // TMA box (C, B, A)
+  long long off;             // element offset inside a stage
+};
+struct TmaPlan {
+  int rank = 2;
+  int stages = 2;
+  long long stage_bytes = 0;
+  std::vector<TmaView> views;
+};
+constexpr int kTmaThreads = 256;
+
+// "QxP" (register template) or "tTBxTC" (TMA template)
+bool parse_shape(const char* txt, Shape& f) {
+  if (!txt || !*txt) return false;
+  if (txt[0] == 't') {
+    f = Shape{1, 1, 0, 0};
+    return std::sscanf(txt + 1, "%dx%d", &f.tb, &f.tc) == 2 && f.tb >= 1 && f.tc >= 1 && 256 % f.tc == 0 &&
+           f.tb % (256 / f.tc) == 0;
+  }
+  return std::sscanf(txt, "%dx%d", &f.Q, &f.P) == 2 && f.Q >= 1 && f.P >= 1;
+}
 
 // Generate the body + parameter block of a group for tile shape (Q, P). Returns
 // false when the group exceeds the template's capacity (caller falls back).
@@ -615,20 +762,332 @@ bool generate(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::st
   return true;
 }
 
+// The TMA template's body: same loop semantics as generate() (tape order, forwarding
+// of values written earlier at the point, row recompute), operands read from the
+// shared-memory boxes of the staged views.
+bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std::string& body,
+                  int& red_op, TmaPlan* plan_out) {
+  std::memset(&jp, 0, sizeof jp);
+  const int nd = Ls[0].ndim;
+  if (nd < 2 || n > OOC_JMAX_LOOPS) return false;
+  const Canon cn = canon(nd);
+  int64_t lo[3], hi[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = Ls[0].lo[d];
+    hi[d] = Ls[0].hi[d];
+    for (int i = 1; i < n; ++i) {
+      lo[d] = std::min(lo[d], Ls[i].lo[d]);
+      hi[d] = std::max(hi[d], Ls[i].hi[d]);
+    }
+  }
+  auto ext = [&](int d) { return d < 0 ? 1LL : static_cast<long long>(hi[d] - lo[d]); };
+  jp.nA = ext(cn.A);
+  jp.nB = ext(cn.B);
+  jp.nC = ext(cn.C);
+  red_op = n == 1 ? Ls[0].reduce_op : OOC_RED_NONE;
+  for (int i = 0; i < n; ++i) {
+    if (Ls[i].ndim != nd) return false;
+    if (n > 1 && Ls[i].reduce_op != OOC_RED_NONE) return false;
+    for (int a = 0; a < Ls[i].nargs; ++a) {
+      const ooc_view& v = Ls[i].args[a];
+      if (v.stride[cn.C] != 1) return false;
+      if (reinterpret_cast<uintptr_t>(v.data) % 16 != 0) return false;
+      for (int d = 0; d < nd - 1; ++d)
+        if ((v.stride[d] * 8) % 16 != 0) return false;
+    }
+  }
+  jp.red_op = red_op;
+  auto off_of = [&](const int64_t* o, int d) { return d < 0 ? int64_t{0} : o[d]; };
+  auto zero = [](const int64_t* o) { return o[0] == 0 && o[1] == 0 && o[2] == 0; };
+  auto tape_of = [&](int i, int w) {
+    const ooc_ins* t = Ls[i].tape;
+    for (int k = 0; k < w; ++k) t += Ls[i].write_len[k];
+    return t;
+  };
+  auto last_writer = [&](const double* data, int before, int* wout) -> int {
+    for (int i = before - 1; i >= 0; --i)
+      for (int w = 0; w < Ls[i].nwrites; ++w)
+        if (Ls[i].args[Ls[i].write_arg[w]].data == data) {
+          *wout = w;
+          return i;
+        }
+    return -1;
+  };
+  // loop j's points shifted by s rows all lie in loop a's range
+  auto covers = [&](int a, int j, int s) {
+    for (int d = 0; d < nd; ++d) {
+      const int64_t sh_d = d == cn.B ? s : 0;
+      if (Ls[j].lo[d] + sh_d < Ls[a].lo[d] || Ls[j].hi[d] + sh_d > Ls[a].hi[d]) return false;
+    }
+    return true;
+  };
+  for (int i = 0; i < n; ++i) {
+    int* r = jp.rng[i];
+    auto rel = [&](int d, bool upper) -> int {
+      if (d < 0) return upper ? 1 : 0;
+      return static_cast<int>((upper ? Ls[i].hi[d] : Ls[i].lo[d]) - lo[d]);
+    };
+    r[0] = rel(cn.A, false);
+    r[1] = rel(cn.A, true);
+    r[2] = rel(cn.B, false);
+    r[3] = rel(cn.B, true);
+    r[4] = rel(cn.C, false);
+    r[5] = rel(cn.C, true);
+  }
+  // ---- staged views
+  TmaPlan plan;
+  plan.rank = nd;
+  auto view_of = [&](const ooc_view& v) -> int {
+    for (std::size_t k = 0; k < plan.views.size(); ++k)
+      if (plan.views[k].v->data == v.data) return static_cast<int>(k);
+    TmaView tv{&v, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}, 0};
+    for (int d = 0; d < 3; ++d) {
+      tv.omin[d] = INT64_MAX;
+      tv.omax[d] = INT64_MIN;
+    }
+    plan.views.push_back(tv);
+    return static_cast<int>(plan.views.size()) - 1;
+  };
+  bool final_pass = false;
+  std::ostringstream out;
+  // operand: view v at canonical offset (oa, ob, oc) from the point
+  auto smem = [&](const ooc_view& v, int64_t oa, int64_t ob, int64_t oc) -> std::string {
+    const int k = view_of(v);
+    TmaView& t = plan.views[k];
+    const int64_t o[3] = {oa, ob, oc};
+    if (!final_pass) {
+      for (int d = 0; d < 3; ++d) {
+        t.omin[d] = std::min(t.omin[d], o[d]);
+        t.omax[d] = std::max(t.omax[d], o[d]);
+      }
+      return "0.0";
+    }
+    const long long WC = t.box[0], HB = t.box[1];
+    const long long K = t.off + ((oa - t.omin[0]) * HB + (ob - t.omin[1])) * WC + (oc - t.omin[2]);
+    return "S[" + std::to_string(K) + " + lr * " + std::to_string(WC) + " + lc]";
+  };
+  auto smem_at = [&](const ooc_view& v, const int64_t* o, int64_t shift) {
+    return smem(v, off_of(o, cn.A), off_of(o, cn.B) + shift, off_of(o, cn.C));
+  };
+  int ncst = 0, nwrite = 0;
+  std::vector<std::vector<std::vector<int>>> cst_idx;
+  std::map<std::tuple<int, int, int, int>, std::string> memo;
+  int rc_count = 0;
+  const int64_t zo[3] = {0, 0, 0};
+  auto active_at = [&](int a, int s) {
+    const std::string as = std::to_string(a), bs = "(bq + (" + std::to_string(s) + "))";
+    return "(ia >= p.rng[" + as + "][0] && ia < p.rng[" + as + "][1] && " + bs + " >= p.rng[" + as +
+           "][2] && " + bs + " < p.rng[" + as + "][3] && c >= p.rng[" + as + "][4] && c < p.rng[" + as +
+           "][5])";
+  };
+  // emit a tape; reads resolved by `rd`; returns the result symbol
+  std::function<std::string(int, int, int, int)> rc;
+  auto emit_tape = [&](const ooc_ins* t, int len, const std::string& tag, int loop, int wi, bool fresh_cst,
+                       const std::function<std::string(const ooc_ins&)>& rd) -> std::string {
+    std::vector<std::string> st;
+    int tmp = 0;
+    std::size_t ci = 0;
+    for (int k = 0; k < len; ++k) {
+      const ooc_ins& in = t[k];
+      if (in.op == OOC_OP_CONST) {
+        int idx;
+        if (fresh_cst) {
+          if (ncst >= OOC_JMAX_CONST) throw std::runtime_error("constants");
+          jp.cst[ncst] = in.value;
+          idx = ncst++;
+          if (wi >= 0) cst_idx[loop][wi].push_back(idx);
+        } else {
+          idx = cst_idx[loop][wi].at(ci++);
+        }
+        st.push_back("p.cst[" + std::to_string(idx) + "]");
+      } else if (in.op == OOC_OP_READ) {
+        st.push_back(rd(in));
+      } else if (in.op >= OOC_OP_ADD && in.op <= OOC_OP_MAX) {
+        if (st.size() < 2) throw std::runtime_error("stack");
+        std::string y = st.back();
+        st.pop_back();
+        std::string x = st.back();
+        st.pop_back();
+        const std::string name = tag + std::to_string(tmp++);
+        out << "      const double " << name << " = ";
+        switch (in.op) {
+          case OOC_OP_ADD: out << x << " + " << y; break;
+          case OOC_OP_SUB: out << x << " - " << y; break;
+          case OOC_OP_MUL: out << x << " * " << y; break;
+          case OOC_OP_DIV: out << x << " / " << y; break;
+          case OOC_OP_MIN: out << "ooc_min(" << x << ", " << y << ")"; break;
+          default: out << "ooc_max(" << x << ", " << y << ")"; break;
+        }
+        out << ";\n";
+        st.push_back(name);
+      } else {
+        throw std::runtime_error("op");
+      }
+    }
+    if (st.size() != 1) throw std::runtime_error("stack");
+    return st.back();
+  };
+  // value of loop a's write w at row bq+s, as needed by reader j
+  rc = [&](int a, int w, int s, int j) -> std::string {
+    auto key = std::make_tuple(a, w, s, j);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    const ooc_view& X = Ls[a].args[Ls[a].write_arg[w]];
+    std::string res;
+    if (s == 0) {
+      const std::string o = "o" + std::to_string(a) + "_" + std::to_string(w);
+      res = covers(a, j, 0) ? o : "(a" + std::to_string(a) + " ? " + o + " : " + smem_at(X, zo, 0) + ")";
+    } else {
+      const std::string tag = "r" + std::to_string(rc_count++) + "_";
+      const std::string e = emit_tape(tape_of(a, w), Ls[a].write_len[w], tag, a, w, false,
+                                      [&](const ooc_ins& in) -> std::string {
+        const ooc_view& v = Ls[a].args[in.arg];
+        int vw = 0;
+        const int src = last_writer(v.data, a, &vw);
+        const int64_t ob = s + off_of(in.offset, cn.B);
+        if (src >= 0) return rc(src, vw, static_cast<int>(ob), j);
+        return smem_at(v, in.offset, s);
+      });
+      if (covers(a, j, s)) {
+        res = e;
+      } else {
+        res = tag + "v";
+        out << "      const double " << res << " = " << active_at(a, s) << " ? " << e << " : "
+            << smem_at(X, zo, s) << ";\n";
+      }
+    }
+    return memo[key] = res;
+  };
+  auto run = [&]() -> bool {
+    out.str("");
+    ncst = 0;
+    nwrite = 0;
+    rc_count = 0;
+    memo.clear();
+    cst_idx.assign(n, {});
+    for (int i = 0; i < n; ++i) cst_idx[i].resize(Ls[i].nwrites);
+    struct Writer {
+      const double* data;
+      int loop;
+      std::string sym;
+    };
+    std::vector<Writer> writers;
+    for (int i = 0; i < n; ++i) {
+      const ooc_loop& L = Ls[i];
+      const std::string is = std::to_string(i);
+      out << "      const bool a" << is << " = okp && ia >= p.rng[" << is << "][0] && ia < p.rng[" << is
+          << "][1] && bq >= p.rng[" << is << "][2] && bq < p.rng[" << is << "][3] && c >= p.rng[" << is
+          << "][4] && c < p.rng[" << is << "][5];\n";
+      auto rd = [&](const ooc_ins& in) -> std::string {
+        const ooc_view& v = L.args[in.arg];
+        int w = 0;
+        const int src = last_writer(v.data, i, &w);
+        if (src < 0) return smem_at(v, in.offset, 0);
+        if (!zero(in.offset)) return rc(src, w, static_cast<int>(off_of(in.offset, cn.B)), i);
+        // forwarded: the newest writer active at the point, else older ones, else memory
+        std::function<std::string(int)> layer = [&](int idx) -> std::string {
+          if (idx < 0) return smem_at(v, zo, 0);
+          const Writer& wr = writers[static_cast<std::size_t>(idx)];
+          if (wr.data != v.data) return layer(idx - 1);
+          if (covers(wr.loop, i, 0)) return wr.sym;
+          return "(a" + std::to_string(wr.loop) + " ? " + wr.sym + " : " + layer(idx - 1) + ")";
+        };
+        return layer(static_cast<int>(writers.size()) - 1);
+      };
+      const ooc_ins* t = L.tape;
+      for (int w = 0; w < L.nwrites; ++w) {
+        const std::string e = emit_tape(t, L.write_len[w], "t" + is + "_" + std::to_string(w) + "_", i, w, true, rd);
+        out << "      const double o" << is << "_" << w << " = " << e << ";\n";
+        t += L.write_len[w];
+      }
+      if (L.reduce_op != OOC_RED_NONE) {
+        const std::string e = emit_tape(t, L.reduce_len, "t" + is + "_r_", i, -1, true, rd);
+        out << "#if OOC_RED\n      if (a" << is << ") acc = ooc_red(p.red_op, acc, " << e << ");\n#endif\n";
+      }
+      for (int w = 0; w < L.nwrites; ++w) {
+        if (nwrite >= OOC_JMAX_WRITES) return false;
+        const ooc_view& v = L.args[L.write_arg[w]];
+        long long off = 0;
+        for (int d = 0; d < 3; ++d) off += (lo[d] - v.lo[d]) * v.stride[d];
+        jp.wp[nwrite] = v.data + off;
+        jp.wsA[nwrite] = cn.A < 0 ? 0 : v.stride[cn.A];
+        jp.wsB[nwrite] = v.stride[cn.B];
+        const std::string ws = std::to_string(nwrite);
+        const std::string sym = "o" + is + "_" + std::to_string(w);
+        out << "      if (a" << is << ") p.wp[" << ws << "][ia * p.wsA[" << ws << "] + bq * p.wsB[" << ws
+            << "] + c] = " << sym << ";\n";
+        writers.push_back({v.data, i, sym});
+        ++nwrite;
+      }
+    }
+    return true;
+  };
+  try {
+    if (!run()) return false;  // pass 1: collect each view's reach
+    if (plan.views.empty() || static_cast<int>(plan.views.size()) > OOC_JMAX_VIEWS) return false;
+    long long off = 0;
+    for (TmaView& t : plan.views) {
+      for (int d = 0; d < 3; ++d) {  // canonical dims absent from the rank: no reach
+        const int cd = d == 0 ? cn.A : d == 1 ? cn.B : cn.C;
+        if (cd < 0) t.omin[d] = t.omax[d] = 0;
+      }
+      long long wc = sh.tc + (t.omax[2] - t.omin[2]);
+      wc = (wc + 1) / 2 * 2;  // TMA: inner box bytes a multiple of 16
+      const long long hb = sh.tb + (t.omax[1] - t.omin[1]);
+      const long long da = 1 + (t.omax[0] - t.omin[0]);
+      if (wc > 256 || hb > 256 || da > 256) return false;
+      t.box[0] = static_cast<int>(wc);
+      t.box[1] = static_cast<int>(hb);
+      t.box[2] = static_cast<int>(da);
+      t.off = off;
+      off += (wc * hb * da + 15) / 16 * 16;  // 128-byte aligned boxes
+    }
+    plan.stage_bytes = off * 8;
+    const long long budget = 200 * 1024;
+    plan.stages = plan.stage_bytes * 3 <= budget ? 3 : plan.stage_bytes * 2 <= budget + 20 * 1024 ? 2 : 0;
+    if (plan.stages == 0) return false;
+    std::memset(jp.cst, 0, sizeof jp.cst);
+    final_pass = true;
+    if (!run()) return false;
+  } catch (const std::exception&) {
+    return false;
+  }
+  for (std::size_t k = 0; k < plan.views.size(); ++k) {
+    const TmaView& t = plan.views[k];
+    const ooc_view& v = *t.v;
+    const int dims[3] = {cn.C, cn.B, cn.A};
+    const int64_t om[3] = {t.omin[2], t.omin[1], t.omin[0]};
+    for (int e = 0; e < 3; ++e)
+      jp.tv_org[k][e] = dims[e] < 0 ? 0 : static_cast<int>(lo[dims[e]] - v.lo[dims[e]] + om[e]);
+  }
+  std::ostringstream issue, defs;
+  for (std::size_t k = 0; k < plan.views.size(); ++k) {
+    const std::string ks = std::to_string(k);
+    issue << "    ooc_tma(base + " << plan.views[k].off * 8 << "u, &m.t[" << ks << "][0], p.tv_org[" << ks
+          << "][0] + c0, p.tv_org[" << ks << "][1] + ib0, p.tv_org[" << ks << "][2] + a0, b);\n";
+  }
+  defs << "#define OOC_TB " << sh.tb << "\n#define OOC_TC " << sh.tc << "\n#define OOC_THREADS " << kTmaThreads
+       << "\n#define OOC_STAGES " << plan.stages << "\n#define OOC_STAGE_BYTES " << plan.stage_bytes
+       << "\n#define OOC_RANK " << nd << "\n";
+  body = "<<TMA>>\n" + defs.str() + "<<ISSUE>>\n" + issue.str() + "<<TBODY>>\n" + out.str();
+  if (plan_out) *plan_out = plan;
+  return true;
+}
+
 // Tile shape: as many rows per thread as keeps the loaded values in registers.
 bool pick_and_generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& body, int& red_op,
                        Shape& sh) {
   const bool flat = Ls[0].ndim == 1;
-  static const char* forced = std::getenv("OOC_JIT_SHAPE");  // "QxP" (experiments)
-  if (forced && *forced) {
-    Shape f;
-    if (std::sscanf(forced, "%dx%d", &f.Q, &f.P) == 2 && f.Q >= 1 && f.P >= 1) {
-      if (flat) f.Q = 1;
-      int values = 0;
-      if (!generate(Ls, n, f, jp, body, red_op, &values)) return false;
-      sh = f;
-      return true;
-    }
+  static const char* forced = std::getenv("OOC_JIT_SHAPE");  // "QxP" / "tTBxTC" (experiments)
+  Shape f;
+  if (parse_shape(forced, f)) {
+    if (flat) f.Q = 1;
+    int values = 0;
+    if (f.tma() ? !generate_tma(Ls, n, f, jp, body, red_op, nullptr)
+                : !generate(Ls, n, f, jp, body, red_op, &values))
+      return false;
+    sh = f;
+    return true;
   }
   static const Shape cands2d[] = {{4, 2}, {2, 2}, {1, 2}, {1, 1}};
   static const Shape cands1d[] = {{1, 4}, {1, 2}, {1, 1}};
@@ -648,7 +1107,7 @@ bool pick_and_generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& bo
 // load = false: compile only (checks that the generated kernel builds for sm_100a;
 // needs NVRTC but no driver/GPU).
 bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled& out,
-             std::string& err, bool load = true) {
+             std::string& err, bool load = true, long long smem = 0) {
   Api& a = api();
   if (load ? !a.ok : !a.nvrtc_ok) {
     err = a.why;
@@ -660,14 +1119,24 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
                     "\n#define OOC_JMAX_LOOPS " + std::to_string(OOC_JMAX_LOOPS) +
                     "\n#define OOC_JMAX_FAMILIES " + std::to_string(OOC_JMAX_FAMILIES) +
                     "\n#define OOC_JMAX_WRITES " + std::to_string(OOC_JMAX_WRITES) +
-                    "\n#define OOC_JMAX_CONST " + std::to_string(OOC_JMAX_CONST) + "\n";
-  std::string tpl = kTemplate;
-  const std::size_t fpos = key.find("<<FAST>>\n");
-  const std::string slow_body = key.substr(9, fpos - 9);  // after "<<SLOW>>\n"
-  const std::string fast_body = key.substr(fpos + 9);
-  tpl.replace(tpl.find("<<FAST>>"), 8, fast_body);
-  tpl.replace(tpl.find("<<BODY>>"), 8, slow_body);
-  src += tpl;
+                    "\n#define OOC_JMAX_CONST " + std::to_string(OOC_JMAX_CONST) +
+                    "\n#define OOC_JMAX_VIEWS " + std::to_string(OOC_JMAX_VIEWS) + "\n";
+  if (key.rfind("<<TMA>>\n", 0) == 0) {
+    // "<<TMA>>\n" defines "<<ISSUE>>\n" issue-code "<<TBODY>>\n" point-body
+    const std::size_t ip = key.find("<<ISSUE>>\n"), bp = key.find("<<TBODY>>\n");
+    std::string tpl = std::string(kCommon) + kTmaKernel;
+    tpl.replace(tpl.find("<<ISSUE>>"), 9, key.substr(ip + 10, bp - ip - 10));
+    tpl.replace(tpl.find("<<BODY>>"), 8, key.substr(bp + 10));
+    src += key.substr(8, ip - 8) + tpl;
+  } else {
+    std::string tpl = std::string(kCommon) + kRegKernel;
+    const std::size_t fpos = key.find("<<FAST>>\n");
+    const std::string slow_body = key.substr(9, fpos - 9);  // after "<<SLOW>>\n"
+    const std::string fast_body = key.substr(fpos + 9);
+    tpl.replace(tpl.find("<<FAST>>"), 8, fast_body);
+    tpl.replace(tpl.find("<<BODY>>"), 8, slow_body);
+    src += tpl;
+  }
   nvrtcProgram prog;
   if (a.create(&prog, src.c_str(), "ooc_par_loop.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     err = "nvrtcCreateProgram failed";
@@ -715,6 +1184,22 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
   out.block = block;
   out.Q = Q;
   out.P = P;
+  out.smem = smem;
+  out.occ = 1;
+  if (smem > 0) {
+    if (!a.func_set_attr || !a.occupancy ||
+        a.func_set_attr(out.fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, static_cast<int>(smem)) !=
+            CUDA_SUCCESS) {
+      err = "cuFuncSetAttribute(max dynamic smem) failed";
+      return false;
+    }
+    int occ = 0;
+    if (a.occupancy(&occ, out.fn, block, static_cast<size_t>(smem)) != CUDA_SUCCESS || occ < 1) {
+      err = "TMA kernel does not fit on an SM";
+      return false;
+    }
+    out.occ = occ;
+  }
   return true;
 }
 
@@ -739,12 +1224,11 @@ std::unordered_map<std::string, Tuning> g_tune;
 // of a short contiguous row (3-D grids) are replaced by narrower ones.
 std::vector<Shape> candidates(int ndim, long long nC) {
   static const char* forced = std::getenv("OOC_JIT_SHAPE");
-  if (forced && *forced) {
-    Shape f;
-    if (std::sscanf(forced, "%dx%d", &f.Q, &f.P) == 2 && f.Q >= 1 && f.P >= 1) {
-      if (ndim == 1) f.Q = 1;
-      return {f};
-    }
+  Shape f;
+  if (parse_shape(forced, f)) {
+    if (ndim == 1) f.Q = 1;
+    if (f.tma()) return {Shape{1, 4}, f};  // register fallback for unaligned launches
+    return {f};
   }
   if (ndim == 1) return {{1, 4}, {1, 8}, {1, 2}};
   auto waste = [&](int P) {
@@ -756,6 +1240,19 @@ std::vector<Shape> candidates(int ndim, long long nC) {
                   Shape{8, 1}})
     if (waste(s.P) <= 0.2 && out.size() < 4) out.push_back(s);
   if (out.empty()) out = {{4, 1}, {8, 1}, {2, 1}};
+  // shared-memory-staged (TMA) tiles: OOC_TB rows x OOC_TC columns
+  static const bool no_tma = std::getenv("OOC_JIT_NO_TMA") != nullptr;
+  if (!no_tma) {
+    auto twaste = [&](int tc) {
+      return static_cast<double>((nC + tc - 1) / tc * tc) / static_cast<double>(nC) - 1.0;
+    };
+    int added = 0;
+    for (Shape s : {Shape{1, 1, 16, 64}, Shape{1, 1, 8, 128}, Shape{1, 1, 32, 32}, Shape{1, 1, 64, 32}})
+      if (twaste(s.tc) <= 0.2 && added < 2) {
+        out.push_back(s);
+        ++added;
+      }
+  }
   return out;
 }
 
@@ -770,8 +1267,9 @@ const std::unordered_map<std::size_t, Shape>& preset_shapes() {
   if (!fp) return m;
   char hex[64];
   Shape sh;
-  while (std::fscanf(fp, "%63s %dx%d", hex, &sh.Q, &sh.P) == 3)
-    m[static_cast<std::size_t>(std::strtoull(hex, nullptr, 16))] = sh;
+  char name[32];
+  while (std::fscanf(fp, "%63s %31s", hex, name) == 2)
+    if (parse_shape(name, sh)) m[static_cast<std::size_t>(std::strtoull(hex, nullptr, 16))] = sh;
   std::fclose(fp);
   return m;
 }
@@ -799,13 +1297,16 @@ void settle(Tuning& T) {
 // Generate the group's kernel for tile shape `sh` (filling `jp`) and fetch or
 // compile its binary. Caller holds g_cache_mu.
 bool compiled_for(ooc_ctx* c, const ooc_loop* Ls, int n, const Shape& sh, bool red, JitParams& jp,
-                  Compiled& k, std::string& err) {
+                  Compiled& k, std::string& err, TmaPlan* plan = nullptr) {
   std::string body;
   int red_op = OOC_RED_NONE;
-  if (!generate(Ls, n, sh, jp, body, red_op, nullptr)) {
+  TmaPlan local;
+  if (sh.tma() ? !generate_tma(Ls, n, sh, jp, body, red_op, plan ? plan : &local)
+               : !generate(Ls, n, sh, jp, body, red_op, nullptr)) {
     err = "group exceeds the kernel template's capacity";
     return false;
   }
+  const TmaPlan& pl = plan ? *plan : local;
   const std::string key = body + "|Q" + std::to_string(sh.Q) + "P" + std::to_string(sh.P) +
                           (red ? "|red" : "|nored");
   auto it = g_cache.find(key);
@@ -814,7 +1315,9 @@ bool compiled_for(ooc_ctx* c, const ooc_loop* Ls, int n, const Shape& sh, bool r
     return true;
   }
   auto t0 = std::chrono::steady_clock::now();
-  if (!compile(body, 128, sh.Q, sh.P, red, k, err)) return false;
+  if (!compile(body, sh.tma() ? kTmaThreads : 128, sh.Q, sh.P, red, k, err, true,
+               sh.tma() ? pl.stages * pl.stage_bytes : 0))
+    return false;
   c->stats.jit_compiles++;
   c->stats.jit_compile_ms += static_cast<long long>(
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
@@ -854,7 +1357,14 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   std::lock_guard<std::mutex> lk(g_cache_mu);
   Tuning& T = g_tune[body + (red ? "|red" : "|nored")];
   if (T.cands.empty()) {
-    T.cands = candidates(Ls[0].ndim, jp->nC);
+    // compile every candidate now (first sight of this structure, normally a
+    // warm-up chain) so later launches never wait for NVRTC; shapes whose kernel
+    // cannot be built (shared-memory budget, TMA box limits) drop out
+    for (const Shape& cs : candidates(Ls[0].ndim, jp->nC)) {
+      Compiled kk;
+      std::string e2;
+      if (compiled_for(c, Ls, n, cs, red, *jp, kk, e2) || !cs.tma()) T.cands.push_back(cs);
+    }
     T.ns_per_point.assign(T.cands.size(), -1.f);
     T.ev.resize(T.cands.size());
     T.points.assign(T.cands.size(), 0);
@@ -866,14 +1376,7 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     auto ps = pre.find(std::hash<std::string>{}(body + (red ? "|red" : "|nored")));
     if (ps != pre.end())
       for (std::size_t i = 0; i < T.cands.size(); ++i)
-        if (T.cands[i].Q == ps->second.Q && T.cands[i].P == ps->second.P) T.best = static_cast<int>(i);
-    // compile every candidate now (first sight of this structure, normally a
-    // warm-up chain) so later launches never wait for NVRTC
-    for (const Shape& cs : T.cands) {
-      Compiled kk;
-      std::string e2;
-      compiled_for(c, Ls, n, cs, red, *jp, kk, e2);
-    }
+        if (T.cands[i].name() == ps->second.name()) T.best = static_cast<int>(i);
   }
   if (T.best < 0) settle(T);
   int pick = T.best;
@@ -893,10 +1396,21 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
       timing = true;
     }
   }
-  const Shape sh = T.cands[pick];
+  Shape sh = T.cands[pick];
   Compiled k;
   std::string err;
-  if (!compiled_for(c, Ls, n, sh, red, *jp, k, err)) {
+  TmaPlan plan;
+  bool built = compiled_for(c, Ls, n, sh, red, *jp, k, err, &plan);
+  if (!built && sh.tma()) {  // e.g. a view not 16-byte aligned at this launch
+    timing = false;
+    for (const Shape& cs : T.cands)
+      if (!cs.tma()) {
+        sh = cs;
+        built = compiled_for(c, Ls, n, sh, red, *jp, k, err);
+        break;
+      }
+  }
+  if (!built) {
     delete jp;
     if (m == 2) {
       set_error("JIT: " + err);
@@ -907,7 +1421,47 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   const long long rows = jp->nA * ((jp->nB + k.Q - 1) / k.Q);
   const long long xblocks = (jp->nC + k.block * k.P - 1) / (k.block * k.P);
   unsigned gx = static_cast<unsigned>(std::min<long long>(xblocks, 1 << 20)), gy;
-  if (red) {
+  struct alignas(64) HostMaps {
+    CUtensorMap t[OOC_JMAX_VIEWS];
+  };
+  HostMaps* maps = nullptr;
+  if (sh.tma()) {
+    // persistent CTAs over the tiles; one tensor map per staged view
+    maps = new HostMaps;
+    std::memset(maps, 0, sizeof *maps);
+    const Canon cn = canon(plan.rank);
+    for (std::size_t v = 0; v < plan.views.size(); ++v) {
+      const TmaView& tv = plan.views[v];
+      const ooc_view& w = *tv.v;
+      const int dims[3] = {cn.C, cn.B, cn.A};
+      cuuint64_t gdim[3], gstr[2];
+      cuuint32_t box[3], es[3] = {1, 1, 1};
+      for (int e = 0; e < plan.rank; ++e) {
+        gdim[e] = static_cast<cuuint64_t>(w.hi[dims[e]] - w.lo[dims[e]]);
+        box[e] = static_cast<cuuint32_t>(tv.box[e]);
+        if (e > 0) gstr[e - 1] = static_cast<cuuint64_t>(w.stride[dims[e]]) * 8;
+      }
+      CUresult er = api().encode_tiled(&maps->t[v], CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                                       static_cast<cuuint32_t>(plan.rank), const_cast<double*>(w.data),
+                                       gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (er != CUDA_SUCCESS) {
+        delete maps;
+        delete jp;
+        set_error("cuTensorMapEncodeTiled failed");
+        return OOC_ERR_CUDA;
+      }
+    }
+    const long long tiles = jp->nA * ((jp->nB + sh.tb - 1) / sh.tb) * ((jp->nC + sh.tc - 1) / sh.tc);
+    long long grid = std::min<long long>(tiles, static_cast<long long>(c->prop.multiProcessorCount) * k.occ);
+    if (red) {
+      grid = std::min<long long>(grid, c->red_part_cap);
+      jp->part = c->red_part[q];
+    }
+    gx = static_cast<unsigned>(std::max<long long>(grid, 1));
+    gy = 1;
+  } else if (red) {
     gx = static_cast<unsigned>(std::min<long long>(xblocks, c->red_part_cap));
     long long cap = std::max<long long>(1, c->red_part_cap / gx);
     cap = std::min<long long>(cap, std::max<long long>(1, 4 * 148 * 8 / gx));
@@ -925,10 +1479,11 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     }
     cudaEventRecord(e.first, st);
   }
-  void* args[] = {jp};
-  CUresult cr = api().launch(k.fn, gx, gy, 1, k.block, 1, 1, 0, reinterpret_cast<CUstream>(st),
-                             args, nullptr);
+  void* args[] = {jp, maps};
+  CUresult cr = api().launch(k.fn, gx, gy, 1, k.block, 1, 1, static_cast<unsigned>(k.smem),
+                             reinterpret_cast<CUstream>(st), args, nullptr);
   delete jp;
+  delete maps;
   if (cr != CUDA_SUCCESS) {
     const char* s = "?";
     if (api().error_string) api().error_string(cr, &s);
@@ -962,7 +1517,7 @@ extern "C" int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, in
   delete jp;
   if (!ok) err = "group exceeds the kernel template's capacity";
   Compiled k;
-  if (ok) ok = compile(body, 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
+  if (ok) ok = compile(body, sh.tma() ? kTmaThreads : 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
   if (ok && std::getenv("OOC_JIT_VERBOSE")) body = err + "\n" + body;
   if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", ok ? body.c_str() : err.c_str());
   return ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
@@ -980,10 +1535,10 @@ extern "C" int ooc_jit_report(char* buf, int len) {
     while ((pos = fast.find("const bool a", pos)) != std::string::npos) ++nl, ++pos;
     o << (first ? "" : ",") << "{\"loops\":" << nl << ",\"red\":" << (key.find("|red") != std::string::npos)
       << ",\"key\":\"" << std::hex << std::hash<std::string>{}(key) << std::dec << "\",\"shape\":\"";
-    if (T.best >= 0) o << T.cands[T.best].Q << "x" << T.cands[T.best].P;
+    if (T.best >= 0) o << T.cands[T.best].name();
     o << "\",\"ns_per_point\":{";
     for (std::size_t i = 0; i < T.cands.size(); ++i)
-      o << (i ? "," : "") << "\"" << T.cands[i].Q << "x" << T.cands[i].P << "\":" << T.ns_per_point[i];
+      o << (i ? "," : "") << "\"" << T.cands[i].name() << "\":" << T.ns_per_point[i];
     o << "}}";
     first = false;
   }

@@ -8,6 +8,7 @@
 #define OOC_JMAX_FAMILIES 48
 #define OOC_JMAX_WRITES 24
 #define OOC_JMAX_CONST 128
+#define OOC_JMAX_VIEWS 16
 
 // A load family: one dataset view read at one (a, c) offset; its rows are loaded
 // once per thread tile and shared by every read of that view at any b offset.
@@ -24,6 +25,8 @@ struct JitParams {
   double* wp[OOC_JMAX_WRITES];
   long long wsA[OOC_JMAX_WRITES], wsB[OOC_JMAX_WRITES];
   double cst[OOC_JMAX_CONST];
+  int tv_org[OOC_JMAX_VIEWS][3];           // TMA template: tensor coords (c, b, a) of each staged
+                                           // view's box at tile (0, 0, 0)
 };
 
 namespace oocdev {

@@ -270,6 +270,21 @@ def test_row_recompute_fusion_parity(golden_random, row_recompute, jit_always):
     assert not bad, bad
 
 
+@pytest.mark.parametrize("shape,recompute", [("t16x64", "0"), ("t8x128", "0"), ("t32x32", "1"),
+                                             ("1x4", "1"), ("t16x64", "1")])
+def test_forced_tile_shapes(shape, recompute):
+    """Every specialised launch forced to one tile shape — register template (QxP) or
+    shared-memory/TMA template (tTBxTC), with and without row recompute — gives the
+    reference's bits (child process: the shape is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, OOC_JIT_SHAPE=shape, OOC_ROW_RECOMPUTE=recompute)
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "shape_parity_child.py")],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_slab_runtime_with_nccl_single_rank():
     """The multi-GPU path on one GPU: a 1-rank NCCL communicator, a dim-0 window with
     ghost rows, all-reduce of the fieldsum — same bits / same reduction as plain."""
