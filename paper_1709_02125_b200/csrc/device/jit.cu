@@ -220,9 +220,22 @@ __device__ __forceinline__ unsigned ooc_smem(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 __device__ __forceinline__ void ooc_mbar_wait(unsigned bar, unsigned phase) {
-  asm volatile("{\n .reg .pred P1;\n WAIT_%=:\n"
-               " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-               " @!P1 bra WAIT_%=;\n}\n" :: "r"(bar), "r"(phase) : "memory");
+  // bounded: a transaction count that never completes traps (a loud launch error)
+  // instead of hanging the device
+  for (unsigned tries = 0;; ++tries) {
+    unsigned done;
+    asm volatile("{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, P1;\n}\n" : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+    if (done) return;
+    if (tries > (1u << 26)) {
+      printf("ooc_jit_kernel: mbarrier wait timed out (block %d thread %d phase %u)\n", blockIdx.x, threadIdx.x, phase);
+#ifndef OOC_NO_TRAP
+      asm volatile("trap;");
+#else
+      return;
+#endif
+    }
+  }
 }
 __device__ __forceinline__ void ooc_tma(unsigned dst, const void* map, int x, int y, int z, unsigned bar) {
 #if OOC_RANK == 1
@@ -254,16 +267,24 @@ extern "C" __global__ void __launch_bounds__(OOC_THREADS) ooc_jit_kernel(const _
     const int ib0 = static_cast<int>((rem / tC) * OOC_TB), c0 = static_cast<int>((rem % tC) * OOC_TC);
     const int a0 = static_cast<int>(ia);
     const unsigned b = ooc_smem(&bar[s]);
-    const unsigned base = ooc_smem(ooc_sm) + s * OOC_STAGE_BYTES;
+    const unsigned base = ooc_smem(ooc_sm) + OOC_PAD_BYTES + s * OOC_STAGE_BYTES;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(OOC_STAGE_BYTES) : "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(OOC_TX_BYTES) : "memory");
 <<ISSUE>>
   };
+#ifdef OOC_TMA_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0)
+    printf("tma kernel: ntiles %lld grid %d org %d %d %d smem %p\n", ntiles, gridDim.x, p.tv_org[0][0], p.tv_org[0][1],
+           p.tv_org[0][2], ooc_sm);
+#endif
   if (threadIdx.x == 0)
     for (int s = 0; s < OOC_STAGES; ++s) {
       const long long t = blockIdx.x + static_cast<long long>(s) * gridDim.x;
       if (t < ntiles) issue(t, s);
     }
+#ifdef OOC_TMA_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) printf("tma kernel: issued\n");
+#endif
 #if OOC_RED
   double acc = p.red_op == 2 ? __longlong_as_double(0x7ff0000000000000LL)
              : p.red_op == 3 ? __longlong_as_double(0xfff0000000000000LL) : 0.0;
@@ -272,10 +293,14 @@ extern "C" __global__ void __launch_bounds__(OOC_THREADS) ooc_jit_kernel(const _
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
     const int s = k % OOC_STAGES;
     ooc_mbar_wait(ooc_smem(&bar[s]), static_cast<unsigned>((k / OOC_STAGES) & 1));
-    const double* S = reinterpret_cast<const double*>(ooc_sm + s * OOC_STAGE_BYTES);
+#ifdef OOC_TMA_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0 && k < 2) printf("tma kernel: tile %lld landed\n", tile);
+#endif
+    const double* S = reinterpret_cast<const double*>(ooc_sm + OOC_PAD_BYTES + s * OOC_STAGE_BYTES);
     const long long ia = tile / (tB * tC), rem = tile - ia * tB * tC;
     const long long ib0 = (rem / tC) * OOC_TB, c0 = (rem % tC) * OOC_TC;
     const int lc = threadIdx.x % OOC_TC;
+<<SHIFT>>
 #pragma unroll 1
     for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
       const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
@@ -338,6 +363,7 @@ struct TmaPlan {
   int rank = 2;
   int stages = 2;
   long long stage_bytes = 0;
+  long long pad_bytes = 0;
   std::vector<TmaView> views;
 };
 constexpr int kTmaThreads = 256;
@@ -849,6 +875,7 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
     return static_cast<int>(plan.views.size()) - 1;
   };
   bool final_pass = false;
+  long long tx_bytes = 0;
   std::ostringstream out;
   // operand: view v at canonical offset (oa, ob, oc) from the point
   auto smem = [&](const ooc_view& v, int64_t oa, int64_t ob, int64_t oc) -> std::string {
@@ -864,7 +891,7 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
     }
     const long long WC = t.box[0], HB = t.box[1];
     const long long K = t.off + ((oa - t.omin[0]) * HB + (ob - t.omin[1])) * WC + (oc - t.omin[2]);
-    return "S[" + std::to_string(K) + " + lr * " + std::to_string(WC) + " + lc]";
+    return "S[" + std::to_string(K) + " + lr * " + std::to_string(WC) + " + lc + sh" + std::to_string(k) + "]";
   };
   auto smem_at = [&](const ooc_view& v, const int64_t* o, int64_t shift) {
     return smem(v, off_of(o, cn.A), off_of(o, cn.B) + shift, off_of(o, cn.C));
@@ -1026,12 +1053,15 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
     if (!run()) return false;  // pass 1: collect each view's reach
     if (plan.views.empty() || static_cast<int>(plan.views.size()) > OOC_JMAX_VIEWS) return false;
     long long off = 0;
+    tx_bytes = 0;
     for (TmaView& t : plan.views) {
       for (int d = 0; d < 3; ++d) {  // canonical dims absent from the rank: no reach
         const int cd = d == 0 ? cn.A : d == 1 ? cn.B : cn.C;
         if (cd < 0) t.omin[d] = t.omax[d] = 0;
       }
-      long long wc = sh.tc + (t.omax[2] - t.omin[2]);
+      // +1: the load starts at an even column (16-byte aligned, a TMA requirement
+      // found on the device) and the tile's reads shift by the dropped element
+      long long wc = sh.tc + (t.omax[2] - t.omin[2]) + 1;
       wc = (wc + 1) / 2 * 2;  // TMA: inner box bytes a multiple of 16
       const long long hb = sh.tb + (t.omax[1] - t.omin[1]);
       const long long da = 1 + (t.omax[0] - t.omin[0]);
@@ -1040,11 +1070,12 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
       t.box[1] = static_cast<int>(hb);
       t.box[2] = static_cast<int>(da);
       t.off = off;
+      tx_bytes += wc * hb * da * 8;          // what the TMA engine delivers
       off += (wc * hb * da + 15) / 16 * 16;  // 128-byte aligned boxes
     }
     plan.stage_bytes = off * 8;
     const long long budget = 200 * 1024;
-    plan.stages = plan.stage_bytes * 3 <= budget ? 3 : plan.stage_bytes * 2 <= budget + 20 * 1024 ? 2 : 0;
+    plan.stages = plan.stage_bytes * 3 <= budget ? 3 : plan.stage_bytes * 2 <= budget ? 2 : 0;
     if (plan.stages == 0) return false;
     std::memset(jp.cst, 0, sizeof jp.cst);
     final_pass = true;
@@ -1060,16 +1091,43 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
     for (int e = 0; e < 3; ++e)
       jp.tv_org[k][e] = dims[e] < 0 ? 0 : static_cast<int>(lo[dims[e]] - v.lo[dims[e]] + om[e]);
   }
-  std::ostringstream issue, defs;
+  // TMA tile loads fault unless the box starts at a non-negative, 16-byte aligned
+  // column (measured on the device: odd or negative innermost coordinates raise an
+  // illegal-instruction error). Each tile's box is therefore loaded from the even
+  // column at or below its start (never below 0) and rows/planes from >= 0; the
+  // tile's reads shift by the difference. Elements skipped below a view's origin are
+  // never consumed by an active point (validate_loop), they only need to be
+  // addressable — a front pad before the stages covers the worst negative shift.
+  long long pad = 0;
+  for (const TmaView& t : plan.views)
+    pad = std::max<long long>(pad, static_cast<long long>(t.box[2] > 1 ? t.box[1] * t.box[0] : 0) +
+                                       2LL * t.box[0] + 16);
+  pad = (pad + 15) / 16 * 16;
+  for (std::size_t k = 0; k < plan.views.size(); ++k) {  // runtime check: worst shift at tile 0
+    const TmaView& t = plan.views[k];
+    const long long dx = std::max(0, -jp.tv_org[k][0]), dy = std::max(0, -jp.tv_org[k][1]),
+                    dz = std::max(0, -jp.tv_org[k][2]);
+    if (dx + dy * t.box[0] + dz * t.box[1] * t.box[0] > pad) return false;
+  }
+  std::ostringstream issue, shift, defs;
   for (std::size_t k = 0; k < plan.views.size(); ++k) {
     const std::string ks = std::to_string(k);
-    issue << "    ooc_tma(base + " << plan.views[k].off * 8 << "u, &m.t[" << ks << "][0], p.tv_org[" << ks
-          << "][0] + c0, p.tv_org[" << ks << "][1] + ib0, p.tv_org[" << ks << "][2] + a0, b);\n";
+    const TmaView& t = plan.views[k];
+    issue << "    {\n      const int xr = p.tv_org[" << ks << "][0] + c0, yr = p.tv_org[" << ks
+          << "][1] + ib0, zr = p.tv_org[" << ks << "][2] + a0;\n      ooc_tma(base + " << t.off * 8 << "u, &m.t["
+          << ks << "][0], max(xr, 0) & ~1, max(yr, 0), max(zr, 0), b);\n    }\n";
+    shift << "    const int sh" << ks << " = [&] {\n      const int xr = p.tv_org[" << ks
+          << "][0] + static_cast<int>(c0), yr = p.tv_org[" << ks << "][1] + static_cast<int>(ib0), zr = p.tv_org["
+          << ks << "][2] + static_cast<int>(ia);\n      return (xr - (max(xr, 0) & ~1)) + (yr - max(yr, 0)) * "
+          << t.box[0] << " + (zr - max(zr, 0)) * " << static_cast<long long>(t.box[1]) * t.box[0] << ";\n    }();\n";
   }
+  plan.pad_bytes = pad * 8;
   defs << "#define OOC_TB " << sh.tb << "\n#define OOC_TC " << sh.tc << "\n#define OOC_THREADS " << kTmaThreads
        << "\n#define OOC_STAGES " << plan.stages << "\n#define OOC_STAGE_BYTES " << plan.stage_bytes
+       << "\n#define OOC_TX_BYTES " << tx_bytes << "\n#define OOC_PAD_BYTES " << pad * 8
        << "\n#define OOC_RANK " << nd << "\n";
-  body = "<<TMA>>\n" + defs.str() + "<<ISSUE>>\n" + issue.str() + "<<TBODY>>\n" + out.str();
+  body = "<<TMA>>\n" + defs.str() + "<<ISSUE>>\n" + issue.str() + "<<SHIFT>>\n" + shift.str() + "<<TBODY>>\n" +
+         out.str();
   if (plan_out) *plan_out = plan;
   return true;
 }
@@ -1113,7 +1171,9 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
     err = a.why;
     return false;
   }
-  std::string src = "#define OOC_BLOCK " + std::to_string(block) + "\n#define OOC_Q " +
+  std::string src = std::string(std::getenv("OOC_JIT_NO_TRAP") ? "#define OOC_NO_TRAP 1\n" : "") +
+                    std::string(std::getenv("OOC_TMA_TRACE") ? "#define OOC_TMA_TRACE 1\n" : "") +
+                    "#define OOC_BLOCK " + std::to_string(block) + "\n#define OOC_Q " +
                     std::to_string(Q) + "\n#define OOC_P " +
                     std::to_string(P) + "\n#define OOC_RED " + (red ? "1" : "0") +
                     "\n#define OOC_JMAX_LOOPS " + std::to_string(OOC_JMAX_LOOPS) +
@@ -1123,9 +1183,11 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
                     "\n#define OOC_JMAX_VIEWS " + std::to_string(OOC_JMAX_VIEWS) + "\n";
   if (key.rfind("<<TMA>>\n", 0) == 0) {
     // "<<TMA>>\n" defines "<<ISSUE>>\n" issue-code "<<TBODY>>\n" point-body
-    const std::size_t ip = key.find("<<ISSUE>>\n"), bp = key.find("<<TBODY>>\n");
+    const std::size_t ip = key.find("<<ISSUE>>\n"), sp = key.find("<<SHIFT>>\n"),
+                      bp = key.find("<<TBODY>>\n");
     std::string tpl = std::string(kCommon) + kTmaKernel;
-    tpl.replace(tpl.find("<<ISSUE>>"), 9, key.substr(ip + 10, bp - ip - 10));
+    tpl.replace(tpl.find("<<ISSUE>>"), 9, key.substr(ip + 10, sp - ip - 10));
+    tpl.replace(tpl.find("<<SHIFT>>"), 9, key.substr(sp + 10, bp - sp - 10));
     tpl.replace(tpl.find("<<BODY>>"), 8, key.substr(bp + 10));
     src += key.substr(8, ip - 8) + tpl;
   } else {
@@ -1227,7 +1289,6 @@ std::vector<Shape> candidates(int ndim, long long nC) {
   Shape f;
   if (parse_shape(forced, f)) {
     if (ndim == 1) f.Q = 1;
-    if (f.tma()) return {Shape{1, 4}, f};  // register fallback for unaligned launches
     return {f};
   }
   if (ndim == 1) return {{1, 4}, {1, 8}, {1, 2}};
@@ -1316,7 +1377,7 @@ bool compiled_for(ooc_ctx* c, const ooc_loop* Ls, int n, const Shape& sh, bool r
   }
   auto t0 = std::chrono::steady_clock::now();
   if (!compile(body, sh.tma() ? kTmaThreads : 128, sh.Q, sh.P, red, k, err, true,
-               sh.tma() ? pl.stages * pl.stage_bytes : 0))
+               sh.tma() ? pl.pad_bytes + pl.stages * pl.stage_bytes : 0))
     return false;
   c->stats.jit_compiles++;
   c->stats.jit_compile_ms += static_cast<long long>(
@@ -1365,6 +1426,14 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
       std::string e2;
       if (compiled_for(c, Ls, n, cs, red, *jp, kk, e2) || !cs.tma()) T.cands.push_back(cs);
     }
+    if (T.cands.empty()) {  // e.g. a forced TMA shape on a 1-D group: the register template
+      Shape r{1, 4};
+      if (Ls[0].ndim == 1) r = Shape{1, 4};
+      Compiled kk;
+      std::string e2;
+      compiled_for(c, Ls, n, r, red, *jp, kk, e2);
+      T.cands.push_back(r);
+    }
     T.ns_per_point.assign(T.cands.size(), -1.f);
     T.ev.resize(T.cands.size());
     T.points.assign(T.cands.size(), 0);
@@ -1403,12 +1472,13 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   bool built = compiled_for(c, Ls, n, sh, red, *jp, k, err, &plan);
   if (!built && sh.tma()) {  // e.g. a view not 16-byte aligned at this launch
     timing = false;
+    sh = Shape{1, 4};
     for (const Shape& cs : T.cands)
       if (!cs.tma()) {
         sh = cs;
-        built = compiled_for(c, Ls, n, sh, red, *jp, k, err);
         break;
       }
+    built = compiled_for(c, Ls, n, sh, red, *jp, k, err);
   }
   if (!built) {
     delete jp;
@@ -1446,6 +1516,14 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
                                        gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      static const bool dbg = std::getenv("OOC_TMA_DEBUG") != nullptr;
+      if (dbg)
+        std::fprintf(stderr, "tma view %zu: addr %p rank %d gdim %llu %llu %llu gstr %llu %llu box %u %u %u org %d %d %d rc %d\n",
+                     v, static_cast<const void*>(w.data), plan.rank, (unsigned long long)gdim[0],
+                     (unsigned long long)gdim[1], plan.rank > 2 ? (unsigned long long)gdim[2] : 0ULL,
+                     (unsigned long long)gstr[0], plan.rank > 2 ? (unsigned long long)gstr[1] : 0ULL, box[0], box[1],
+                     plan.rank > 2 ? box[2] : 0u, jp->tv_org[v][0], jp->tv_org[v][1], jp->tv_org[v][2],
+                     static_cast<int>(er));
       if (er != CUDA_SUCCESS) {
         delete maps;
         delete jp;

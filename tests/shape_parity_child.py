@@ -23,6 +23,7 @@ for app, nx, ny, nz, iters, span in [("miniflow2d", 300, 256, 0, 12, 0), ("minif
         want.pop("_rt", None)
         got.pop("_rt", None)
         d = compare(want, got)
+        print(app, kw, "ok" if not d else "DIFF", flush=True)
         if d:
             bad.append((app, kw, str(d)[:300]))
 for seed in range(20):

@@ -240,3 +240,25 @@ def test_fusion_plan_miniflow2d():
             assert all(g["ok"] for g in got)
     finally:
         B.set_row_recompute(False)
+
+
+@pytest.mark.parametrize("shape", ["t16x64", "t8x128"])
+def test_tma_template_compiles_for_sm100a(shape):
+    """The shared-memory/TMA kernel template builds for sm_100a for every fused group of
+    the 2-D and 3-D apps (child process: OOC_JIT_SHAPE is read once per process)."""
+    import subprocess
+    import sys
+    if B.jit_status() not in ("ok", "libcuda.so.1 (driver) not available"):
+        pytest.skip("NVRTC unavailable")
+    code = (
+        "import paper_1709_02125_b200 as B\n"
+        "for app, nz, span in (('miniflow2d', 0, 0), ('miniflow3d', 24, 0), ('rk3chain3d', 20, 3)):\n"
+        "    rt = B.Runtime('plan_only', record=True, tiles=1)\n"
+        "    rt.run_app(app, 40, 36, nz, 6, span)\n"
+        "    g = rt.chain_jit_check(rt.num_chains() - 1, fuse=True)\n"
+        "    assert g and all(x['ok'] for x in g), (app, [x.get('log', '')[:800] for x in g if not x['ok']])\n"
+        "    assert any('<<TMA>>' in x.get('log', '') for x in g), app\n")
+    env = dict(__import__("os").environ, OOC_JIT_SHAPE=shape, OOC_JIT_DUMP="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)), timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
