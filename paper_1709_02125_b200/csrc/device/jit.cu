@@ -301,12 +301,29 @@ extern "C" __global__ void __launch_bounds__(OOC_THREADS) ooc_jit_kernel(const _
     const long long ib0 = (rem / tC) * OOC_TB, c0 = (rem % tC) * OOC_TC;
     const int lc = threadIdx.x % OOC_TC;
 <<SHIFT>>
-#pragma unroll 1
-    for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
-      const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
-      const long long bq = ib0 + lr, c = c0 + lc;
-      const bool okp = bq < p.nB && c < p.nC;
+    // interior tile: every point active in every loop (and every recomputed row):
+    // predicates fold to true and the snapshot reads behind them disappear
+    const bool interior = ia >= p.inner[0] && ia < p.inner[1] && ib0 >= p.inner[2] &&
+                          ib0 + OOC_TB <= p.inner[3] && c0 >= p.inner[4] && c0 + OOC_TC <= p.inner[5];
+    if (interior) {
+#define OOC_PRED(x) true
+#pragma unroll
+      for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
+        const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
+        const long long bq = ib0 + lr, c = c0 + lc;
 <<BODY>>
+      }
+#undef OOC_PRED
+    } else {
+#define OOC_PRED(x) (x)
+#pragma unroll 1
+      for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
+        const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
+        const long long bq = ib0 + lr, c = c0 + lc;
+        const bool okp = bq < p.nB && c < p.nC;
+<<BODY>>
+      }
+#undef OOC_PRED
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -900,6 +917,7 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
   std::vector<std::vector<std::vector<int>>> cst_idx;
   std::map<std::tuple<int, int, int, int>, std::string> memo;
   int rc_count = 0;
+  std::vector<std::pair<int, int>> shifts;  // (loop, row shift) of every recomputation
   const int64_t zo[3] = {0, 0, 0};
   auto active_at = [&](int a, int s) {
     const std::string as = std::to_string(a), bs = "(bq + (" + std::to_string(s) + "))";
@@ -979,9 +997,10 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
         res = e;
       } else {
         res = tag + "v";
-        out << "      const double " << res << " = " << active_at(a, s) << " ? " << e << " : "
+        out << "      const double " << res << " = OOC_PRED" << active_at(a, s) << " ? " << e << " : "
             << smem_at(X, zo, s) << ";\n";
       }
+      shifts.push_back({a, s});
     }
     return memo[key] = res;
   };
@@ -991,6 +1010,7 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
     nwrite = 0;
     rc_count = 0;
     memo.clear();
+    shifts.clear();
     cst_idx.assign(n, {});
     for (int i = 0; i < n; ++i) cst_idx[i].resize(Ls[i].nwrites);
     struct Writer {
@@ -1002,9 +1022,9 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
     for (int i = 0; i < n; ++i) {
       const ooc_loop& L = Ls[i];
       const std::string is = std::to_string(i);
-      out << "      const bool a" << is << " = okp && ia >= p.rng[" << is << "][0] && ia < p.rng[" << is
+      out << "      const bool a" << is << " = OOC_PRED(okp && ia >= p.rng[" << is << "][0] && ia < p.rng[" << is
           << "][1] && bq >= p.rng[" << is << "][2] && bq < p.rng[" << is << "][3] && c >= p.rng[" << is
-          << "][4] && c < p.rng[" << is << "][5];\n";
+          << "][4] && c < p.rng[" << is << "][5]);\n";
       auto rd = [&](const ooc_ins& in) -> std::string {
         const ooc_view& v = L.args[in.arg];
         int w = 0;
@@ -1082,6 +1102,19 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
     if (!run()) return false;
   } catch (const std::exception&) {
     return false;
+  }
+  {  // interior tiles: inside every loop's range, rows shifted by every recomputation too
+    long long inner[6] = {0, jp.nA, 0, jp.nB, 0, jp.nC};
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < 6; k += 2) {
+        inner[k] = std::max<long long>(inner[k], jp.rng[i][k]);
+        inner[k + 1] = std::min<long long>(inner[k + 1], jp.rng[i][k + 1]);
+      }
+    for (const auto& [a, sft] : shifts) {
+      inner[2] = std::max<long long>(inner[2], jp.rng[a][2] - sft);
+      inner[3] = std::min<long long>(inner[3], jp.rng[a][3] - sft);
+    }
+    for (int k = 0; k < 6; ++k) jp.inner[k] = inner[k];
   }
   for (std::size_t k = 0; k < plan.views.size(); ++k) {
     const TmaView& t = plan.views[k];
@@ -1188,7 +1221,8 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
     std::string tpl = std::string(kCommon) + kTmaKernel;
     tpl.replace(tpl.find("<<ISSUE>>"), 9, key.substr(ip + 10, sp - ip - 10));
     tpl.replace(tpl.find("<<SHIFT>>"), 9, key.substr(sp + 10, bp - sp - 10));
-    tpl.replace(tpl.find("<<BODY>>"), 8, key.substr(bp + 10));
+    const std::string tbody = key.substr(bp + 10);
+    for (std::size_t at; (at = tpl.find("<<BODY>>")) != std::string::npos;) tpl.replace(at, 8, tbody);
     src += key.substr(8, ip - 8) + tpl;
   } else {
     std::string tpl = std::string(kCommon) + kRegKernel;
@@ -1308,8 +1342,9 @@ std::vector<Shape> candidates(int ndim, long long nC) {
       return static_cast<double>((nC + tc - 1) / tc * tc) / static_cast<double>(nC) - 1.0;
     };
     int added = 0;
-    for (Shape s : {Shape{1, 1, 16, 64}, Shape{1, 1, 8, 128}, Shape{1, 1, 32, 32}, Shape{1, 1, 64, 32}})
-      if (twaste(s.tc) <= 0.2 && added < 2) {
+    for (Shape s : {Shape{1, 1, 16, 64}, Shape{1, 1, 8, 128}, Shape{1, 1, 8, 64}, Shape{1, 1, 32, 32},
+                    Shape{1, 1, 64, 32}})
+      if (twaste(s.tc) <= 0.2 && added < 3) {
         out.push_back(s);
         ++added;
       }
