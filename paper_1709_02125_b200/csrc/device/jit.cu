@@ -362,9 +362,10 @@ struct Family {
 struct Shape {
   int Q = 1, P = 4;
   int tb = 0, tc = 0;  // > 0: shared-memory-staged TMA template with OOC_TB x OOC_TC tiles
+  int th = 256;        // TMA template: threads per CTA
   bool tma() const { return tb > 0; }
   std::string name() const {
-    return tma() ? "t" + std::to_string(tb) + "x" + std::to_string(tc)
+    return tma() ? "t" + std::to_string(tb) + "x" + std::to_string(tc) + (th != 256 ? "w" + std::to_string(th) : "")
                  : std::to_string(Q) + "x" + std::to_string(P);
   }
 };
@@ -383,15 +384,16 @@ struct TmaPlan {
   long long pad_bytes = 0;
   std::vector<TmaView> views;
 };
-constexpr int kTmaThreads = 256;
 
 // "QxP" (register template) or "tTBxTC" (TMA template)
 bool parse_shape(const char* txt, Shape& f) {
   if (!txt || !*txt) return false;
   if (txt[0] == 't') {
     f = Shape{1, 1, 0, 0};
-    return std::sscanf(txt + 1, "%dx%d", &f.tb, &f.tc) == 2 && f.tb >= 1 && f.tc >= 1 && 256 % f.tc == 0 &&
-           f.tb % (256 / f.tc) == 0;
+    f.th = 256;
+    const int got = std::sscanf(txt + 1, "%dx%dw%d", &f.tb, &f.tc, &f.th);
+    return got >= 2 && f.tb >= 1 && f.tc >= 1 && f.th >= 32 && f.th <= 1024 && f.th % f.tc == 0 &&
+           f.tb % (f.th / f.tc) == 0;
   }
   return std::sscanf(txt, "%dx%d", &f.Q, &f.P) == 2 && f.Q >= 1 && f.P >= 1;
 }
@@ -1155,7 +1157,7 @@ bool generate_tma(const ooc_loop* Ls, int n, const Shape& sh, JitParams& jp, std
           << t.box[0] << " + (zr - max(zr, 0)) * " << static_cast<long long>(t.box[1]) * t.box[0] << ";\n    }();\n";
   }
   plan.pad_bytes = pad * 8;
-  defs << "#define OOC_TB " << sh.tb << "\n#define OOC_TC " << sh.tc << "\n#define OOC_THREADS " << kTmaThreads
+  defs << "#define OOC_TB " << sh.tb << "\n#define OOC_TC " << sh.tc << "\n#define OOC_THREADS " << sh.th
        << "\n#define OOC_STAGES " << plan.stages << "\n#define OOC_STAGE_BYTES " << plan.stage_bytes
        << "\n#define OOC_TX_BYTES " << tx_bytes << "\n#define OOC_PAD_BYTES " << pad * 8
        << "\n#define OOC_RANK " << nd << "\n";
@@ -1342,8 +1344,12 @@ std::vector<Shape> candidates(int ndim, long long nC) {
       return static_cast<double>((nC + tc - 1) / tc * tc) / static_cast<double>(nC) - 1.0;
     };
     int added = 0;
-    for (Shape s : {Shape{1, 1, 16, 64}, Shape{1, 1, 8, 128}, Shape{1, 1, 8, 64}, Shape{1, 1, 32, 32},
-                    Shape{1, 1, 64, 32}})
+    auto T = [](int tb, int tc, int th) {
+      Shape s{1, 1, tb, tc};
+      s.th = th;
+      return s;
+    };
+    for (Shape s : {T(8, 128, 512), T(16, 64, 512), T(8, 128, 256), T(16, 32, 512), T(32, 32, 256)})
       if (twaste(s.tc) <= 0.2 && added < 3) {
         out.push_back(s);
         ++added;
@@ -1411,7 +1417,7 @@ bool compiled_for(ooc_ctx* c, const ooc_loop* Ls, int n, const Shape& sh, bool r
     return true;
   }
   auto t0 = std::chrono::steady_clock::now();
-  if (!compile(body, sh.tma() ? kTmaThreads : 128, sh.Q, sh.P, red, k, err, true,
+  if (!compile(body, sh.tma() ? sh.th : 128, sh.Q, sh.P, red, k, err, true,
                sh.tma() ? pl.pad_bytes + pl.stages * pl.stage_bytes : 0))
     return false;
   c->stats.jit_compiles++;
@@ -1630,7 +1636,7 @@ extern "C" int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, in
   delete jp;
   if (!ok) err = "group exceeds the kernel template's capacity";
   Compiled k;
-  if (ok) ok = compile(body, sh.tma() ? kTmaThreads : 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
+  if (ok) ok = compile(body, sh.tma() ? sh.th : 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
   if (ok && std::getenv("OOC_JIT_VERBOSE")) body = err + "\n" + body;
   if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", ok ? body.c_str() : err.c_str());
   return ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
