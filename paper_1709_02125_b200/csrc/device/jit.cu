@@ -250,91 +250,88 @@ __device__ __forceinline__ void ooc_tma(unsigned dst, const void* map, int x, in
                : "memory");
 #endif
 }
-extern "C" __global__ void __launch_bounds__(OOC_THREADS) ooc_jit_kernel(const __grid_constant__ JitParams p,
-                                                                       const __grid_constant__ TmaMaps m) {
+extern "C" __global__ void __launch_bounds__(OOC_THREADS + 32) ooc_jit_kernel(const __grid_constant__ JitParams p,
+                                                                            const __grid_constant__ TmaMaps m) {
+  // warps 0..OOC_THREADS/32-1 compute; the last warp is the TMA producer. Stage s is
+  // guarded by full[s] (producer arms the byte count, TMA completes it) and empty[s]
+  // (every consumer warp arrives once it has read the tile).
   extern __shared__ __align__(128) unsigned char ooc_sm[];
-  __shared__ __align__(8) unsigned long long bar[OOC_STAGES];
+  __shared__ __align__(8) unsigned long long full[OOC_STAGES], empty[OOC_STAGES];
   const long long tC = (p.nC + OOC_TC - 1) / OOC_TC, tB = (p.nB + OOC_TB - 1) / OOC_TB;
   const long long ntiles = p.nA * tB * tC;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < OOC_STAGES; ++s)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(ooc_smem(&bar[s])) : "memory");
+    for (int s = 0; s < OOC_STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(ooc_smem(&full[s])) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ooc_smem(&empty[s])), "r"(OOC_THREADS / 32)
+                   : "memory");
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](long long tile, int s) {
-    const long long ia = tile / (tB * tC), rem = tile - ia * tB * tC;
-    const int ib0 = static_cast<int>((rem / tC) * OOC_TB), c0 = static_cast<int>((rem % tC) * OOC_TC);
-    const int a0 = static_cast<int>(ia);
-    const unsigned b = ooc_smem(&bar[s]);
-    const unsigned base = ooc_smem(ooc_sm) + OOC_PAD_BYTES + s * OOC_STAGE_BYTES;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(OOC_TX_BYTES) : "memory");
-<<ISSUE>>
-  };
-#ifdef OOC_TMA_TRACE
-  if (threadIdx.x == 0 && blockIdx.x == 0)
-    printf("tma kernel: ntiles %lld grid %d org %d %d %d smem %p\n", ntiles, gridDim.x, p.tv_org[0][0], p.tv_org[0][1],
-           p.tv_org[0][2], ooc_sm);
-#endif
-  if (threadIdx.x == 0)
-    for (int s = 0; s < OOC_STAGES; ++s) {
-      const long long t = blockIdx.x + static_cast<long long>(s) * gridDim.x;
-      if (t < ntiles) issue(t, s);
-    }
-#ifdef OOC_TMA_TRACE
-  if (threadIdx.x == 0 && blockIdx.x == 0) printf("tma kernel: issued\n");
-#endif
 #if OOC_RED
   double acc = p.red_op == 2 ? __longlong_as_double(0x7ff0000000000000LL)
              : p.red_op == 3 ? __longlong_as_double(0xfff0000000000000LL) : 0.0;
 #endif
-  int k = 0;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-    const int s = k % OOC_STAGES;
-    ooc_mbar_wait(ooc_smem(&bar[s]), static_cast<unsigned>((k / OOC_STAGES) & 1));
-#ifdef OOC_TMA_TRACE
-    if (threadIdx.x == 0 && blockIdx.x == 0 && k < 2) printf("tma kernel: tile %lld landed\n", tile);
-#endif
-    const double* S = reinterpret_cast<const double*>(ooc_sm + OOC_PAD_BYTES + s * OOC_STAGE_BYTES);
-    const long long ia = tile / (tB * tC), rem = tile - ia * tB * tC;
-    const long long ib0 = (rem / tC) * OOC_TB, c0 = (rem % tC) * OOC_TC;
-    const int lc = threadIdx.x % OOC_TC;
+  if (threadIdx.x >= OOC_THREADS) {
+    if (threadIdx.x == OOC_THREADS) {  // producer
+      int k = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int s = k % OOC_STAGES;
+        if (k >= OOC_STAGES) ooc_mbar_wait(ooc_smem(&empty[s]), static_cast<unsigned>((k / OOC_STAGES - 1) & 1));
+        const long long ia = tile / (tB * tC), rem = tile - ia * tB * tC;
+        const int ib0 = static_cast<int>((rem / tC) * OOC_TB), c0 = static_cast<int>((rem % tC) * OOC_TC);
+        const int a0 = static_cast<int>(ia);
+        const unsigned b = ooc_smem(&full[s]);
+        const unsigned base = ooc_smem(ooc_sm) + OOC_PAD_BYTES + s * OOC_STAGE_BYTES;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(b), "r"(OOC_TX_BYTES)
+                     : "memory");
+<<ISSUE>>
+      }
+    }
+  } else {
+    int k = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+      const int s = k % OOC_STAGES;
+      ooc_mbar_wait(ooc_smem(&full[s]), static_cast<unsigned>((k / OOC_STAGES) & 1));
+      const double* S = reinterpret_cast<const double*>(ooc_sm + OOC_PAD_BYTES + s * OOC_STAGE_BYTES);
+      const long long ia = tile / (tB * tC), rem = tile - ia * tB * tC;
+      const long long ib0 = (rem / tC) * OOC_TB, c0 = (rem % tC) * OOC_TC;
+      const int lc = threadIdx.x % OOC_TC;
 <<SHIFT>>
-    // interior tile: every point active in every loop (and every recomputed row):
-    // predicates fold to true and the snapshot reads behind them disappear
-    const bool interior = ia >= p.inner[0] && ia < p.inner[1] && ib0 >= p.inner[2] &&
-                          ib0 + OOC_TB <= p.inner[3] && c0 >= p.inner[4] && c0 + OOC_TC <= p.inner[5];
-    if (interior) {
+      // interior tile: every point active in every loop (and every recomputed row):
+      // predicates fold to true and the snapshot reads behind them disappear
+      const bool interior = ia >= p.inner[0] && ia < p.inner[1] && ib0 >= p.inner[2] &&
+                            ib0 + OOC_TB <= p.inner[3] && c0 >= p.inner[4] && c0 + OOC_TC <= p.inner[5];
+      if (interior) {
 #define OOC_PRED(x) true
 #pragma unroll
-      for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
-        const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
-        const long long bq = ib0 + lr, c = c0 + lc;
+        for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
+          const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
+          const long long bq = ib0 + lr, c = c0 + lc;
 <<BODY>>
-      }
+        }
 #undef OOC_PRED
-    } else {
+      } else {
 #define OOC_PRED(x) (x)
 #pragma unroll 1
-      for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
-        const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
-        const long long bq = ib0 + lr, c = c0 + lc;
-        const bool okp = bq < p.nB && c < p.nC;
+        for (int i = 0; i < OOC_TB / (OOC_THREADS / OOC_TC); ++i) {
+          const int lr = threadIdx.x / OOC_TC + i * (OOC_THREADS / OOC_TC);
+          const long long bq = ib0 + lr, c = c0 + lc;
+          const bool okp = bq < p.nB && c < p.nC;
 <<BODY>>
-      }
+        }
 #undef OOC_PRED
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const long long nt = tile + static_cast<long long>(OOC_STAGES) * gridDim.x;
-      if (nt < ntiles) issue(nt, s);
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(ooc_smem(&empty[s])) : "memory");
     }
   }
 #if OOC_RED
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc = ooc_red(p.red_op, acc, __shfl_down_sync(0xffffffffu, acc, o));
-  __shared__ double warp_part[OOC_THREADS / 32];
+  __shared__ double warp_part[OOC_THREADS / 32 + 1];
   if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1417,7 +1414,7 @@ bool compiled_for(ooc_ctx* c, const ooc_loop* Ls, int n, const Shape& sh, bool r
     return true;
   }
   auto t0 = std::chrono::steady_clock::now();
-  if (!compile(body, sh.tma() ? sh.th : 128, sh.Q, sh.P, red, k, err, true,
+  if (!compile(body, sh.tma() ? sh.th + 32 : 128, sh.Q, sh.P, red, k, err, true,
                sh.tma() ? pl.pad_bytes + pl.stages * pl.stage_bytes : 0))
     return false;
   c->stats.jit_compiles++;
@@ -1636,7 +1633,7 @@ extern "C" int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, in
   delete jp;
   if (!ok) err = "group exceeds the kernel template's capacity";
   Compiled k;
-  if (ok) ok = compile(body, sh.tma() ? sh.th : 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
+  if (ok) ok = compile(body, sh.tma() ? sh.th + 32 : 128, sh.Q, sh.P, red_op != OOC_RED_NONE, k, err, /*load=*/false);
   if (ok && std::getenv("OOC_JIT_VERBOSE")) body = err + "\n" + body;
   if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", ok ? body.c_str() : err.c_str());
   return ok ? OOC_OK : OOC_ERR_UNSUPPORTED;
