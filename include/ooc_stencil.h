@@ -160,8 +160,9 @@ const char* ooc_rt_dist_plan_json(ooc_runtime* rt, int chain);
 /* Group recorded chain `chain` as the engine would (fuse = 1: loop fusion) and
  * generate + NVRTC-compile each group's specialised sm_100a kernel (no GPU needed). */
 const char* ooc_rt_chain_jit_check(ooc_runtime* rt, int chain, int fuse);
-/* Process-wide fusion policy: 1 admits row-recompute groups (neighbour reads along
- * the row dimension of values written earlier in the launch, re-evaluated in-thread). */
+/* Process-wide fusion policy: 1 (default; env OOC_ROW_RECOMPUTE=0 turns it off) admits
+ * row-recompute groups (neighbour reads along the row dimension of values written
+ * earlier in the launch, re-evaluated in-thread). */
 void ooc_rt_set_row_recompute(int on);
 /* dependency_oracle over recorded chain `chain` planned with `tiles`. */
 const char* ooc_rt_chain_oracle_json(ooc_runtime* rt, int chain, int tiles);

@@ -1346,7 +1346,9 @@ std::vector<Shape> candidates(int ndim, long long nC) {
       s.th = th;
       return s;
     };
-    for (Shape s : {T(8, 128, 512), T(16, 64, 512), T(8, 128, 256), T(16, 32, 512), T(32, 32, 256)})
+    const std::vector<Shape> tma2 = {T(8, 128, 512), T(16, 64, 512), T(8, 128, 256), T(16, 32, 512)};
+    const std::vector<Shape> tma3 = {T(8, 64, 256), T(4, 128, 256), T(16, 32, 256), T(4, 64, 256)};
+    for (Shape s : ndim == 3 ? tma3 : tma2)
       if (twaste(s.tc) <= 0.2 && added < 3) {
         out.push_back(s);
         ++added;

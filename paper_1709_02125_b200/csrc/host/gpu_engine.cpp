@@ -179,14 +179,15 @@ int GpuEngine::alloc_red_slot() {
 // recomputation. Reducing loops always run alone.
 namespace {
 
-// Row recompute trades DRAM bytes for registers; with the register-staged kernel
-// template the extra live values spill (8-loop miniflow2d group: 226-255 regs), so it
-// is opt-in (OOC_ROW_RECOMPUTE=1) until operands are staged in shared memory.
+// Row recompute trades DRAM bytes for re-evaluated expressions. The register-staged
+// kernel template spills on such groups (8-loop miniflow2d group: 226-255 regs); the
+// shared-memory/TMA template runs them at 44-128 regs, and the autotuner picks
+// whichever is faster. Default on; OOC_ROW_RECOMPUTE=0 disables.
 int g_row_recompute = -1;  // -1: from the environment
 bool row_recompute_enabled() {
   if (g_row_recompute < 0) {
     const char* e = std::getenv("OOC_ROW_RECOMPUTE");
-    g_row_recompute = e && std::atoi(e) != 0;
+    g_row_recompute = !(e && std::atoi(e) == 0);
   }
   return g_row_recompute != 0;
 }

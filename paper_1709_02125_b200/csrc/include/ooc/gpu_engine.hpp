@@ -31,7 +31,7 @@ LoweredLoop lower_loop(const ParLoop& loop);
 bool can_fuse(const std::vector<const ParLoop*>& group, std::size_t group_tape, const ParLoop& b,
               bool enabled);
 
-/// Process-wide: admit row-recompute fusion (default: OOC_ROW_RECOMPUTE env, off).
+/// Process-wide: admit row-recompute fusion (default on; OOC_ROW_RECOMPUTE=0 disables).
 void set_row_recompute(bool on);
 
 /// Fusion partition of a chain into consecutive launch groups: starts[j] = 1 where a
