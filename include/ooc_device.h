@@ -208,6 +208,7 @@ typedef struct {
   long long copy_calls;
   long long jit_launches, jit_compiles, jit_compile_ms;
   long long comm_bytes;
+  long long jit_host_us;  /* host time spent preparing specialised launches */
 } ooc_dev_stats;
 int ooc_stats(ooc_ctx* ctx, ooc_dev_stats* out);
 int ooc_stats_reset(ooc_ctx* ctx);

@@ -1429,6 +1429,14 @@ bool compiled_for(ooc_ctx* c, const ooc_loop* Ls, int n, const Shape& sh, bool r
 // Returns OOC_OK when launched, 1 when the group should go to the interpreter,
 // negative on a hard error. `blocks_out` = number of reduction partials.
 int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_out) {
+  struct HostTimer {
+    ooc_ctx* c;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~HostTimer() {
+      c->stats.jit_host_us += std::chrono::duration_cast<std::chrono::microseconds>(
+                                  std::chrono::steady_clock::now() - t0).count();
+    }
+  } host_timer{c};
   const int m = mode();
   if (m == 0) return 1;
   long long pts = 1;
