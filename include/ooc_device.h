@@ -90,6 +90,19 @@ int ooc_queue_sync(ooc_ctx* ctx, int queue);
 /* Raw cudaStream_t of a queue (for callers that time on the launching stream). */
 int ooc_queue_handle(ooc_ctx* ctx, int queue, void** stream);
 
+/* ------------------------------------------------------------ CUDA graphs
+ * Capture the work issued on a queue between begin and end into an executable graph
+ * (relaxed capture: NVRTC compiles may happen inside), replay it with one launch.
+ * `kernels` = launches the graph holds, added to the statistics on every replay. */
+typedef struct ooc_graph ooc_graph;
+int ooc_graph_begin(ooc_ctx* ctx, int queue);
+int ooc_graph_end(ooc_ctx* ctx, int queue, long long kernels, ooc_graph** out);
+int ooc_graph_launch(ooc_ctx* ctx, int queue, ooc_graph* g);
+void ooc_graph_destroy(ooc_graph* g);
+/* 1 when every specialised-kernel structure seen so far has finished tile-shape
+ * tuning (graphs must not bake a tuning launch). */
+int ooc_jit_settled(void);
+
 /* ------------------------------------------------------------ box views and copies */
 /* A strided window covering the box [lo, hi) in global index space: element p
  * lives at data[sum_d (p[d]-lo[d]) * stride[d]]. The last used dimension
@@ -209,6 +222,7 @@ typedef struct {
   long long jit_launches, jit_compiles, jit_compile_ms;
   long long comm_bytes;
   long long jit_host_us;  /* host time spent preparing specialised launches */
+  long long graph_launches;
 } ooc_dev_stats;
 int ooc_stats(ooc_ctx* ctx, ooc_dev_stats* out);
 int ooc_stats_reset(ooc_ctx* ctx);

@@ -53,4 +53,5 @@ struct ooc_ctx {
   // multi-GPU (comm.cu): NCCL communicator of the slab decomposition
   void* comm = nullptr;
   int rank = 0, world = 1;
+  long long capture_launches0 = 0;  // kernel-launch count when a graph capture began
 };

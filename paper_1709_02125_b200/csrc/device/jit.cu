@@ -1628,6 +1628,15 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
 
 }  // namespace oocdev
 
+extern "C" int ooc_jit_settled(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  for (auto& [key, T] : g_tune) {
+    if (T.best < 0) settle(T);
+    if (T.best < 0) return 0;
+  }
+  return 1;
+}
+
 extern "C" int ooc_jit_config(int m, long long min_points) {
   g_mode = m;
   if (min_points >= 0) g_min_points = min_points;

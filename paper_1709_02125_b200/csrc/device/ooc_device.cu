@@ -332,3 +332,48 @@ int ooc_stats_reset(ooc_ctx* c) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ CUDA graphs
+struct ooc_graph {
+  cudaGraphExec_t exec = nullptr;
+  long long kernels = 0;
+};
+
+int ooc_graph_begin(ooc_ctx* c, int q) {
+  OOC_ARG_CHECK(c && q >= 0 && q < OOC_NUM_QUEUES, "ooc_graph_begin: bad args");
+  OOC_CUDA_TRY(cudaStreamBeginCapture(c->q[q], cudaStreamCaptureModeRelaxed));
+  c->capture_launches0 = c->stats.kernel_launches;
+  return OOC_OK;
+}
+
+int ooc_graph_end(ooc_ctx* c, int q, long long kernels, ooc_graph** out) {
+  OOC_ARG_CHECK(c && out && q >= 0 && q < OOC_NUM_QUEUES, "ooc_graph_end: bad args");
+  cudaGraph_t g = nullptr;
+  OOC_CUDA_TRY(cudaStreamEndCapture(c->q[q], &g));
+  auto* G = new ooc_graph;
+  G->kernels = kernels >= 0 ? kernels : c->stats.kernel_launches - c->capture_launches0;
+  cudaError_t e = cudaGraphInstantiate(&G->exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    delete G;
+    OOC_CUDA_TRY(e);
+  }
+  // captured launches did not run: the replay that follows counts them
+  c->stats.kernel_launches = c->capture_launches0;
+  *out = G;
+  return OOC_OK;
+}
+
+int ooc_graph_launch(ooc_ctx* c, int q, ooc_graph* g) {
+  OOC_ARG_CHECK(c && g && q >= 0 && q < OOC_NUM_QUEUES, "ooc_graph_launch: bad args");
+  OOC_CUDA_TRY(cudaGraphLaunch(g->exec, c->q[q]));
+  c->stats.kernel_launches += g->kernels;
+  c->stats.graph_launches++;
+  return OOC_OK;
+}
+
+void ooc_graph_destroy(ooc_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  delete g;
+}

@@ -458,6 +458,7 @@ const char* ooc_rt_device_json(ooc_runtime* h) {
     w.key("jit_compiles").value(st.jit_compiles);
     w.key("jit_compile_ms").value(st.jit_compile_ms);
     w.key("jit_host_us").value(st.jit_host_us);
+    w.key("graph_launches").value(st.graph_launches);
     w.key("mem_in_use").value(in_use);
     w.key("mem_peak").value(peak);
     w.key("build").value(std::string(ooc_dev_build_info()));

@@ -109,6 +109,10 @@ GpuEngine::GpuEngine(const RuntimeOptions& opts) : opts_(opts) {
 GpuEngine::~GpuEngine() {
   if (!ctx_) return;
   ooc_ctx_sync(ctx_);
+  for (auto& [k, e] : graphs_) {
+    ooc_graph_destroy(e.g[0]);
+    ooc_graph_destroy(e.g[1]);
+  }
   auto drop = [&](std::vector<ooc_event*>& v) {
     for (auto* e : v) ooc_event_destroy(ctx_, e);
     v.clear();
@@ -161,7 +165,7 @@ void GpuEngine::recycle(ooc_event* e) {
 
 int GpuEngine::alloc_red_slot() {
   int s = next_red_slot_;
-  next_red_slot_ = (next_red_slot_ + 1) % OOC_REDUCE_SLOTS;
+  next_red_slot_ = (next_red_slot_ + 1) % (OOC_REDUCE_SLOTS / 2);  // upper half: graphs
   auto it = red_ready_.find(s);
   if (it != red_ready_.end()) {  // slot reuse: its previous value must have landed
     DEV(ooc_event_sync(ctx_, it->second));
@@ -876,12 +880,68 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
     }
   pc.t.uploaded = up;
   DEV(ooc_event_record(ctx_, pc.start, OOC_Q_COMPUTE));
-  for (const ParLoop& l : chain.loops)
-    if (l.has_reduction()) {
-      int s = alloc_red_slot();
-      out.reduction_slot[l.id] = s;
-      DEV(ooc_reduce_reset(ctx_, OOC_Q_COMPUTE, s, lower_loop(l).reduce_op));
+  // A chain whose launches repeat exactly (same loops, constants, plan, buffers and
+  // reduction slots — e.g. every steady-state chain of an app) is captured into a CUDA
+  // graph on its third sighting, once tile-shape tuning has settled, and replayed with
+  // one launch from then on: the host cost of thousands of small launches (L2-tiled
+  // chains) disappears.
+  static const bool graphs_on = [] {
+    const char* e = std::getenv("OOC_GRAPHS");
+    return !(e && std::atoi(e) == 0);
+  }();
+  const bool graphs_ok = graphs_on && !(halos && comm_ready_) && !opts_.profile_loops && !opts_.timeline;
+  GraphEntry* ge = nullptr;
+  int par = 0;
+  if (graphs_ok) {
+    ge = &graphs_[graph_key(chain, plan)];
+    ++ge->seen;
+    par = ge->flip;
+    ge->flip ^= 1;
+    if (ge->slots[par].empty()) {
+      int need = 0;
+      for (const ParLoop& l : chain.loops) need += l.has_reduction() ? 1 : 0;
+      if (next_graph_slot_ + need > OOC_REDUCE_SLOTS) {
+        ge = nullptr;  // slot range exhausted: this structure runs without graphs
+      } else {
+        for (int r = 0; r < need; ++r) ge->slots[par].push_back(next_graph_slot_++);
+        if (need == 0) ge->slots[par].push_back(-1);  // mark as assigned
+      }
     }
+  }
+  {
+    std::size_t r = 0;
+    for (const ParLoop& l : chain.loops)
+      if (l.has_reduction()) {
+        if (ge) {
+          const int s = ge->slots[par][r++];
+          auto it = red_ready_.find(s);  // the chain two back used it: its value has landed?
+          if (it != red_ready_.end()) DEV(ooc_event_sync(ctx_, it->second));
+          out.reduction_slot[l.id] = s;
+        } else {
+          out.reduction_slot[l.id] = alloc_red_slot();
+        }
+      }
+  }
+  auto mark_written = [&] {
+    for (const ParLoop& l : chain.loops)
+      for (const LoopArg& a : l.args)
+        if (access_writes(a.mode)) {
+          mesh[a.dataset].ever_written = true;
+          res_[static_cast<std::size_t>(a.dataset)].host_outdated = true;
+        }
+  };
+  if (ge && ge->g[par]) {
+    DEV(ooc_graph_launch(ctx_, OOC_Q_COMPUTE, ge->g[par]));
+    mark_written();
+    for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
+    finish_chain(chain, out.reduction_slot, pc);
+    return;
+  }
+  const bool capture = ge && ge->seen >= 3 && ooc_jit_settled();  // both parities by the 4th
+  if (capture) DEV(ooc_graph_begin(ctx_, OOC_Q_COMPUTE));
+  for (const ParLoop& l : chain.loops)
+    if (l.has_reduction())
+      DEV(ooc_reduce_reset(ctx_, OOC_Q_COMPUTE, out.reduction_slot.at(l.id), lower_loop(l).reduce_op));
   std::vector<LoweredLoop> lowered_store(chain.loops.size());
   std::vector<const LoweredLoop*> lowered(chain.loops.size());
   std::vector<std::vector<ooc_view>> views(chain.loops.size());
@@ -912,6 +972,10 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
   flush_group(OOC_Q_COMPUTE);
+  if (capture) {
+    DEV(ooc_graph_end(ctx_, OOC_Q_COMPUTE, -1, &ge->g[par]));
+    DEV(ooc_graph_launch(ctx_, OOC_Q_COMPUTE, ge->g[par]));
+  }
   if (halos && comm_ready_) {
     // slab decomposition: refresh every ghost band from the neighbours' owned rows,
     // then combine the ranks' reductions — both stream-ordered after the kernels
@@ -936,6 +1000,49 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
   }
   for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
   finish_chain(chain, out.reduction_slot, pc);
+}
+
+std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan) const {
+  std::string k;
+  auto put = [&](const void* p, std::size_t n) { k.append(static_cast<const char*>(p), n); };
+  auto put_i = [&](long long v) { put(&v, sizeof v); };
+  put_i(static_cast<long long>(chain.loops.size()));
+  put_i(opts_.fuse ? 1 : 0);
+  for (const ParLoop& l : chain.loops) {
+    put_i(l.range.ndim);
+    for (int d = 0; d < 3; ++d) {
+      put_i(l.range.lo[d]);
+      put_i(l.range.hi[d]);
+    }
+    for (const LoopArg& a : l.args) {
+      put_i(a.dataset);
+      put_i(static_cast<long long>(a.mode));
+      const double* dev = res_[static_cast<std::size_t>(a.dataset)].dev;
+      put(&dev, sizeof dev);
+      put_i(static_cast<long long>(a.stencil.offsets.size()));
+      for (const Point& o : a.stencil.offsets) put(o.data(), sizeof(index_t) * 3);
+    }
+    const LoweredLoop lw = lower_loop(l);
+    for (const ooc_ins& in : lw.tape) {  // field by field: no struct padding in the key
+      put_i(in.op);
+      put_i(in.arg);
+      put(&in.value, sizeof in.value);
+      for (int d = 0; d < 3; ++d) put_i(in.offset[d]);
+    }
+    put_i(lw.reduce_op);
+  }
+  if (plan) {
+    put_i(plan->tile_count);
+    for (std::size_t j = 0; j < chain.loops.size(); ++j)
+      for (int t = 0; t < plan->tile_count; ++t) {
+        const Extent e = plan->subrange(static_cast<int>(j), t);
+        for (int d = 0; d < 3; ++d) {
+          put_i(e.lo[d]);
+          put_i(e.hi[d]);
+        }
+      }
+  }
+  return k;
 }
 
 void GpuEngine::comm_init(int rank, int world, const void* id) {

@@ -181,6 +181,18 @@ class GpuEngine {
   void timeline_cmd(int kind, int queue, index_t bytes, DatasetId d, int tile,
                     std::vector<std::pair<int, index_t>> loops, const std::function<void()>& issue);
   std::vector<TLPending> tl_pending_;
+  // CUDA graphs of repeated resident chains (key: everything a launch bakes in)
+  // Two graphs per chain structure, alternating, each with its own reduction slots
+  // (from the upper half of the slot range) so a replay never waits on the previous chain.
+  struct GraphEntry {
+    int seen = 0;
+    int flip = 0;
+    ooc_graph* g[2] = {nullptr, nullptr};
+    std::vector<int> slots[2];
+  };
+  std::map<std::string, GraphEntry> graphs_;
+  int next_graph_slot_ = OOC_REDUCE_SLOTS / 2;
+  std::string graph_key(const LoopChain& chain, const TilePlan* plan) const;
   ooc_event* tl_base_ = nullptr;
   std::chrono::steady_clock::time_point tl_host0_;
   int next_cmd_ = 0;

@@ -285,6 +285,19 @@ def test_forced_tile_shapes(shape, recompute):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+@pytest.mark.parametrize("budget", [0, 2 << 20])
+def test_graph_replay_parity(budget, jit_always):
+    """Steady-state resident chains replay as CUDA graphs (third sighting on): same bits
+    and reductions as the oracle, untiled and L2-tiled."""
+    prog = P.app_program("miniflow2d", 200, 180, 0, iters=52)
+    want = oracle_record(prog, "reference")
+    got = product_record(prog, "resident", resident_budget=budget)
+    rt = got.pop("_rt")
+    want.pop("_rt", None)
+    assert not compare(want, got, check_audit=False, check_totals=False)
+    assert rt.device()["graph_launches"] >= 2
+
+
 def test_slab_runtime_with_nccl_single_rank():
     """The multi-GPU path on one GPU: a 1-rank NCCL communicator, a dim-0 window with
     ghost rows, all-reduce of the fieldsum — same bits / same reduction as plain."""
