@@ -100,8 +100,11 @@ int ooc_graph_end(ooc_ctx* ctx, int queue, long long kernels, ooc_graph** out);
 int ooc_graph_launch(ooc_ctx* ctx, int queue, ooc_graph* g);
 void ooc_graph_destroy(ooc_graph* g);
 /* 1 when every specialised-kernel structure seen so far has finished tile-shape
- * tuning (graphs must not bake a tuning launch). */
+ * tuning. */
 int ooc_jit_settled(void);
+/* freeze = 1: launches of structures still being tuned use the fastest shape measured
+ * so far (no timing launches) — set while capturing a graph. */
+void ooc_jit_freeze(int freeze);
 
 /* ------------------------------------------------------------ box views and copies */
 /* A strided window covering the box [lo, hi) in global index space: element p
@@ -223,6 +226,7 @@ typedef struct {
   long long comm_bytes;
   long long jit_host_us;  /* host time spent preparing specialised launches */
   long long graph_launches;
+  long long jit_unsettled;  /* specialised launches made while their shape was still being tuned */
 } ooc_dev_stats;
 int ooc_stats(ooc_ctx* ctx, ooc_dev_stats* out);
 int ooc_stats_reset(ooc_ctx* ctx);

@@ -1314,6 +1314,7 @@ struct Tuning {
   int best = -1;
 };
 std::unordered_map<std::string, Tuning> g_tune;
+bool g_frozen = false;
 
 // Candidate tile shapes; shapes whose column block (128*P) wastes more than 20 %
 // of a short contiguous row (3-D grids) are replaced by narrower ones.
@@ -1498,7 +1499,12 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
   if (T.best < 0) settle(T);
   int pick = T.best;
   bool timing = false;
-  if (pick < 0) {
+  if (pick < 0 && g_frozen) {  // graph capture: no tuning launch gets baked in
+    pick = 0;
+    for (std::size_t i = 0; i < T.cands.size(); ++i)
+      if (T.ns_per_point[i] >= 0 && (T.ns_per_point[pick] < 0 || T.ns_per_point[i] < T.ns_per_point[pick]))
+        pick = static_cast<int>(i);
+  } else if (pick < 0) {
     for (std::size_t i = 0; i < T.cands.size() && pick < 0; ++i)
       if (!T.issued[i]) pick = static_cast<int>(i);
     if (pick < 0) {
@@ -1513,6 +1519,7 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
       timing = true;
     }
   }
+  if (T.best < 0) c->stats.jit_unsettled++;
   Shape sh = T.cands[pick];
   Compiled k;
   std::string err;
@@ -1627,6 +1634,8 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
 }
 
 }  // namespace oocdev
+
+extern "C" void ooc_jit_freeze(int freeze) { g_frozen = freeze != 0; }
 
 extern "C" int ooc_jit_settled(void) {
   std::lock_guard<std::mutex> lk(g_cache_mu);

@@ -15,6 +15,7 @@
 // omits (kernels of tile t wait for the H2D of tile t).
 #include "ooc/gpu_engine.hpp"
 
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 
@@ -937,8 +938,24 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
     finish_chain(chain, out.reduction_slot, pc);
     return;
   }
-  const bool capture = ge && ge->seen >= 3 && ooc_jit_settled();  // both parities by the 4th
-  if (capture) DEV(ooc_graph_begin(ctx_, OOC_Q_COMPUTE));
+  // capture on the third sighting (tuning-complete chains from the second); shapes
+  // still being tuned are frozen at the fastest measured
+  const bool capture = ge && (ge->settled || ge->seen >= 3);
+  static const bool gdbg = std::getenv("OOC_GRAPH_DEBUG") != nullptr;
+  if (gdbg)
+    std::fprintf(stderr, "graph: chain %d loops %zu ok %d entry %d seen %d par %d settled %d graphs %zu\n",
+                 chain.chain_id, chain.loops.size(), graphs_ok ? 1 : 0, ge ? 1 : 0, ge ? ge->seen : -1, par,
+                 ge && ge->settled ? 1 : 0, graphs_.size());
+  long long unsettled0 = 0;
+  if (ge && !capture) {
+    ooc_dev_stats st{};
+    DEV(ooc_stats(ctx_, &st));
+    unsettled0 = st.jit_unsettled;
+  }
+  if (capture) {
+    ooc_jit_freeze(1);
+    DEV(ooc_graph_begin(ctx_, OOC_Q_COMPUTE));
+  }
   for (const ParLoop& l : chain.loops)
     if (l.has_reduction())
       DEV(ooc_reduce_reset(ctx_, OOC_Q_COMPUTE, out.reduction_slot.at(l.id), lower_loop(l).reduce_op));
@@ -973,8 +990,13 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
     }
   flush_group(OOC_Q_COMPUTE);
   if (capture) {
+    ooc_jit_freeze(0);
     DEV(ooc_graph_end(ctx_, OOC_Q_COMPUTE, -1, &ge->g[par]));
     DEV(ooc_graph_launch(ctx_, OOC_Q_COMPUTE, ge->g[par]));
+  } else if (ge) {
+    ooc_dev_stats st{};
+    DEV(ooc_stats(ctx_, &st));
+    ge->settled = ge->seen >= 2 && st.jit_unsettled == unsettled0;
   }
   if (halos && comm_ready_) {
     // slab decomposition: refresh every ghost band from the neighbours' owned rows,

@@ -187,6 +187,7 @@ class GpuEngine {
   struct GraphEntry {
     int seen = 0;
     int flip = 0;
+    bool settled = false;  // the last direct run made no tuning launch
     ooc_graph* g[2] = {nullptr, nullptr};
     std::vector<int> slots[2];
   };
