@@ -1053,16 +1053,9 @@ std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan) c
     }
     put_i(lw.reduce_op);
   }
-  if (plan) {
+  if (plan) {  // plans live in the runtime's PlanCache (never evicted): identity suffices
+    put(&plan, sizeof plan);
     put_i(plan->tile_count);
-    for (std::size_t j = 0; j < chain.loops.size(); ++j)
-      for (int t = 0; t < plan->tile_count; ++t) {
-        const Extent e = plan->subrange(static_cast<int>(j), t);
-        for (int d = 0; d < 3; ++d) {
-          put_i(e.lo[d]);
-          put_i(e.hi[d]);
-        }
-      }
   }
   return k;
 }

@@ -150,8 +150,12 @@ const PlanCache::Entry& Runtime::plan_for(const LoopChain& chain) {  // runtime.
   // resident (in-core) tiling has no slot rotation: one tile's working set must fit
   // the budget (e.g. L2), so choose the smallest T with slot_bytes <= budget.
   if (opts_.executor == ExecutorKind::resident) budget = 3 * opts_.resident_budget;
-  TileChoice c = choose_tile_count(mesh_, chain, budget, opts_.tiled_dim);
-  return plans_.get(mesh_, chain, c.tile_count, opts_.tiled_dim);
+  // the linear scan is O(T) plans: remember its answer per chain structure and budget
+  const std::string key = chain_structural_key(mesh_, chain) + "|" + std::to_string(budget);
+  auto it = tile_choice_.find(key);
+  if (it == tile_choice_.end())
+    it = tile_choice_.emplace(key, choose_tile_count(mesh_, chain, budget, opts_.tiled_dim).tile_count).first;
+  return plans_.get(mesh_, chain, it->second, opts_.tiled_dim);
 }
 
 void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148

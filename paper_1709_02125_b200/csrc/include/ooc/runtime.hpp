@@ -253,6 +253,7 @@ class Runtime {
   int next_loop_id_ = 0;
   int next_chain_id_ = 0;
   PlanCache plans_;
+  std::map<std::string, int> tile_choice_;  // choose_tile_count results per structure+budget
   std::vector<FlushRecord> flush_log_;
   std::vector<LoopMetric> loop_metrics_;
   std::map<int, std::size_t> metric_index_;
