@@ -62,6 +62,7 @@ struct Api {
                      unsigned, CUstream, void**, void**) = nullptr;
   CUresult (*error_string)(CUresult, const char**) = nullptr;
   CUresult (*func_set_attr)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*launch_ex)(const CUlaunchConfig*, CUfunction, void**, void**) = nullptr;
   CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
   CUresult (*encode_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -95,6 +96,7 @@ Api& api() {
     BIND(cu, launch, "cuLaunchKernel");
     BIND(cu, error_string, "cuGetErrorString");
     BIND(cu, func_set_attr, "cuFuncSetAttribute");
+    BIND(cu, launch_ex, "cuLaunchKernelEx");
     BIND(cu, occupancy, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
     BIND(cu, encode_tiled, "cuTensorMapEncodeTiled");
   }
@@ -168,6 +170,10 @@ __device__ __forceinline__ double ooc_red(int op, double acc, double v) {
 
 const char* kRegKernel = R"CUDA(
 extern "C" __global__ void __launch_bounds__(OOC_BLOCK) ooc_jit_kernel(const __grid_constant__ JitParams p) {
+  // programmatic dependent launch: this grid may start while the previous one drains;
+  // nothing global is touched before the previous grid has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long nBq = (p.nB + OOC_Q - 1) / OOC_Q;
   const long long rows = p.nA * nBq;
   const long long xblocks = (p.nC + OOC_BLOCK * OOC_P - 1) / (OOC_BLOCK * OOC_P);
@@ -268,6 +274,10 @@ extern "C" __global__ void __launch_bounds__(OOC_THREADS + 32) ooc_jit_kernel(co
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: barrier setup overlapped the previous grid's drain;
+  // no global access (TMA loads, stores) before it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #if OOC_RED
   double acc = p.red_op == 2 ? __longlong_as_double(0x7ff0000000000000LL)
              : p.red_op == 3 ? __longlong_as_double(0xfff0000000000000LL) : 0.0;
@@ -1613,8 +1623,28 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     cudaEventRecord(e.first, st);
   }
   void* args[] = {jp, maps};
-  CUresult cr = api().launch(k.fn, gx, gy, 1, k.block, 1, 1, static_cast<unsigned>(k.smem),
-                             reinterpret_cast<CUstream>(st), args, nullptr);
+  CUresult cr;
+  static const bool pdl = !(std::getenv("OOC_PDL") && std::atoi(std::getenv("OOC_PDL")) == 0);
+  if (pdl && api().launch_ex) {
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg{};
+    cfg.gridDimX = gx;
+    cfg.gridDimY = gy;
+    cfg.gridDimZ = 1;
+    cfg.blockDimX = static_cast<unsigned>(k.block);
+    cfg.blockDimY = 1;
+    cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = static_cast<unsigned>(k.smem);
+    cfg.hStream = reinterpret_cast<CUstream>(st);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cr = api().launch_ex(&cfg, k.fn, args, nullptr);
+  } else {
+    cr = api().launch(k.fn, gx, gy, 1, k.block, 1, 1, static_cast<unsigned>(k.smem),
+                      reinterpret_cast<CUstream>(st), args, nullptr);
+  }
   delete jp;
   delete maps;
   if (cr != CUDA_SUCCESS) {
