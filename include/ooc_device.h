@@ -178,6 +178,31 @@ int ooc_launch_loop(ooc_ctx* ctx, int queue, const ooc_loop* loop);
  * it. Reducing loops are launched alone. Same observable result as n launches. */
 int ooc_launch_group(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n);
 
+/* Row-sweep fusion (2-D, new): a run of consecutive loops — any stencils, including
+ * column-offset reads of values written earlier in the run — executed by one kernel
+ * that streams the mesh through shared-memory rings (csrc/device/sweep.cu). A dataset
+ * the run both reads from memory and writes ("out of place") is written to a
+ * caller-provided buffer of identical layout; every element of its view inside the
+ * run's bounding box is written there, so the caller swaps the two buffers after the
+ * launch. Everything else is updated in place. Same observable result as launching
+ * the loops one by one (plus the swap).
+ * ooc_sweep_check: 1 = the run is sweepable, 0 = not. flags (may be NULL) receive, per
+ * loop i and argument a, flags[i*OOC_MAX_ARGS + a] = 1 (out of place) | 2 (read from
+ * memory by the run) | 4 (written by the run).
+ * A redirect with dst = NULL marks a dataset whose values the run produces but nobody
+ * reads before they are overwritten (the caller's dead-store analysis): not stored,
+ * and for an out-of-place dataset no swap. */
+typedef struct {
+  const double* src; /* view data of the dataset before the launch */
+  double* dst;       /* buffer receiving its new values (same box and strides); NULL: dead */
+} ooc_redirect;
+int ooc_sweep_check(const ooc_loop* loops, int n, int* flags);
+int ooc_launch_sweep(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n, const ooc_redirect* redirects,
+                     int nredirects);
+/* JSON description of the sweep plan (lags, halos, rings); compile = 1 also builds the
+ * kernel with NVRTC for sm_100a (no GPU needed). */
+int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int len, int compile);
+
 /* Specialised kernels: the par_loop kernel template instantiated per loop body
  * (or fused group) with NVRTC at first use, cached per process. mode 0: never
  * (interpreter only), 1: for launches of >= min_points points (default 2^18),
@@ -227,6 +252,7 @@ typedef struct {
   long long jit_host_us;  /* host time spent preparing specialised launches */
   long long graph_launches;
   long long jit_unsettled;  /* specialised launches made while their shape was still being tuned */
+  long long sweep_launches; /* row-sweep launches (ooc_launch_sweep) */
 } ooc_dev_stats;
 int ooc_stats(ooc_ctx* ctx, ooc_dev_stats* out);
 int ooc_stats_reset(ooc_ctx* ctx);

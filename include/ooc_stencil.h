@@ -160,6 +160,9 @@ const char* ooc_rt_dist_plan_json(ooc_runtime* rt, int chain);
 /* Group recorded chain `chain` as the engine would (fuse = 1: loop fusion) and
  * generate + NVRTC-compile each group's specialised sm_100a kernel (no GPU needed). */
 const char* ooc_rt_chain_jit_check(ooc_runtime* rt, int chain, int fuse);
+/* Row-sweep partition of a recorded chain (resident, untiled): JSON list of runs with
+ * their sweep plans; compile = 1 builds each run's kernel with NVRTC (no GPU). */
+const char* ooc_rt_chain_sweep_check(ooc_runtime* rt, int chain, int compile);
 /* Process-wide fusion policy: 1 (default; env OOC_ROW_RECOMPUTE=0 turns it off) admits
  * row-recompute groups (neighbour reads along the row dimension of values written
  * earlier in the launch, re-evaluated in-thread). */

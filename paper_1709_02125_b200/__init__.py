@@ -348,6 +348,15 @@ class Runtime:
         """Compile (NVRTC, sm_100a, no GPU needed) the specialised kernels of a recorded chain."""
         return self._json(_native.lib().ooc_rt_chain_jit_check, chain, int(fuse))
 
+    def chain_sweep_check(self, chain, compile=True):
+        """Row-sweep runs of a recorded chain with their plans (lags, halos, rings);
+        compile=True builds each run's kernel for sm_100a (NVRTC, no GPU needed)."""
+        out = self._json(_native.lib().ooc_rt_chain_sweep_check, chain, int(compile))
+        for g in out:
+            if g["ok"] and g["plan"].startswith("{"):
+                g["plan"] = json.loads(g["plan"].split("\n")[0])
+        return out
+
     def chain_oracle(self, chain, tiles):
         return self._json(_native.lib().ooc_rt_chain_oracle_json, chain, tiles)
 

@@ -24,7 +24,8 @@ CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INC = ["-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(CSRC, "include")]
 
-DEV_SRCS = ["device/ooc_device.cu", "device/loop_kernels.cu", "device/jit.cu", "device/comm.cu"]
+DEV_SRCS = ["device/ooc_device.cu", "device/loop_kernels.cu", "device/jit.cu", "device/sweep.cu",
+            "device/comm.cu"]
 HOST_SRCS = ["host/core.cpp", "host/tiler.cpp", "host/runtime.cpp", "host/gpu_engine.cpp",
              "host/apps.cpp", "host/capi.cpp"]
 HEADERS_DEV = ["device/internal.cuh", "device/jit.cuh"]

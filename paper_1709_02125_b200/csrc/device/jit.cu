@@ -1204,44 +1204,11 @@ bool pick_and_generate(const ooc_loop* Ls, int n, JitParams& jp, std::string& bo
   return false;
 }
 
-// load = false: compile only (checks that the generated kernel builds for sm_100a;
-// needs NVRTC but no driver/GPU).
-bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled& out,
-             std::string& err, bool load = true, long long smem = 0) {
+// NVRTC-compile `src` for sm_100a (exact arithmetic flags), load it and fetch `kname`;
+// with smem > 0 also raise the dynamic shared-memory limit and record the occupancy.
+bool nvrtc_build(const std::string& src, const char* kname, int block, long long smem, Compiled& out,
+                 std::string& err, bool load) {
   Api& a = api();
-  if (load ? !a.ok : !a.nvrtc_ok) {
-    err = a.why;
-    return false;
-  }
-  std::string src = std::string(std::getenv("OOC_JIT_NO_TRAP") ? "#define OOC_NO_TRAP 1\n" : "") +
-                    std::string(std::getenv("OOC_TMA_TRACE") ? "#define OOC_TMA_TRACE 1\n" : "") +
-                    "#define OOC_BLOCK " + std::to_string(block) + "\n#define OOC_Q " +
-                    std::to_string(Q) + "\n#define OOC_P " +
-                    std::to_string(P) + "\n#define OOC_RED " + (red ? "1" : "0") +
-                    "\n#define OOC_JMAX_LOOPS " + std::to_string(OOC_JMAX_LOOPS) +
-                    "\n#define OOC_JMAX_FAMILIES " + std::to_string(OOC_JMAX_FAMILIES) +
-                    "\n#define OOC_JMAX_WRITES " + std::to_string(OOC_JMAX_WRITES) +
-                    "\n#define OOC_JMAX_CONST " + std::to_string(OOC_JMAX_CONST) +
-                    "\n#define OOC_JMAX_VIEWS " + std::to_string(OOC_JMAX_VIEWS) + "\n";
-  if (key.rfind("<<TMA>>\n", 0) == 0) {
-    // "<<TMA>>\n" defines "<<ISSUE>>\n" issue-code "<<TBODY>>\n" point-body
-    const std::size_t ip = key.find("<<ISSUE>>\n"), sp = key.find("<<SHIFT>>\n"),
-                      bp = key.find("<<TBODY>>\n");
-    std::string tpl = std::string(kCommon) + kTmaKernel;
-    tpl.replace(tpl.find("<<ISSUE>>"), 9, key.substr(ip + 10, sp - ip - 10));
-    tpl.replace(tpl.find("<<SHIFT>>"), 9, key.substr(sp + 10, bp - sp - 10));
-    const std::string tbody = key.substr(bp + 10);
-    for (std::size_t at; (at = tpl.find("<<BODY>>")) != std::string::npos;) tpl.replace(at, 8, tbody);
-    src += key.substr(8, ip - 8) + tpl;
-  } else {
-    std::string tpl = std::string(kCommon) + kRegKernel;
-    const std::size_t fpos = key.find("<<FAST>>\n");
-    const std::string slow_body = key.substr(9, fpos - 9);  // after "<<SLOW>>\n"
-    const std::string fast_body = key.substr(fpos + 9);
-    tpl.replace(tpl.find("<<FAST>>"), 8, fast_body);
-    tpl.replace(tpl.find("<<BODY>>"), 8, slow_body);
-    src += tpl;
-  }
   nvrtcProgram prog;
   if (a.create(&prog, src.c_str(), "ooc_par_loop.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     err = "nvrtcCreateProgram failed";
@@ -1282,13 +1249,11 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
     err = std::string("cuModuleLoadData: ") + s;
     return false;
   }
-  if (a.get_function(&out.fn, mod, "ooc_jit_kernel") != CUDA_SUCCESS) {
+  if (a.get_function(&out.fn, mod, kname) != CUDA_SUCCESS) {
     err = "cuModuleGetFunction failed";
     return false;
   }
   out.block = block;
-  out.Q = Q;
-  out.P = P;
   out.smem = smem;
   out.occ = 1;
   if (smem > 0) {
@@ -1306,6 +1271,47 @@ bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled
     out.occ = occ;
   }
   return true;
+}
+
+// load = false: compile only (checks that the generated kernel builds for sm_100a;
+// needs NVRTC but no driver/GPU).
+bool compile(const std::string& key, int block, int Q, int P, bool red, Compiled& out,
+             std::string& err, bool load = true, long long smem = 0) {
+  Api& a = api();
+  if (load ? !a.ok : !a.nvrtc_ok) {
+    err = a.why;
+    return false;
+  }
+  std::string src = std::string(std::getenv("OOC_JIT_NO_TRAP") ? "#define OOC_NO_TRAP 1\n" : "") +
+                    std::string(std::getenv("OOC_TMA_TRACE") ? "#define OOC_TMA_TRACE 1\n" : "") +
+                    "#define OOC_BLOCK " + std::to_string(block) + "\n#define OOC_Q " +
+                    std::to_string(Q) + "\n#define OOC_P " +
+                    std::to_string(P) + "\n#define OOC_RED " + (red ? "1" : "0") +
+                    "\n#define OOC_JMAX_LOOPS " + std::to_string(OOC_JMAX_LOOPS) +
+                    "\n#define OOC_JMAX_FAMILIES " + std::to_string(OOC_JMAX_FAMILIES) +
+                    "\n#define OOC_JMAX_WRITES " + std::to_string(OOC_JMAX_WRITES) +
+                    "\n#define OOC_JMAX_CONST " + std::to_string(OOC_JMAX_CONST) +
+                    "\n#define OOC_JMAX_VIEWS " + std::to_string(OOC_JMAX_VIEWS) + "\n";
+  if (key.rfind("<<TMA>>\n", 0) == 0) {
+    // "<<TMA>>\n" defines "<<ISSUE>>\n" issue-code "<<TBODY>>\n" point-body
+    const std::size_t ip = key.find("<<ISSUE>>\n"), sp = key.find("<<SHIFT>>\n"),
+                      bp = key.find("<<TBODY>>\n");
+    std::string tpl = std::string(kCommon) + kTmaKernel;
+    tpl.replace(tpl.find("<<ISSUE>>"), 9, key.substr(ip + 10, sp - ip - 10));
+    tpl.replace(tpl.find("<<SHIFT>>"), 9, key.substr(sp + 10, bp - sp - 10));
+    const std::string tbody = key.substr(bp + 10);
+    for (std::size_t at; (at = tpl.find("<<BODY>>")) != std::string::npos;) tpl.replace(at, 8, tbody);
+    src += key.substr(8, ip - 8) + tpl;
+  } else {
+    std::string tpl = std::string(kCommon) + kRegKernel;
+    const std::size_t fpos = key.find("<<FAST>>\n");
+    const std::string slow_body = key.substr(9, fpos - 9);  // after "<<SLOW>>\n"
+    const std::string fast_body = key.substr(fpos + 9);
+    tpl.replace(tpl.find("<<FAST>>"), 8, fast_body);
+    tpl.replace(tpl.find("<<BODY>>"), 8, slow_body);
+    src += tpl;
+  }
+  return nvrtc_build(src, "ooc_jit_kernel", block, smem, out, err, load) && ((out.Q = Q), (out.P = P), true);
 }
 
 }  // namespace
@@ -1659,6 +1665,66 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* Ls, int n, int* blocks_o
     T.points[pick] = pts;
   }
   *blocks_out = static_cast<int>(gx * gy);
+  c->stats.jit_launches++;
+  return OOC_OK;
+}
+
+
+int jit_policy(long long* min_points) {
+  const int m = mode();
+  if (min_points) *min_points = g_min_points;
+  return m;
+}
+
+bool jit_available(bool load, std::string& why) {
+  Api& a = api();
+  why = a.why;
+  return load ? a.ok : a.nvrtc_ok;
+}
+
+bool jit_build_kernel(const std::string& src, const char* kname, int block, long long smem, void** fn,
+                      int* occ, std::string& err, bool load) {
+  if (!jit_available(load, err)) return false;
+  Compiled k;
+  if (!nvrtc_build(src, kname, block, smem, k, err, load)) return false;
+  if (fn) *fn = reinterpret_cast<void*>(k.fn);
+  if (occ) *occ = k.occ;
+  return true;
+}
+
+int jit_launch_kernel(ooc_ctx* c, int q, void* fn, unsigned gx, unsigned gy, unsigned block, unsigned smem,
+                      void** args) {
+  cudaStream_t st = c->q[q];
+  CUresult cr;
+  static const bool pdl = !(std::getenv("OOC_PDL") && std::atoi(std::getenv("OOC_PDL")) == 0);
+  if (pdl && api().launch_ex) {
+    CUlaunchAttribute attr[1];
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg{};
+    cfg.gridDimX = gx;
+    cfg.gridDimY = gy;
+    cfg.gridDimZ = 1;
+    cfg.blockDimX = block;
+    cfg.blockDimY = 1;
+    cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = smem;
+    cfg.hStream = reinterpret_cast<CUstream>(st);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cr = api().launch_ex(&cfg, reinterpret_cast<CUfunction>(fn), args, nullptr);
+  } else {
+    cr = api().launch(reinterpret_cast<CUfunction>(fn), gx, gy, 1, block, 1, 1, smem,
+                      reinterpret_cast<CUstream>(st), args, nullptr);
+  }
+  if (cr != CUDA_SUCCESS) {
+    const char* s = "?";
+    if (api().error_string) api().error_string(cr, &s);
+    set_error(std::string("JIT cuLaunchKernelEx: ") + s);
+    return OOC_ERR_CUDA;
+  }
+  c->stats.kernel_launches++;
+  c->stats.special_launches++;
   c->stats.jit_launches++;
   return OOC_OK;
 }

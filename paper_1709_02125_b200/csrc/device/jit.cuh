@@ -2,6 +2,8 @@
 // template declares an identical struct.
 #pragma once
 
+#include <string>
+
 #include "ooc_device.h"
 
 #define OOC_JMAX_LOOPS 8
@@ -31,4 +33,13 @@ struct JitParams {
 
 namespace oocdev {
 int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* loops, int n, int* blocks_out);
+// Generic NVRTC path shared with the row-sweep kernels (sweep.cu): build `kname` from
+// `src` for sm_100a with the exact-arithmetic flags; launch with programmatic
+// dependent launch on queue q (counts one specialised launch).
+int jit_policy(long long* min_points);  // OOC_JIT mode (0/1/2) and its size threshold
+bool jit_available(bool load, std::string& why);
+bool jit_build_kernel(const std::string& src, const char* kname, int block, long long smem, void** fn,
+                      int* occ, std::string& err, bool load);
+int jit_launch_kernel(ooc_ctx* c, int q, void* fn, unsigned gx, unsigned gy, unsigned block, unsigned smem,
+                      void** args);
 }

@@ -1,0 +1,750 @@
+// Row-sweep fusion: a whole run of 2-D par_loops — typically one or more complete
+// timesteps of an app — executed by ONE kernel that streams the mesh through shared
+// memory once.
+//
+// The register and TMA templates (jit.cu) fuse loops only while every value a point
+// consumes is either in memory or produced at the same point (or recomputable along
+// the row dimension); a read of an in-launch value at a column offset ends the group.
+// miniflow2d's iteration therefore needs two launches and 22 arrays of DRAM traffic.
+// The sweep kernel lifts that restriction the B200 way: each CTA owns a strip of
+// TC columns and walks its rows top to bottom (a 2.5-D streaming sweep). Every dataset
+// the group touches lives in a ring of W_d rows x 128 columns of shared memory; loop i
+// runs `lag_i` rows behind the loads, so when it evaluates row r every value it reads —
+// loaded from HBM, or produced by an earlier loop of the group at any (row, column)
+// offset within the halo — is already in its ring. Per step a CTA:
+//   1. waits for the cp.async loads of this step (issued P steps earlier) and syncs,
+//   2. issues the loads of step s+P (8-byte cp.async, zero-filled outside the view),
+//   3. evaluates the loops in order (one point per thread per loop; a barrier only
+//      between loops that touch a common dataset),
+//   4. stores the final rows of every written dataset to HBM (coalesced, 1 KB rows).
+// DRAM traffic is one read of every input and one write of every output per group,
+// however many loops and timesteps the group spans: miniflow2d goes from 22 arrays
+// per iteration to 13 (one iteration per group) or fewer (several).
+//
+// Correctness constraints, all resolved at generation time from the loops' stencils:
+//  * lags: RAW  lag_reader >= lag_writer + max row offset of the read;
+//          WAR  lag_writer >= lag_reader - min row offset (the ring row is rewritten
+//               only after every earlier loop has read the old value);
+//          WAW  later writers never run ahead of earlier ones;
+//  * column halos: loop j computes h_j extra columns each side, h_j >= h_k + |dc| for
+//    every later loop k reading j's output at column offset dc, so a strip's owned
+//    columns are exact (the halo is recomputed redundantly, never exchanged);
+//  * warm-up rows: a CTA owning rows [r0, r1) starts its sweep `warm` rows earlier —
+//    the depth of the dependency cone — and stores only its own rows;
+//  * out-of-place outputs: a dataset the group both loads and writes is written to a
+//    shadow buffer (the host engine flips the two after the launch), so a neighbouring
+//    CTA's halo / warm-up rows always read the values from before the launch. Datasets
+//    first written in the group (temporaries) are stored in place, only where a loop of
+//    the group writes them.
+// Arithmetic is the same tape order, IEEE binary64, --fmad=false, std::min/max
+// semantics as every other kernel: results are bit-identical to the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "internal.cuh"
+#include "jit.cuh"
+
+using namespace oocdev;
+
+#define SW_MAXL 48
+#define SW_MAXD 16
+#define SW_MAXC 384
+
+namespace {
+
+constexpr int kRC = 128;  // ring row width in columns (TC owned + 2*HC halo)
+
+// Parameter block; the kernel source declares an identical struct.
+struct SweepParams {
+  long long R0, R1, C0, C1;  // launch box: rows [R0,R1) x columns [C0,C1), absolute
+  long long seg_rows;        // rows owned per CTA row-segment
+  long long rng[SW_MAXL][4];  // per loop: rows [0,1), columns [2,3), absolute
+  const double* src[SW_MAXD];
+  double* dst[SW_MAXD];
+  long long s0[SW_MAXD];      // row stride (elements)
+  long long box[SW_MAXD][4];  // view box: rows [0,1), columns [2,3)
+  double cst[SW_MAXC];
+};
+
+const char* kSweepDecl = R"CUDA(
+struct SweepParams {
+  long long R0, R1, C0, C1;
+  long long seg_rows;
+  long long rng[SW_MAXL][4];
+  const double* src[SW_MAXD];
+  double* dst[SW_MAXD];
+  long long s0[SW_MAXD];
+  long long box[SW_MAXD][4];
+  double cst[SW_MAXC];
+};
+__device__ __forceinline__ double ooc_min(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double ooc_max(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ long long sw_floordiv(long long a, long long k) {
+  return a >= 0 ? a / k : -((-a + k - 1) / k);
+}
+__device__ __forceinline__ void sw_cp8(double* dst, const double* src, bool ok) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(s), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+)CUDA";
+
+struct Rd {
+  long long omin = LLONG_MAX, omax = LLONG_MIN, oc = 0;  // row offsets range, max |column offset|
+};
+
+struct SwLoop {
+  long long lag = 0, h = 0;
+  std::vector<int> wds;        // dataset of each write
+  std::map<int, Rd> rd;        // dataset -> read offsets
+  bool barrier = false;        // barrier before this loop (within a step)
+};
+
+struct SwDs {
+  const ooc_view* v = nullptr;
+  bool loaded = false, written = false, oop = false;
+  bool store = false;  // written and still live after the group (not a dead store)
+  long long lagL = 0, lagS = 0, W = 0, off = 0;
+  std::vector<int> writers;
+};
+
+struct SwPlan {
+  int n = 0, K = 2, P = 2, NT = 256;
+  long long HC = 0, TC = 0, warm = 0, lagS_max = 0, smem = 0;
+  long long box[4] = {0, 0, 0, 0};  // launch box rows/cols
+  std::vector<SwLoop> L;
+  std::vector<SwDs> D;
+};
+
+long long smem_budget() {
+  static long long b = [] {
+    const char* e = std::getenv("OOC_SWEEP_SMEM");
+    return e ? std::atoll(e) : 110LL * 1024;
+  }();
+  return b;
+}
+
+bool fail(std::string* why, const std::string& m) {
+  if (why) *why = m;
+  return false;
+}
+
+// Analyse a group for the sweep template with K rows per step (NT = 128*K threads)
+// and a P-step load prefetch. Fills the plan (lags, halos, rings, barriers).
+bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* why,
+             const std::vector<const double*>* dead = nullptr) {
+  pl = SwPlan{};
+  pl.n = n;
+  pl.K = K;
+  pl.P = P;
+  pl.NT = kRC;
+  if (n < 1 || n > SW_MAXL) return fail(why, "group size");
+  pl.L.resize(static_cast<std::size_t>(n));
+  int ncst = 0;
+  auto ds_of = [&](const ooc_view& v) -> int {
+    for (std::size_t d = 0; d < pl.D.size(); ++d) {
+      const ooc_view& w = *pl.D[d].v;
+      if (w.data != v.data) continue;
+      for (int k = 0; k < 3; ++k)
+        if (w.lo[k] != v.lo[k] || w.hi[k] != v.hi[k] || w.stride[k] != v.stride[k]) return -2;
+      return static_cast<int>(d);
+    }
+    if (v.stride[1] != 1 || v.lo[2] != 0 || v.hi[2] != 1) return -2;
+    if (pl.D.size() >= SW_MAXD) return -3;
+    SwDs D;
+    D.v = &v;
+    pl.D.push_back(D);
+    return static_cast<int>(pl.D.size()) - 1;
+  };
+  long long tape_total = 0;
+  for (int i = 0; i < n; ++i) {
+    const ooc_loop& L = Ls[i];
+    SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+    if (L.ndim != 2) return fail(why, "not 2-D");
+    if (L.reduce_op != OOC_RED_NONE) return fail(why, "reduction");
+    if (L.lo[2] != 0 || L.hi[2] != 1 || L.hi[0] <= L.lo[0] || L.hi[1] <= L.lo[1]) return fail(why, "range");
+    tape_total += L.ntape;
+    for (int t = 0; t < L.ntape; ++t) {
+      const ooc_ins& in = L.tape[t];
+      if (in.op == OOC_OP_CONST) {
+        ++ncst;
+      } else if (in.op == OOC_OP_READ) {
+        if (in.arg < 0 || in.arg >= L.nargs) return fail(why, "bad arg");
+        const int d = ds_of(L.args[in.arg]);
+        if (d < 0) return fail(why, "dataset views differ / too many datasets");
+        if (in.offset[2] != 0 || std::llabs(in.offset[0]) > 8 || std::llabs(in.offset[1]) > 8)
+          return fail(why, "offset");
+        Rd& r = S.rd[d];
+        r.omin = std::min<long long>(r.omin, in.offset[0]);
+        r.omax = std::max<long long>(r.omax, in.offset[0]);
+        r.oc = std::max<long long>(r.oc, std::llabs(in.offset[1]));
+      } else if (in.op < OOC_OP_ADD || in.op > OOC_OP_MAX) {
+        return fail(why, "opcode");
+      }
+    }
+    for (int w = 0; w < L.nwrites; ++w) {
+      const int d = ds_of(L.args[L.write_arg[w]]);
+      if (d < 0) return fail(why, "dataset views differ / too many datasets");
+      S.wds.push_back(d);
+      auto it = S.rd.find(d);
+      if (it != S.rd.end() && (it->second.omin != 0 || it->second.omax != 0 || it->second.oc != 0))
+        return fail(why, "loop reads its own output at an offset");
+    }
+  }
+  if (ncst > SW_MAXC) return fail(why, "constants");
+  if (tape_total > 1600) return fail(why, "tape length");
+  const long long nd = static_cast<long long>(pl.D.size());
+  auto writes = [&](int j, int d) {
+    for (int x : pl.L[static_cast<std::size_t>(j)].wds)
+      if (x == d) return true;
+    return false;
+  };
+  auto reads = [&](int j, int d) { return pl.L[static_cast<std::size_t>(j)].rd.count(d) > 0; };
+  for (int d = 0; d < nd; ++d)
+    for (int j = 0; j < n; ++j)
+      if (writes(j, d)) pl.D[static_cast<std::size_t>(d)].writers.push_back(j);
+  // ---- column halos (backward)
+  for (int k = n - 1; k >= 0; --k)
+    for (const auto& [d, r] : pl.L[static_cast<std::size_t>(k)].rd)
+      for (int j = 0; j < k; ++j)
+        if (writes(j, d)) pl.L[static_cast<std::size_t>(j)].h = std::max(pl.L[static_cast<std::size_t>(j)].h,
+                                                                        pl.L[static_cast<std::size_t>(k)].h + r.oc);
+  long long HC = 0;
+  for (const SwLoop& S : pl.L) {
+    HC = std::max(HC, S.h);
+    for (const auto& [d, r] : S.rd) HC = std::max(HC, S.h + r.oc);
+  }
+  if (HC > 16) return fail(why, "column halo");
+  pl.HC = HC;
+  pl.TC = kRC - 2 * HC;
+  // ---- loaded / written / out-of-place
+  for (int d = 0; d < nd; ++d) {
+    SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    D.written = !D.writers.empty();
+    for (int k = 0; k < n && !D.loaded; ++k) {
+      if (!reads(k, d)) continue;
+      const ooc_loop& L = Ls[k];
+      const Rd& r = pl.L[static_cast<std::size_t>(k)].rd.at(d);
+      const long long b0 = L.lo[0] + r.omin, b1 = L.hi[0] + r.omax, c0 = L.lo[1] - r.oc, c1 = L.hi[1] + r.oc;
+      bool covered = false;
+      for (int j = 0; j < k && !covered; ++j)
+        if (writes(j, d))
+          covered = Ls[j].lo[0] <= b0 && Ls[j].hi[0] >= b1 && Ls[j].lo[1] <= c0 && Ls[j].hi[1] >= c1;
+      if (!covered) D.loaded = true;
+    }
+    D.oop = D.loaded && D.written;
+    D.store = D.written && !(dead && std::find(dead->begin(), dead->end(), D.v->data) != dead->end());
+  }
+  // ---- lags (forward)
+  for (int i = 0; i < n; ++i) {
+    SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+    long long lag = LLONG_MIN;
+    for (const auto& [d, r] : S.rd)
+      for (int j = 0; j < i; ++j)
+        if (writes(j, d)) lag = std::max(lag, pl.L[static_cast<std::size_t>(j)].lag + r.omax);
+    for (int d : S.wds)
+      for (int j = 0; j < i; ++j) {
+        const SwLoop& J = pl.L[static_cast<std::size_t>(j)];
+        if (reads(j, d)) lag = std::max(lag, J.lag - J.rd.at(d).omin);
+        if (writes(j, d)) lag = std::max(lag, J.lag);
+      }
+    S.lag = lag == LLONG_MIN ? 0 : lag;
+  }
+  for (int d = 0; d < nd; ++d) {
+    SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    if (!D.loaded) continue;
+    long long l = LLONG_MAX;
+    for (int k = 0; k < n; ++k) {
+      if (reads(k, d)) l = std::min(l, pl.L[static_cast<std::size_t>(k)].lag - pl.L[static_cast<std::size_t>(k)].rd.at(d).omax);
+      if (writes(k, d)) l = std::min(l, pl.L[static_cast<std::size_t>(k)].lag);
+    }
+    D.lagL = l;
+  }
+  long long m = LLONG_MAX;
+  for (const SwLoop& S : pl.L) m = std::min(m, S.lag);
+  for (const SwDs& D : pl.D)
+    if (D.loaded) m = std::min(m, D.lagL);
+  for (SwLoop& S : pl.L) S.lag -= m;
+  for (SwDs& D : pl.D)
+    if (D.loaded) D.lagL -= m;
+  for (SwDs& D : pl.D)
+    for (int j : D.writers) D.lagS = std::max(D.lagS, pl.L[static_cast<std::size_t>(j)].lag);
+  // ---- ring windows: rows live at step s are [sK - A, sK + B]
+  long long off = 0;
+  for (int d = 0; d < nd; ++d) {
+    SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    long long A = LLONG_MIN, B = LLONG_MIN;
+    if (D.loaded) {
+      A = std::max(A, D.lagL);
+      B = std::max(B, (P + 1) * K - 1 - D.lagL);
+    }
+    if (D.written) A = std::max(A, D.lagS);
+    for (int k = 0; k < n; ++k) {
+      const SwLoop& S = pl.L[static_cast<std::size_t>(k)];
+      if (reads(k, d)) {
+        A = std::max(A, S.lag - S.rd.at(d).omin);
+        B = std::max(B, K - 1 - S.lag + S.rd.at(d).omax);
+      }
+      if (writes(k, d)) {
+        A = std::max(A, S.lag);
+        B = std::max(B, K - 1 - S.lag);
+      }
+    }
+    D.W = 1;
+    while (D.W < std::max<long long>(A + B + 1, K)) D.W *= 2;  // power of two: slot = row & (W-1)
+    D.off = off;
+    off += D.W * kRC;
+  }
+  pl.smem = off * 8;
+  if (pl.smem > smem_budget()) return fail(why, "shared memory");
+  // ---- warm-up depth: first correct row of every version (relative to the sweep start)
+  const long long NONE = LLONG_MIN / 4;
+  std::vector<long long> F(static_cast<std::size_t>(nd), NONE);
+  for (int d = 0; d < nd; ++d)
+    if (pl.D[static_cast<std::size_t>(d)].loaded) F[static_cast<std::size_t>(d)] = -pl.D[static_cast<std::size_t>(d)].lagL;
+  for (int i = 0; i < n; ++i) {
+    const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+    long long Fi = -S.lag;
+    for (const auto& [d, r] : S.rd) {
+      if (F[static_cast<std::size_t>(d)] == NONE) return fail(why, "read of an unwritten, unloaded dataset");
+      Fi = std::max(Fi, F[static_cast<std::size_t>(d)] - r.omin);
+    }
+    for (int d : S.wds) F[static_cast<std::size_t>(d)] = F[static_cast<std::size_t>(d)] == NONE ? Fi : std::max(F[static_cast<std::size_t>(d)], Fi);
+  }
+  pl.warm = 0;
+  pl.lagS_max = 0;
+  for (int d = 0; d < nd; ++d)
+    if (pl.D[static_cast<std::size_t>(d)].store) {
+      pl.warm = std::max(pl.warm, F[static_cast<std::size_t>(d)]);
+      pl.lagS_max = std::max(pl.lagS_max, pl.D[static_cast<std::size_t>(d)].lagS);
+    }
+  // ---- barriers: a loop starts a new region when it touches a dataset a loop of the
+  // current region wrote, or writes one the region read
+  std::vector<char> rr(static_cast<std::size_t>(nd), 0), ww(static_cast<std::size_t>(nd), 0);
+  for (int i = 0; i < n; ++i) {
+    SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+    bool conflict = false;
+    for (const auto& [d, r] : S.rd) conflict = conflict || ww[static_cast<std::size_t>(d)];
+    for (int d : S.wds) conflict = conflict || ww[static_cast<std::size_t>(d)] || rr[static_cast<std::size_t>(d)];
+    if (conflict && i > 0) {
+      S.barrier = true;
+      std::fill(rr.begin(), rr.end(), 0);
+      std::fill(ww.begin(), ww.end(), 0);
+    }
+    for (const auto& [d, r] : S.rd) rr[static_cast<std::size_t>(d)] = 1;
+    for (int d : S.wds) ww[static_cast<std::size_t>(d)] = 1;
+  }
+  // ---- launch box: loop ranges plus the allocations of out-of-place outputs (their
+  // shadow must receive every element, written or not)
+  long long bx[4] = {LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN};
+  auto grow = [&](long long r0, long long r1, long long c0, long long c1) {
+    bx[0] = std::min(bx[0], r0);
+    bx[1] = std::max(bx[1], r1);
+    bx[2] = std::min(bx[2], c0);
+    bx[3] = std::max(bx[3], c1);
+  };
+  for (int i = 0; i < n; ++i) grow(Ls[i].lo[0], Ls[i].hi[0], Ls[i].lo[1], Ls[i].hi[1]);
+  const double pts_loops = static_cast<double>(bx[1] - bx[0]) * static_cast<double>(bx[3] - bx[2]);
+  for (const SwDs& D : pl.D)
+    if (D.oop) grow(D.v->lo[0], D.v->hi[0], D.v->lo[1], D.v->hi[1]);
+  const double pts = static_cast<double>(bx[1] - bx[0]) * static_cast<double>(bx[3] - bx[2]);
+  if (pts > 1.25 * pts_loops + 4096) return fail(why, "out-of-place allocation much larger than the loops");
+  for (int k = 0; k < 4; ++k) pl.box[k] = bx[k];
+  return true;
+}
+
+// Kernel source of an analysed group (structure only: ranges, pointers and
+// constants are parameters). Fills the constant table in tape order.
+std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* cst) {
+  // One thread per ring column (NT = 128); each thread evaluates K consecutive rows of
+  // every loop per step. Ring sizes are powers of two and every thread of the CTA works
+  // on the same rows, so ring slot offsets are CTA-uniform and every shared-memory
+  // access is [thread base + uniform slot + immediate]. Steps whose rows lie inside
+  // every loop range, store window and load box (all but a few at the ends of a
+  // segment) run a body without any row predicate.
+  std::ostringstream o;
+  const int nd = static_cast<int>(pl.D.size());
+  const int K = pl.K;
+  o << "#define SW_MAXL " << SW_MAXL << "\n#define SW_MAXD " << SW_MAXD << "\n#define SW_MAXC " << SW_MAXC << "\n";
+  o << kSweepDecl;
+  o << "extern \"C\" __global__ void __launch_bounds__(" << pl.NT << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p) {\n";
+  o << "  extern __shared__ __align__(16) double sw_sm[];\n";
+  o << "  const int lc = threadIdx.x;\n";
+  o << "  double* const B = sw_sm + lc;\n";
+  o << "  const long long c0 = p.C0 + static_cast<long long>(blockIdx.x) * " << pl.TC << ";\n";
+  o << "  const long long r_own0 = p.R0 + static_cast<long long>(blockIdx.y) * p.seg_rows;\n";
+  o << "  const long long r_own1 = min(p.R1, r_own0 + p.seg_rows);\n";
+  o << "  const long long rbase = r_own0 - " << pl.warm << ";\n";
+  o << "  const long long c = c0 - " << pl.HC << " + lc;\n";
+  o << "  const int nsteps = static_cast<int>((r_own1 - rbase + " << pl.lagS_max << " + " << K - 1 << ") / " << K << ");\n";
+  // fast steps: every row predicate true for all K rows
+  o << "  long long s_lo = 0, s_hi = nsteps;\n";
+  auto fast_rows = [&](long long q, const std::string& A, const std::string& Bs) {
+    o << "  s_lo = max(s_lo, -sw_floordiv(-((" << A << ") - rbase - (" << q << ")), " << K << "));\n";
+    o << "  s_hi = min(s_hi, sw_floordiv((" << Bs << ") - rbase - (" << q << ") - " << K << ", " << K << ") + 1);\n";
+  };
+  for (int i = 0; i < pl.n; ++i)
+    fast_rows(-pl.L[static_cast<std::size_t>(i)].lag, "p.rng[" + std::to_string(i) + "][0]",
+              "p.rng[" + std::to_string(i) + "][1]");
+  for (int d = 0; d < nd; ++d) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    const std::string ds = std::to_string(d);
+    if (D.loaded) fast_rows(static_cast<long long>(pl.P) * K - D.lagL, "p.box[" + ds + "][0]", "p.box[" + ds + "][1]");
+    if (D.store) {
+      fast_rows(-D.lagS, "max(r_own0, p.box[" + ds + "][0])", "min(r_own1, p.box[" + ds + "][1])");
+      if (!D.oop)
+        for (int j : D.writers)
+          fast_rows(-D.lagS, "p.rng[" + std::to_string(j) + "][0]", "p.rng[" + std::to_string(j) + "][1]");
+    }
+  }
+  // column predicates of every loop / store, once per thread, as bit masks
+  o << "  unsigned long long colmask = 0ull;\n  unsigned stmask = 0u, stfast = 0u;\n";
+  for (int i = 0; i < pl.n; ++i) {
+    const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+    o << "  if (lc >= " << pl.HC - S.h << " && lc < " << pl.HC + pl.TC + S.h << " && c >= p.rng[" << i
+      << "][2] && c < p.rng[" << i << "][3]) colmask |= 1ull << " << i << ";\n";
+  }
+  o << "  const bool own_col = lc >= " << pl.HC << " && lc < " << pl.HC + pl.TC << " && c < p.C1;\n";
+  for (int d = 0; d < nd; ++d) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    if (D.loaded)
+      o << "  const bool colok" << d << " = c >= p.box[" << d << "][2] && c < p.box[" << d << "][3];\n";
+    if (D.store) {
+      o << "  if (own_col && c >= p.box[" << d << "][2] && c < p.box[" << d << "][3]) {\n    stmask |= 1u << " << d
+        << ";\n";
+      if (D.oop) {
+        o << "    stfast |= 1u << " << d << ";\n";
+      } else {
+        o << "    if (false";
+        for (int j : D.writers) o << " || (c >= p.rng[" << j << "][2] && c < p.rng[" << j << "][3])";
+        o << ") stfast |= 1u << " << d << ";\n";
+      }
+      o << "  }\n";
+    }
+  }
+  o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
+  // element (dataset d, row u + q) of this thread's column; u, q relative to rbase
+  auto at = [&](int d, const std::string& u, long long q, long long oc) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    std::ostringstream e;
+    e << "B[" << D.off << " + (((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << kRC;
+    if (oc) e << " + (" << oc << ")";
+    e << "]";
+    return e.str();
+  };
+  auto loads = [&](const std::string& step, const char* ind, bool fast) {
+    for (int d = 0; d < nd; ++d) {
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (!D.loaded) continue;
+      o << ind << "{\n" << ind << "  const int ul = (" << step << ") * " << K << " - " << D.lagL << ";\n";
+      o << ind << "  const double* g = p.src[" << d << "] + (rbase + ul - p.box[" << d << "][0]) * p.s0[" << d
+        << "] + (c - p.box[" << d << "][2]);\n";
+      o << ind << "#pragma unroll\n" << ind << "  for (int r = 0; r < " << K << "; ++r) {\n";
+      if (fast) {
+        o << ind << "    const bool ok = colok" << d << ";\n";
+      } else {
+        o << ind << "    const long long row = rbase + ul + r;\n";
+        o << ind << "    const bool ok = colok" << d << " && row >= p.box[" << d << "][0] && row < p.box[" << d
+          << "][1];\n";
+      }
+      o << ind << "    sw_cp8(&" << at(d, "ul + r", 0, 0) << ", ok ? g + r * p.s0[" << d << "] : p.src[" << d
+        << "], ok);\n";
+      o << ind << "  }\n" << ind << "}\n";
+    }
+    o << ind << "asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
+  };
+  for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false);
+  int ci0 = 0;
+  auto body = [&](bool fast) {
+    const char* ind = "      ";
+    loads("s + " + std::to_string(pl.P), ind, fast);
+    o << ind << "const int u = s * " << K << ";\n";
+    int ci = ci0;
+    for (int i = 0; i < pl.n; ++i) {
+      const ooc_loop& L = Ls[i];
+      const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+      if (S.barrier) o << ind << "__syncthreads();\n";
+      const std::string is = std::to_string(i);
+      o << ind << "if (colmask & (1ull << " << i << ")) {  // loop " << i << " (lag " << S.lag << ", halo " << S.h << ")\n";
+      o << "#pragma unroll\n" << ind << "  for (int r = 0; r < " << K << "; ++r) {\n";
+      if (!fast) {
+        o << ind << "    const long long row = rbase + u + r - " << S.lag << ";\n";
+        o << ind << "    if (row >= p.rng[" << is << "][0] && row < p.rng[" << is << "][1]) {\n";
+      } else {
+        o << ind << "    {\n";
+      }
+      int dsof_arg[OOC_MAX_ARGS];
+      for (int a = 0; a < L.nargs; ++a) {
+        dsof_arg[a] = -1;
+        for (int d = 0; d < nd; ++d)
+          if (pl.D[static_cast<std::size_t>(d)].v->data == L.args[a].data) dsof_arg[a] = d;
+      }
+      const std::string ur = "u + r - " + std::to_string(S.lag);
+      int tmp = 0;
+      std::vector<std::string> outs;
+      const ooc_ins* t = L.tape;
+      for (int w = 0; w < L.nwrites; ++w) {
+        std::vector<std::string> st;
+        for (int k = 0; k < L.write_len[w]; ++k, ++t) {
+          const ooc_ins& in = *t;
+          if (in.op == OOC_OP_CONST) {
+            if (cst && !fast) cst->push_back(in.value);
+            st.push_back("p.cst[" + std::to_string(ci++) + "]");
+          } else if (in.op == OOC_OP_READ) {
+            const std::string name = "v" + is + "_" + std::to_string(tmp++);
+            o << ind << "      const double " << name << " = " << at(dsof_arg[in.arg], ur, in.offset[0], in.offset[1])
+              << ";\n";
+            st.push_back(name);
+          } else {
+            const std::string y = st.back();
+            st.pop_back();
+            const std::string x = st.back();
+            st.pop_back();
+            const std::string name = "v" + is + "_" + std::to_string(tmp++);
+            o << ind << "      const double " << name << " = ";
+            switch (in.op) {
+              case OOC_OP_ADD: o << x << " + " << y; break;
+              case OOC_OP_SUB: o << x << " - " << y; break;
+              case OOC_OP_MUL: o << x << " * " << y; break;
+              case OOC_OP_DIV: o << x << " / " << y; break;
+              case OOC_OP_MIN: o << "ooc_min(" << x << ", " << y << ")"; break;
+              default: o << "ooc_max(" << x << ", " << y << ")"; break;
+            }
+            o << ";\n";
+            st.push_back(name);
+          }
+        }
+        outs.push_back(st.back());
+      }
+      for (int w = 0; w < L.nwrites; ++w)
+        o << ind << "      " << at(S.wds[static_cast<std::size_t>(w)], ur, 0, 0) << " = "
+          << outs[static_cast<std::size_t>(w)] << ";\n";
+      o << ind << "    }\n" << ind << "  }\n" << ind << "}\n";
+    }
+    // stores of the final rows (each thread stores the elements it wrote: no barrier)
+    for (int d = 0; d < nd; ++d) {
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (!D.store) continue;
+      const std::string ds = std::to_string(d);
+      o << ind << "if (" << (fast ? "stfast" : "stmask") << " & (1u << " << ds << ")) {\n#pragma unroll\n" << ind
+        << "  for (int r = 0; r < " << K << "; ++r) {\n";
+      o << ind << "    const long long row = rbase + u + r - " << D.lagS << ";\n";
+      if (!fast) {
+        o << ind << "    if (row >= r_own0 && row < r_own1 && row >= p.box[" << ds << "][0] && row < p.box[" << ds
+          << "][1]";
+        if (!D.oop) {
+          o << " && (false";
+          for (int j : D.writers)
+            o << " || (row >= p.rng[" << j << "][0] && row < p.rng[" << j << "][1] && c >= p.rng[" << j
+              << "][2] && c < p.rng[" << j << "][3])";
+          o << ")";
+        }
+        o << ")\n";
+      }
+      o << ind << "      p.dst[" << ds << "][(row - p.box[" << ds << "][0]) * p.s0[" << ds << "] + (c - p.box[" << ds
+        << "][2])] = " << at(d, "u + r", -D.lagS, 0) << ";\n" << ind << "  }\n" << ind << "}\n";
+    }
+  };
+  o << "  for (int s = 0; s < nsteps; ++s) {\n";
+  o << "    asm volatile(\"cp.async.wait_group " << pl.P - 1 << ";\" ::: \"memory\");\n";
+  o << "    __syncthreads();\n";
+  o << "    if (s >= s_lo && s < s_hi) {\n";
+  body(true);
+  o << "    } else {\n";
+  body(false);
+  o << "    }\n  }\n  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n}\n";
+  return o.str();
+}
+
+struct SwKernel {
+  void* fn = nullptr;
+  int occ = 1;
+  bool ok = false;
+  std::string err;
+};
+std::unordered_map<std::string, SwKernel> g_sw_cache;
+std::mutex g_sw_mu;
+
+int sweep_K() {
+  static int k = [] {
+    const char* e = std::getenv("OOC_SWEEP_K");
+    const int v = e ? std::atoi(e) : 2;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
+  }();
+  return k;
+}
+int sweep_P() {
+  static int pp = [] {
+    const char* e = std::getenv("OOC_SWEEP_P");
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 1 && v <= 4 ? v : 2;
+  }();
+  return pp;
+}
+
+}  // namespace
+
+extern "C" int ooc_sweep_check(const ooc_loop* loops, int n, int* oop_args) {
+  OOC_ARG_CHECK(loops && n > 0, "ooc_sweep_check: bad args");
+  // same policy as the specialised kernels: off with OOC_JIT=0 (interpreter only), and
+  // only for launches of >= the JIT threshold unless specialisation is forced
+  long long min_pts = 0;
+  const int m = jit_policy(&min_pts);
+  if (m == 0) return 0;
+  if (m == 1 && static_cast<long long>(loops[0].hi[0] - loops[0].lo[0]) * (loops[0].hi[1] - loops[0].lo[1]) < min_pts)
+    return 0;
+  SwPlan pl;
+  std::string why;
+  const bool ok = analyze(loops, n, sweep_K(), sweep_P(), pl, &why);
+  static const bool dbg = std::getenv("OOC_SWEEP_DEBUG") != nullptr;
+  if (dbg && !ok && n > 1) std::fprintf(stderr, "sweep: %d loops rejected: %s\n", n, why.c_str());
+  if (!ok) return 0;
+  if (oop_args)
+    for (int i = 0; i < n; ++i)
+      for (int a = 0; a < OOC_MAX_ARGS; ++a) {
+        int f = 0;
+        if (a < loops[i].nargs)
+          for (const SwDs& D : pl.D)
+            if (D.v->data == loops[i].args[a].data)
+              f = (D.oop ? 1 : 0) | (D.loaded ? 2 : 0) | (D.written ? 4 : 0);
+        oop_args[i * OOC_MAX_ARGS + a] = f;
+      }
+  return 1;
+}
+
+extern "C" int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int len, int compile) {
+  OOC_ARG_CHECK(loops && n > 0, "ooc_sweep_describe: bad args");
+  SwPlan pl;
+  std::string why;
+  if (!analyze(loops, n, sweep_K(), sweep_P(), pl, &why)) {
+    if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", why.c_str());
+    return OOC_ERR_UNSUPPORTED;
+  }
+  std::ostringstream o;
+  o << "{\"loops\":" << n << ",\"K\":" << pl.K << ",\"P\":" << pl.P << ",\"HC\":" << pl.HC << ",\"TC\":" << pl.TC
+    << ",\"warm\":" << pl.warm << ",\"smem\":" << pl.smem << ",\"lags\":[";
+  for (int i = 0; i < n; ++i) o << (i ? "," : "") << pl.L[static_cast<std::size_t>(i)].lag;
+  o << "],\"halos\":[";
+  for (int i = 0; i < n; ++i) o << (i ? "," : "") << pl.L[static_cast<std::size_t>(i)].h;
+  o << "],\"barriers\":[";
+  for (int i = 0; i < n; ++i) o << (i ? "," : "") << (pl.L[static_cast<std::size_t>(i)].barrier ? 1 : 0);
+  o << "],\"datasets\":[";
+  for (std::size_t d = 0; d < pl.D.size(); ++d) {
+    const SwDs& D = pl.D[d];
+    o << (d ? "," : "") << "{\"loaded\":" << D.loaded << ",\"written\":" << D.written << ",\"oop\":" << D.oop
+      << ",\"lagL\":" << D.lagL << ",\"lagS\":" << D.lagS << ",\"W\":" << D.W << "}";
+  }
+  o << "]}";
+  std::string out = o.str();
+  if (compile) {
+    const std::string src = generate(loops, pl, nullptr);
+    std::string err;
+    if (!jit_build_kernel(src, "ooc_sweep_kernel", pl.NT, pl.smem, nullptr, nullptr, err, /*load=*/false)) {
+      if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", err.c_str());
+      return OOC_ERR_UNSUPPORTED;
+    }
+    if (const char* f = std::getenv("OOC_SWEEP_DUMP")) {  // generated source + ptxas report
+      if (FILE* fp = std::fopen(f, "w")) {
+        std::fprintf(fp, "%s\n/* %s */\n", src.c_str(), err.c_str());
+        std::fclose(fp);
+      }
+    }
+  }
+  if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", out.c_str());
+  return OOC_OK;
+}
+
+extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n, const ooc_redirect* red,
+                                int nred) {
+  OOC_ARG_CHECK(c && loops && n > 0 && q >= 0 && q < OOC_NUM_QUEUES, "ooc_launch_sweep: bad args");
+  std::vector<const double*> dead;
+  for (int r = 0; r < nred; ++r)
+    if (!red[r].dst) dead.push_back(red[r].src);
+  SwPlan pl;
+  std::string why;
+  if (!analyze(loops, n, sweep_K(), sweep_P(), pl, &why, &dead)) {
+    set_error("ooc_launch_sweep: group not sweepable: " + why);
+    return OOC_ERR_UNSUPPORTED;
+  }
+  auto* sp = new SweepParams;
+  std::memset(sp, 0, sizeof *sp);
+  std::vector<double> cst;
+  const std::string src = generate(loops, pl, &cst);
+  for (std::size_t k = 0; k < cst.size(); ++k) sp->cst[k] = cst[k];
+  sp->R0 = pl.box[0];
+  sp->R1 = pl.box[1];
+  sp->C0 = pl.box[2];
+  sp->C1 = pl.box[3];
+  for (int i = 0; i < n; ++i) {
+    sp->rng[i][0] = loops[i].lo[0];
+    sp->rng[i][1] = loops[i].hi[0];
+    sp->rng[i][2] = loops[i].lo[1];
+    sp->rng[i][3] = loops[i].hi[1];
+  }
+  for (std::size_t d = 0; d < pl.D.size(); ++d) {
+    const SwDs& D = pl.D[d];
+    sp->src[d] = D.v->data;
+    sp->dst[d] = D.v->data;
+    sp->s0[d] = D.v->stride[0];
+    sp->box[d][0] = D.v->lo[0];
+    sp->box[d][1] = D.v->hi[0];
+    sp->box[d][2] = D.v->lo[1];
+    sp->box[d][3] = D.v->hi[1];
+    if (D.oop && D.store) {
+      double* to = nullptr;
+      for (int r = 0; r < nred; ++r)
+        if (red[r].src == D.v->data) to = red[r].dst;
+      if (!to) {
+        delete sp;
+        set_error("ooc_launch_sweep: no out-of-place destination for a dataset the group loads and writes");
+        return OOC_ERR_ARG;
+      }
+      sp->dst[d] = to;
+    }
+  }
+  SwKernel* k = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_sw_mu);
+    SwKernel& e = g_sw_cache[src];
+    if (!e.ok && e.err.empty()) {
+      const auto t0 = std::chrono::steady_clock::now();
+      e.ok = jit_build_kernel(src, "ooc_sweep_kernel", pl.NT, pl.smem, &e.fn, &e.occ, e.err, true);
+      c->stats.jit_compiles++;
+      c->stats.jit_compile_ms += std::chrono::duration_cast<std::chrono::milliseconds>(
+                                     std::chrono::steady_clock::now() - t0).count();
+      if (!e.ok && e.err.empty()) e.err = "build failed";
+    }
+    k = &e;
+  }
+  if (!k->ok) {
+    delete sp;
+    set_error("ooc_launch_sweep: " + k->err);
+    return OOC_ERR_UNSUPPORTED;
+  }
+  const long long rows = pl.box[1] - pl.box[0];
+  const long long strips = (pl.box[3] - pl.box[2] + pl.TC - 1) / pl.TC;
+  const long long want = static_cast<long long>(c->prop.multiProcessorCount) * k->occ * 4;
+  long long nseg = std::max<long long>(1, (want + strips - 1) / strips);
+  const long long min_seg = std::max<long long>(64, 8 * (pl.warm + pl.lagS_max + pl.K));
+  nseg = std::max<long long>(1, std::min(nseg, rows / min_seg));
+  sp->seg_rows = (rows + nseg - 1) / nseg;
+  nseg = (rows + sp->seg_rows - 1) / sp->seg_rows;
+  c->stats.sweep_launches++;
+  void* args[] = {sp};
+  const int rc = jit_launch_kernel(c, q, k->fn, static_cast<unsigned>(strips), static_cast<unsigned>(nseg),
+                                   static_cast<unsigned>(pl.NT), static_cast<unsigned>(pl.smem), args);
+  delete sp;
+  return rc;
+}

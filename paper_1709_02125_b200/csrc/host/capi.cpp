@@ -459,6 +459,7 @@ const char* ooc_rt_device_json(ooc_runtime* h) {
     w.key("jit_compile_ms").value(st.jit_compile_ms);
     w.key("jit_host_us").value(st.jit_host_us);
     w.key("graph_launches").value(st.graph_launches);
+    w.key("sweep_launches").value(st.sweep_launches);
     w.key("mem_in_use").value(in_use);
     w.key("mem_peak").value(peak);
     w.key("build").value(std::string(ooc_dev_build_info()));
@@ -487,6 +488,47 @@ const char* ooc_rt_chain_plan_json(ooc_runtime* h, int chain, int tiles, int64_t
       s = dump ? ooc::plan_dump_json(m, c, ch.plan, ch.footprints)
                : ooc::plan_full_json(m, ch.plan, ch.footprints);
     }
+  });
+  return rc ? err_json() : out_str(s);
+}
+
+const char* ooc_rt_chain_sweep_check(ooc_runtime* h, int chain, int compile) {
+  std::string s;
+  int rc = guard([&] {
+    const ooc::LoopChain& c = h->rt->chain_log().at(static_cast<std::size_t>(chain));
+    const ooc::Mesh& m = h->rt->mesh();
+    std::vector<ooc_view> views(m.datasets.size());
+    for (std::size_t d = 0; d < m.datasets.size(); ++d) {
+      const ooc::Extent a = m.datasets[d].alloc();
+      ooc::BoxLayout L = ooc::padded_layout(a);
+      views[d] = ooc::view_at(reinterpret_cast<double*>((d + 1) << 32), a, L.stride);
+    }
+    std::vector<ooc::LoweredLoop> low;
+    for (const auto& l : c.loops) low.push_back(ooc::lower_loop(l));
+    std::vector<ooc_loop> calls;
+    for (std::size_t j = 0; j < c.loops.size(); ++j) {
+      std::vector<ooc_view> v;
+      for (const auto& a : c.loops[j].args) v.push_back(views[static_cast<std::size_t>(a.dataset)]);
+      calls.push_back(ooc::make_call(low[j], c.loops[j].range, v, 0));
+    }
+    ooc::JsonWriter w;
+    w.begin_array();
+    for (const ooc::SweepRun& run : ooc::plan_sweeps(m, c.loops, calls)) {
+      const std::size_t a = run.a, b = run.b;
+      std::vector<ooc_redirect> dead;
+      for (ooc::DatasetId d : run.dead) dead.push_back({views[static_cast<std::size_t>(d)].data, nullptr});
+      std::vector<char> log(1 << 20);
+      int r = ooc_sweep_describe(calls.data() + a, static_cast<int>(b - a), log.data(), static_cast<int>(log.size()),
+                                 compile);
+      w.begin_object().key("first").value(static_cast<long long>(a)).key("loops").value(static_cast<long long>(b - a));
+      w.key("ok").value(r == OOC_OK).key("plan").value(std::string(log.data()));
+      w.key("dead").begin_array();
+      for (ooc::DatasetId d : run.dead) w.value(static_cast<long long>(d));
+      w.end_array();
+      w.end_object();
+    }
+    w.end_array();
+    s = w.str();
   });
   return rc ? err_json() : out_str(s);
 }

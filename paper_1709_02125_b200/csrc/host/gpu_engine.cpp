@@ -349,40 +349,41 @@ bool GpuEngine::fusable(const ParLoop& b) const {
   return can_fuse(group_.loops, group_.tape_len, b, opts_.fuse);
 }
 
-void GpuEngine::flush_group(int queue) {
-  if (group_.calls.empty()) return;
+void GpuEngine::issue_instrumented(int queue, const std::vector<const ParLoop*>& loops,
+                                   const std::vector<index_t>& bytes, const std::function<void()>& issue) {
   if (opts_.timeline) {
-    std::vector<std::pair<int, index_t>> loops;
+    std::vector<std::pair<int, index_t>> ls;
     index_t total = 0;
-    for (std::size_t i = 0; i < group_.loops.size(); ++i) {
-      loops.push_back({group_.loops[i]->id, group_.bytes[i]});
-      total += group_.bytes[i];
+    for (std::size_t i = 0; i < loops.size(); ++i) {
+      ls.push_back({loops[i]->id, bytes[i]});
+      total += bytes[i];
     }
-    timeline_cmd(3, queue, total, -1, cur_tile_, std::move(loops), [&] {
-      DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
-    });
+    timeline_cmd(3, queue, total, -1, cur_tile_, std::move(ls), issue);
   } else if (opts_.profile_loops) {
     PendingLoop pl{{}, 0, fresh_timing_event(), fresh_timing_event()};
     double total = 0;
-    for (index_t b : group_.bytes) total += static_cast<double>(b);
-    for (std::size_t i = 0; i < group_.loops.size(); ++i)
-      pl.weights.push_back({group_.loops[i]->id, total > 0 ? group_.bytes[i] / total : 1.0});
+    for (index_t b : bytes) total += static_cast<double>(b);
+    for (std::size_t i = 0; i < loops.size(); ++i)
+      pl.weights.push_back({loops[i]->id, total > 0 ? bytes[i] / total : 1.0});
     pl.bytes = static_cast<index_t>(total);
     DEV(ooc_event_record(ctx_, pl.a, queue));
-    DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
+    issue();
     DEV(ooc_event_record(ctx_, pl.b, queue));
     pending_loops_.push_back(std::move(pl));
   } else {
-    DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
+    issue();
   }
+}
+
+void GpuEngine::flush_group(int queue) {
+  if (group_.calls.empty()) return;
+  issue_instrumented(queue, group_.loops, group_.bytes, [&] {
+    DEV(ooc_launch_group(ctx_, queue, group_.calls.data(), static_cast<int>(group_.calls.size())));
+  });
   group_ = Group{};
 }
 
-void GpuEngine::launch(int queue, bool group_start, int tile, const ParLoop& loop,
-                       const LoweredLoop& lw, const Extent& sub,
-                       const std::vector<ooc_view>& views, int red_slot) {
-  if (group_start || !fusable(loop)) flush_group(queue);
-  cur_tile_ = tile;
+ooc_loop make_call(const LoweredLoop& lw, const Extent& sub, const std::vector<ooc_view>& views, int red_slot) {
   ooc_loop L{};
   L.ndim = sub.ndim;
   for (int d = 0; d < 3; ++d) {
@@ -401,7 +402,124 @@ void GpuEngine::launch(int queue, bool group_start, int tile, const ParLoop& loo
   L.reduce_slot = red_slot;
   L.ntape = static_cast<int32_t>(lw.tape.size());
   L.tape = lw.tape.data();
-  group_.calls.push_back(L);
+  return L;
+}
+
+namespace {
+// Dead after [a, b): the first access of d after the run is a write (not a read) whose
+// range covers every point the run writes.
+bool dead_after(const std::vector<ParLoop>& loops, std::size_t a, std::size_t b, DatasetId d) {
+  Extent u;
+  bool any = false;
+  for (std::size_t k = a; k < b; ++k)
+    for (const LoopArg& x : loops[k].args)
+      if (x.dataset == d && access_writes(x.mode)) {
+        const Extent& r = loops[k].range;
+        if (!any) {
+          u = r;
+        } else {
+          for (int q = 0; q < 3; ++q) {
+            u.lo[q] = std::min(u.lo[q], r.lo[q]);
+            u.hi[q] = std::max(u.hi[q], r.hi[q]);
+          }
+        }
+        any = true;
+      }
+  if (!any) return false;
+  for (std::size_t k = b; k < loops.size(); ++k) {
+    bool rd = false, wr = false;
+    for (const LoopArg& x : loops[k].args)
+      if (x.dataset == d) {
+        rd = rd || access_reads(x.mode);
+        wr = wr || access_writes(x.mode);
+      }
+    if (rd) return false;
+    if (wr) return loops[k].range.contains(u);
+  }
+  return false;  // live at the end of the chain
+}
+}  // namespace
+
+std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& loops,
+                                  const std::vector<ooc_loop>& calls) {
+  // Least-traffic partition (dynamic programming) of the chain into sweep runs and
+  // single loops left to the other kernels. A run costs one read of every dataset it
+  // loads plus one write of every dataset it writes that is still live after it; a
+  // launch costs ~4 us of HBM time.
+  const std::size_t L = calls.size();
+  constexpr double kLaunchBytes = 24e6;
+  auto bytes_of = [&](DatasetId d) { return static_cast<double>(mesh[d].alloc().size()) * mesh[d].elem_bytes; };
+  std::vector<std::vector<std::pair<std::size_t, double>>> runs(L);  // i -> (j, cost)
+  std::vector<int> flags;
+  for (std::size_t i = 0; i < L; ++i)
+    for (std::size_t j = i + 2; j <= L; ++j) {
+      flags.assign((j - i) * OOC_MAX_ARGS, 0);
+      if (ooc_sweep_check(&calls[i], static_cast<int>(j - i), flags.data()) != 1) {
+        if (j > i + 2 || ooc_sweep_check(&calls[i], 1, nullptr) != 1) break;
+        continue;
+      }
+      std::map<DatasetId, int> f;
+      for (std::size_t k = i; k < j; ++k)
+        for (std::size_t x = 0; x < loops[k].args.size(); ++x)
+          f[loops[k].args[x].dataset] |= flags[(k - i) * OOC_MAX_ARGS + x];
+      double c = kLaunchBytes;
+      for (const auto& [d, fl] : f) {
+        if (fl & 2) c += bytes_of(d);
+        if ((fl & 4) && !dead_after(loops, i, j, d)) c += bytes_of(d);
+      }
+      runs[i].push_back({j, c});
+    }
+  std::vector<double> best(L + 1, 1e300);
+  std::vector<std::size_t> from(L + 1, 0);
+  best[0] = 0;
+  for (std::size_t i = 0; i < L; ++i) {
+    if (best[i] >= 1e299) continue;
+    double single = kLaunchBytes;  // the loop launched on its own
+    for (const LoopArg& x : loops[i].args)
+      single += bytes_of(x.dataset) * (x.mode == AccessMode::read_write ? 2 : 1);
+    if (best[i] + single < best[i + 1]) {
+      best[i + 1] = best[i] + single;
+      from[i + 1] = i;
+    }
+    for (const auto& [j, c] : runs[i])
+      if (best[i] + c < best[j]) {
+        best[j] = best[i] + c;
+        from[j] = i;
+      }
+  }
+  std::vector<SweepRun> out;
+  for (std::size_t j = L; j > 0; j = from[j]) {
+    const std::size_t i = from[j];
+    if (j - i >= 2) {
+      SweepRun r{i, j, {}};
+      std::vector<DatasetId> seen;
+      for (std::size_t k = i; k < j; ++k)
+        for (const LoopArg& x : loops[k].args)
+          if (access_writes(x.mode) && std::find(seen.begin(), seen.end(), x.dataset) == seen.end()) {
+            seen.push_back(x.dataset);
+            if (dead_after(loops, i, j, x.dataset)) r.dead.push_back(x.dataset);
+          }
+      out.push_back(r);
+    }
+  }
+  std::reverse(out.begin(), out.end());
+  return out;
+}
+
+bool sweep_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("OOC_SWEEP");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
+}
+
+void GpuEngine::launch(int queue, bool group_start, int tile, const ParLoop& loop,
+                       const LoweredLoop& lw, const Extent& sub,
+                       const std::vector<ooc_view>& views, int red_slot) {
+  if (group_start || !fusable(loop)) flush_group(queue);
+  cur_tile_ = tile;
+  group_.calls.push_back(make_call(lw, sub, views, red_slot));
   group_.loops.push_back(&loop);
   group_.bytes.push_back(sub.size() * loop_bytes_per_point_views(loop));
   group_.tape_len += lw.tape.size();
@@ -814,6 +932,7 @@ void GpuEngine::ensure_resident(Mesh& mesh, DatasetId d) {
   if (r.dev && r.host_ptr != ds.host.data()) {  // mesh replaced underneath us
     DEV(ooc_ctx_sync(ctx_));
     DEV(ooc_mem_free(ctx_, r.dev));
+    if (r.shadow) DEV(ooc_mem_free(ctx_, r.shadow));
     r = Resident{};
   }
   if (!r.dev) {
@@ -934,6 +1053,10 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
   if (ge && ge->g[par]) {
     DEV(ooc_graph_launch(ctx_, OOC_Q_COMPUTE, ge->g[par]));
     mark_written();
+    for (DatasetId d : ge->flips) {  // the buffers the captured sweeps swapped
+      Resident& r = res_[static_cast<std::size_t>(d)];
+      std::swap(r.dev, r.shadow);
+    }
     for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
     finish_chain(chain, out.reduction_slot, pc);
     return;
@@ -960,38 +1083,72 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
     if (l.has_reduction())
       DEV(ooc_reduce_reset(ctx_, OOC_Q_COMPUTE, out.reduction_slot.at(l.id), lower_loop(l).reduce_op));
   std::vector<LoweredLoop> lowered_store(chain.loops.size());
-  std::vector<const LoweredLoop*> lowered(chain.loops.size());
-  std::vector<std::vector<ooc_view>> views(chain.loops.size());
   for (std::size_t j = 0; j < chain.loops.size(); ++j) {
-    const ParLoop& l = chain.loops[j];
-    lowered_store[j] = lower_loop(l);
-    lowered[j] = &lowered_store[j];
-    for (const LoopArg& a : l.args) {
-      const Resident& r = res_[static_cast<std::size_t>(a.dataset)];
-      views[j].push_back(view_at(r.dev, mesh[a.dataset].alloc(), r.layout.stride));
+    lowered_store[j] = lower_loop(chain.loops[j]);
+    for (const LoopArg& a : chain.loops[j].args)
       if (access_writes(a.mode)) {
         mesh[a.dataset].ever_written = true;
         res_[static_cast<std::size_t>(a.dataset)].host_outdated = true;
       }
-    }
   }
+  // views are taken at launch time: a sweep launch swaps the buffers of the datasets it
+  // rewrites out of place
+  auto views_of = [&](const ParLoop& l) {
+    std::vector<ooc_view> v;
+    for (const LoopArg& a : l.args) {
+      const Resident& r = res_[static_cast<std::size_t>(a.dataset)];
+      v.push_back(view_at(r.dev, mesh[a.dataset].alloc(), r.layout.stride));
+    }
+    return v;
+  };
   std::vector<std::size_t> tape_len(chain.loops.size());
   for (std::size_t j = 0; j < chain.loops.size(); ++j) tape_len[j] = lowered_store[j].tape.size();
   const std::vector<char> starts = plan_fusion(mesh, chain.loops, tape_len, opts_.fuse);
   const int T = plan ? plan->tile_count : 1;
+  // untiled chains: runs of loops the row-sweep kernel accepts stream through shared
+  // memory in one launch each (csrc/device/sweep.cu)
+  static std::map<std::string, std::vector<SweepRun>> sweep_cache;  // per chain structure
+  const std::vector<SweepRun>* sweeps = nullptr;
+  static const std::vector<SweepRun> no_sweeps;
+  if (T == 1 && opts_.fuse && sweep_enabled()) {
+    const std::string key = sweep_key(mesh, chain);
+    auto it = sweep_cache.find(key);
+    if (it == sweep_cache.end()) {
+      std::vector<ooc_loop> calls;
+      for (std::size_t j = 0; j < chain.loops.size(); ++j)
+        calls.push_back(make_call(lowered_store[j], chain.loops[j].range, views_of(chain.loops[j]), 0));
+      it = sweep_cache.emplace(key, plan_sweeps(mesh, chain.loops, calls)).first;
+    }
+    sweeps = &it->second;
+  } else {
+    sweeps = &no_sweeps;
+  }
+  std::vector<DatasetId> flipped;
+  std::size_t next_sweep = 0;
   for (int t = 0; t < T; ++t)
     for (std::size_t j = 0; j < chain.loops.size(); ++j) {
+      if (next_sweep < sweeps->size() && (*sweeps)[next_sweep].a == j) {
+        const SweepRun& run = (*sweeps)[next_sweep];
+        const std::size_t b = run.b;
+        ++next_sweep;
+        flush_group(OOC_Q_COMPUTE);
+        run_sweep(mesh, chain, run, lowered_store, flipped);
+        j = b - 1;
+        continue;
+      }
       const ParLoop& l = chain.loops[j];
       const Extent sub = plan ? plan->subrange(static_cast<int>(j), t) : l.range;
       if (sub.empty()) continue;
       auto rs = out.reduction_slot.find(l.id);
-      launch(OOC_Q_COMPUTE, starts[j] != 0, t, l, *lowered[j], sub, views[j],
+      const bool after_sweep = next_sweep > 0 && (*sweeps)[next_sweep - 1].b == j;
+      launch(OOC_Q_COMPUTE, starts[j] != 0 || after_sweep, t, l, lowered_store[j], sub, views_of(l),
              rs == out.reduction_slot.end() ? 0 : rs->second);
     }
   flush_group(OOC_Q_COMPUTE);
   if (capture) {
     ooc_jit_freeze(0);
     DEV(ooc_graph_end(ctx_, OOC_Q_COMPUTE, -1, &ge->g[par]));
+    ge->flips = flipped;
     DEV(ooc_graph_launch(ctx_, OOC_Q_COMPUTE, ge->g[par]));
   } else if (ge) {
     ooc_dev_stats st{};
@@ -1022,6 +1179,95 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
   }
   for (const ParLoop& l : chain.loops) pc.t.metric_bytes += l.range.size() * loop_bytes_per_point(mesh, l);
   finish_chain(chain, out.reduction_slot, pc);
+}
+
+std::string sweep_key(const Mesh& mesh, const LoopChain& chain) {
+  // everything the sweep partition depends on: ranges, datasets (+ allocations),
+  // access modes, tape structure (opcodes, arguments, offsets; not constant values)
+  std::string k;
+  auto put_i = [&](long long v) { k.append(reinterpret_cast<const char*>(&v), sizeof v); };
+  for (const ParLoop& l : chain.loops) {
+    put_i(l.range.ndim);
+    for (int d = 0; d < 3; ++d) {
+      put_i(l.range.lo[d]);
+      put_i(l.range.hi[d]);
+    }
+    put_i(l.has_reduction() ? 1 : 0);
+    for (const LoopArg& a : l.args) {
+      put_i(a.dataset);
+      put_i(static_cast<long long>(a.mode));
+      const Extent al = mesh[a.dataset].alloc();
+      for (int d = 0; d < 3; ++d) {
+        put_i(al.lo[d]);
+        put_i(al.hi[d]);
+      }
+    }
+    const LoweredLoop lw = lower_loop(l);
+    for (const ooc_ins& in : lw.tape) {
+      put_i(in.op);
+      put_i(in.arg);
+      for (int d = 0; d < 3; ++d) put_i(in.offset[d]);
+    }
+    for (int w : lw.write_len) put_i(w);
+  }
+  return k;
+}
+
+void GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run,
+                          const std::vector<LoweredLoop>& lowered, std::vector<DatasetId>& flipped) {
+  std::vector<ooc_loop> calls;
+  std::vector<const ParLoop*> loops;
+  std::vector<index_t> bytes;
+  for (std::size_t j = run.a; j < run.b; ++j) {
+    const ParLoop& l = chain.loops[j];
+    std::vector<ooc_view> v;
+    for (const LoopArg& x : l.args) {
+      const Resident& r = res_[static_cast<std::size_t>(x.dataset)];
+      v.push_back(view_at(r.dev, mesh[x.dataset].alloc(), r.layout.stride));
+    }
+    calls.push_back(make_call(lowered[j], l.range, v, 0));
+    loops.push_back(&l);
+    bytes.push_back(l.range.size() * loop_bytes_per_point_views(l));
+  }
+  std::vector<int> flags(calls.size() * OOC_MAX_ARGS, 0);
+  if (ooc_sweep_check(calls.data(), static_cast<int>(calls.size()), flags.data()) != 1)
+    throw DeviceError(OOC_ERR_UNSUPPORTED, "sweep group no longer sweepable");
+  std::vector<DatasetId> outs;  // live out-of-place outputs: written to the shadow, then swapped
+  for (std::size_t i = 0; i < calls.size(); ++i)
+    for (std::size_t x = 0; x < loops[i]->args.size(); ++x) {
+      const DatasetId d = loops[i]->args[x].dataset;
+      if ((flags[i * OOC_MAX_ARGS + x] & 1) && std::find(outs.begin(), outs.end(), d) == outs.end() &&
+          std::find(run.dead.begin(), run.dead.end(), d) == run.dead.end())
+        outs.push_back(d);
+    }
+  std::vector<ooc_redirect> red;
+  for (DatasetId d : run.dead) red.push_back({res_[static_cast<std::size_t>(d)].dev, nullptr});
+  for (DatasetId d : outs) {
+    Resident& r = res_[static_cast<std::size_t>(d)];
+    if (!r.shadow) {
+      void* p = nullptr;
+      int rc = ooc_mem_alloc(ctx_, static_cast<std::size_t>(r.layout.elems) * sizeof(double), &p);
+      if (rc == OOC_ERR_CAPACITY) {
+        long long in_use = 0;
+        ooc_mem_usage(ctx_, &in_use, nullptr);
+        throw CapacityError(in_use + r.layout.elems * 8, props_.hbm_bytes);
+      }
+      DEV(rc);
+      r.shadow = static_cast<double*>(p);
+    }
+    red.push_back({r.dev, r.shadow});
+  }
+  issue_instrumented(OOC_Q_COMPUTE, loops, bytes, [&] {
+    DEV(ooc_launch_sweep(ctx_, OOC_Q_COMPUTE, calls.data(), static_cast<int>(calls.size()), red.data(),
+                         static_cast<int>(red.size())));
+  });
+  for (DatasetId d : outs) {
+    Resident& r = res_[static_cast<std::size_t>(d)];
+    std::swap(r.dev, r.shadow);
+    auto it = std::find(flipped.begin(), flipped.end(), d);
+    if (it == flipped.end()) flipped.push_back(d);
+    else flipped.erase(it);
+  }
 }
 
 std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan) const {

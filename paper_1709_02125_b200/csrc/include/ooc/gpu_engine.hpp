@@ -51,6 +51,19 @@ struct BoxLayout {
 BoxLayout padded_layout(const Extent& box, index_t pad_elems = 16);
 ooc_view view_at(double* data, const Extent& box, const Point& stride);
 ooc_view host_view(Dataset& ds);
+ooc_loop make_call(const LoweredLoop& lw, const Extent& sub, const std::vector<ooc_view>& views, int red_slot);
+/// A run of consecutive loops [a, b) executed by one row-sweep launch; `dead` = the
+/// datasets it writes whose values are overwritten before anyone reads them.
+struct SweepRun {
+  std::size_t a = 0, b = 0;
+  std::vector<DatasetId> dead;
+};
+/// Row-sweep partition of an untiled chain: the least-traffic split into sweep runs
+/// (>= 2 loops each, accepted by ooc_sweep_check) and loops left to the other kernels.
+std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& loops,
+                                  const std::vector<ooc_loop>& calls);
+std::string sweep_key(const Mesh& mesh, const LoopChain& chain);
+bool sweep_enabled();  // OOC_SWEEP=0 disables
 
 class GpuEngine {
  public:
@@ -104,6 +117,7 @@ class GpuEngine {
  private:
   struct Resident {
     double* dev = nullptr;
+    double* shadow = nullptr;  // second buffer for out-of-place sweep outputs (swapped with dev)
     BoxLayout layout;
     bool dev_valid = false;
     bool host_outdated = false;
@@ -136,6 +150,10 @@ class GpuEngine {
               const std::vector<ooc_view>& views, int red_slot);
   bool fusable(const ParLoop& b) const;
   void flush_group(int queue);
+  void issue_instrumented(int queue, const std::vector<const ParLoop*>& loops, const std::vector<index_t>& bytes,
+                          const std::function<void()>& issue);
+  void run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run, const std::vector<LoweredLoop>& lowered,
+                 std::vector<DatasetId>& flipped);
   index_t loop_bytes_per_point_views(const ParLoop& loop) const;
   void ensure_pool(index_t elems);
   void ensure_resident(Mesh& mesh, DatasetId d);
@@ -190,6 +208,7 @@ class GpuEngine {
     bool settled = false;  // the last direct run made no tuning launch
     ooc_graph* g[2] = {nullptr, nullptr};
     std::vector<int> slots[2];
+    std::vector<DatasetId> flips;  // datasets whose buffers the chain's sweeps swap (odd count)
   };
   std::map<std::string, GraphEntry> graphs_;
   int next_graph_slot_ = OOC_REDUCE_SLOTS / 2;

@@ -1,0 +1,61 @@
+"""Row-sweep planning on CPU (no GPU): which runs of a chain the sweep kernel takes,
+their schedules (lags, halos, rings, out-of-place outputs), and that every generated
+kernel compiles for sm_100a with NVRTC."""
+import pytest
+
+import paper_1709_02125_b200 as B
+from oracle import programs as P
+
+
+@pytest.fixture
+def jit_always():
+    B.set_jit(2, 0)
+    yield
+    B.set_jit(1, 1 << 18)
+
+
+def _chains(prog):
+    rt = B.load_program(B.Runtime("plan_only", record=True, tiles=1), prog)
+    return rt, range(rt.num_chains())
+
+
+def test_miniflow2d_timesteps_fuse_into_sweeps(jit_always):
+    rt, chains = _chains(P.app_program("miniflow2d", 64, 64, iters=10))
+    groups = [g for c in chains for g in rt.chain_sweep_check(c, compile=True)]
+    assert groups and all(g["ok"] for g in groups)
+    covered = sum(g["loops"] for g in groups)
+    assert covered == 140  # 10 iterations x 14 loops: every loop except the fieldsum
+    assert max(g["loops"] for g in groups) >= 28  # at least two whole timesteps per launch
+    for g in groups:
+        pl = g["plan"]
+        assert pl["smem"] <= 110 * 1024 and pl["TC"] + 2 * pl["HC"] == 128
+        assert min(pl["lags"]) >= 0 and pl["warm"] >= 0
+        for d in pl["datasets"]:
+            assert d["oop"] == (d["loaded"] and d["written"])
+            assert d["W"] >= pl["K"]
+    # runs end on timestep boundaries; the temporaries a later run rewrites before
+    # reading are not stored (dead), only the chain's last run stores them
+    c1 = rt.chain_sweep_check(max(chains), compile=False)
+    assert all(g["loops"] % 14 == 0 for g in c1)
+    assert all(len(g["dead"]) == 6 for g in c1[:-1]) and c1[-1]["dead"] == []
+    first = groups[0]["plan"]["datasets"]
+    # rho, e, v are read and rewritten: out of place; temporaries are written first
+    assert sum(d["oop"] for d in first) == 3
+
+
+def test_reductions_and_3d_are_not_swept(jit_always):
+    rt, chains = _chains(P.app_program("miniflow3d", 12, 10, 8, iters=3))
+    for c in chains:
+        assert rt.chain_sweep_check(c, compile=False) == []
+
+
+def test_random_2d_chains_compile(jit_always):
+    n = 0
+    for seed in range(60):
+        prog = P.random_program(seed, flushes=True, allow_3d=False)
+        rt, chains = _chains(prog)
+        for c in chains:
+            for g in rt.chain_sweep_check(c, compile=True):
+                assert g["ok"], (seed, g)
+                n += 1
+    assert n > 5
