@@ -136,6 +136,15 @@ def measure_link(gpu, nbytes=1 << 30, reps=4):
     return out
 
 
+def _nloops(group):
+    """Loops in a launch label "La-Lb" (specialised kernels hold <= 8, sweeps more)."""
+    try:
+        a, b = group.split("-")
+        return int(b[1:]) - int(a[1:]) + 1
+    except ValueError:
+        return 1
+
+
 def profiled_traffic(group):
     """DRAM bytes per launch of `group` from the committed ncu launch list
     (profiles/*_traffic.json, produced from the same bench command)."""
@@ -375,7 +384,9 @@ def main():
                              "kernel (proj/src/metrics.cpp:10-12); traffic/dram_* are the DRAM bytes the "
                              "fused kernel really moves (ncu)",
                      "peak_source": peak_kind,
-                     "kernel": f"ooc_jit_kernel [{dom}] (fused sm_100a par_loop kernel)",
+                     "kernel": (f"ooc_sweep_kernel [{dom}] (row-sweep: the loops stream through "
+                                "shared-memory rings in one sm_100a launch)" if _nloops(dom) > 8 else
+                                f"ooc_jit_kernel [{dom}] (fused sm_100a par_loop kernel)"),
                      "kernel_share_of_step": kinds[dom]["seconds"] / total_k if dom else None,
                      "bytes_per_launch": kinds[dom]["bytes"] / kinds[dom]["launches"] if dom else None,
                      "launch_ms": 1e3 * kinds[dom]["seconds"] / kinds[dom]["launches"] if dom else None},

@@ -329,20 +329,23 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
       pl.warm = std::max(pl.warm, F[static_cast<std::size_t>(d)]);
       pl.lagS_max = std::max(pl.lagS_max, pl.D[static_cast<std::size_t>(d)].lagS);
     }
-  // ---- barriers: a loop starts a new region when it touches a dataset a loop of the
-  // current region wrote, or writes one the region read
-  std::vector<char> rr(static_cast<std::size_t>(nd), 0), ww(static_cast<std::size_t>(nd), 0);
+  // ---- barriers: a thread owns one ring column for every row, so only column-offset
+  // accesses cross threads. A loop starts a new region (barrier) when it reads at a
+  // column offset a dataset the current region wrote, or writes a dataset the region
+  // read at a column offset; row-offset and point accesses stay in program order.
+  std::vector<char> rc(static_cast<std::size_t>(nd), 0), ww(static_cast<std::size_t>(nd), 0);
   for (int i = 0; i < n; ++i) {
     SwLoop& S = pl.L[static_cast<std::size_t>(i)];
     bool conflict = false;
-    for (const auto& [d, r] : S.rd) conflict = conflict || ww[static_cast<std::size_t>(d)];
-    for (int d : S.wds) conflict = conflict || ww[static_cast<std::size_t>(d)] || rr[static_cast<std::size_t>(d)];
+    for (const auto& [d, r] : S.rd) conflict = conflict || (r.oc != 0 && ww[static_cast<std::size_t>(d)]);
+    for (int d : S.wds) conflict = conflict || rc[static_cast<std::size_t>(d)];
     if (conflict && i > 0) {
       S.barrier = true;
-      std::fill(rr.begin(), rr.end(), 0);
+      std::fill(rc.begin(), rc.end(), 0);
       std::fill(ww.begin(), ww.end(), 0);
     }
-    for (const auto& [d, r] : S.rd) rr[static_cast<std::size_t>(d)] = 1;
+    for (const auto& [d, r] : S.rd)
+      if (r.oc != 0) rc[static_cast<std::size_t>(d)] = 1;
     for (int d : S.wds) ww[static_cast<std::size_t>(d)] = 1;
   }
   // ---- launch box: loop ranges plus the allocations of out-of-place outputs (their

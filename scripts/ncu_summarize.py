@@ -4,7 +4,7 @@
 
 The launch list comes from `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --clock-control none --csv python scripts/ncu_driver.py ...`; the
-last chain's specialised-kernel launches (ooc_jit_kernel) are matched in order with the
+last chain's specialised-kernel launches (ooc_jit_kernel, ooc_sweep_kernel) are matched in order with the
 sequence the driver recorded. Per-launch times under ncu are cold-cache and serialised:
 compare shares, not absolutes.
 """
@@ -29,7 +29,7 @@ def main(csv_path, seq_path, out_path):
         e[r["Metric Name"]] = v * scale
     seq = json.load(open(seq_path))
     last = seq["last_chain"]
-    jit = [rows[i] for i in sorted(rows) if rows[i]["kernel"] == "ooc_jit_kernel"]
+    jit = [rows[i] for i in sorted(rows) if rows[i]["kernel"] in ("ooc_jit_kernel", "ooc_sweep_kernel")]
     jit = jit[-len(last):]
     iters = 14 if seq["app"].startswith("miniflow") else None
     groups = {}
@@ -41,7 +41,7 @@ def main(csv_path, seq_path, out_path):
         else:
             key = f"pos{pos}+{nl}"
         g = groups.setdefault(key, {"launches": 0, "s": 0.0, "dram": 0.0, "metric": 0.0,
-                                    "grid": r["grid"]})
+                                    "grid": r["grid"], "kernel": r["kernel"]})
         g["launches"] += 1
         g["s"] += r["gpu__time_duration.sum"]
         g["dram"] += r["dram__bytes_read.sum"] + r["dram__bytes_write.sum"]
@@ -53,7 +53,7 @@ def main(csv_path, seq_path, out_path):
     for k, g in sorted(groups.items(), key=lambda kv: -kv[1]["s"]):
         us = 1e6 * g["s"] / g["launches"]
         db = g["dram"] / g["launches"]
-        out["kernels"].append({"kernel": "ooc_jit_kernel", "group": k, "grid": g["grid"],
+        out["kernels"].append({"kernel": g["kernel"], "group": k, "grid": g["grid"],
                                "launches": g["launches"], "us_per_launch": round(us, 1),
                                "dram_bytes_per_launch": int(db),
                                "metric_bytes_per_launch": int(g["metric"] / g["launches"]),

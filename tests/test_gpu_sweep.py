@@ -68,9 +68,10 @@ def test_sweep_random_programs_vs_golden(golden_random, jit_always):
 
 
 def test_sweep_graph_replay_flips(jit_always):
-    """Captured chains replay with the recorded buffer swaps: 52 iterations (odd number of
-    sweeps per chain for some datasets) stay bit-exact."""
-    prog = P.app_program("miniflow2d", 200, 180, 0, iters=52)
+    """Captured chains replay with the recorded buffer swaps: 112 iterations (an odd number
+    of swaps per chain, so consecutive chains alternate between two graphs) stay
+    bit-exact."""
+    prog = P.app_program("miniflow2d", 200, 180, 0, iters=112)
     diff, rt = _resident_vs_oracle(prog)
     assert not diff, diff
     dev = rt.device()
