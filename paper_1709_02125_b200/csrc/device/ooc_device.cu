@@ -293,7 +293,21 @@ int ooc_copy_box(ooc_ctx* c, int q, int kind, const ooc_view* src, const ooc_vie
   const size_t rows = B >= 0 ? static_cast<size_t>(hi[B] - lo[B]) : 1;
   const size_t planes = A >= 0 ? static_cast<size_t>(hi[A] - lo[A]) : 1;
   cudaStream_t st = c->q[q];
-  if (planes == 1 && rows == 1) {
+  // Collapse what is contiguous on both sides: one 1-D copy when the whole region is
+  // (H2D pitched 3-D copies run at ~34 GB/s on B200 + PCIe 5, 1-D ones at ~55), one
+  // 2-D copy of whole planes when each plane is.
+  const int64_t w = hi[C] - lo[C];
+  auto rows_dense = [&](const ooc_view* v) { return rows == 1 || v->stride[B] == w; };
+  auto dense = [&](const ooc_view* v) {
+    return rows_dense(v) && (planes == 1 || v->stride[A] == w * static_cast<int64_t>(rows));
+  };
+  if (dense(src) && dense(dst)) {
+    OOC_CUDA_TRY(cudaMemcpyAsync(t, s, width * rows * planes, k, st));
+  } else if (planes > 1 && rows_dense(src) && rows_dense(dst)) {
+    OOC_CUDA_TRY(cudaMemcpy2DAsync(t, static_cast<size_t>(dst->stride[A]) * sizeof(double), s,
+                                   static_cast<size_t>(src->stride[A]) * sizeof(double), width * rows, planes, k,
+                                   st));
+  } else if (planes == 1 && rows == 1) {
     OOC_CUDA_TRY(cudaMemcpyAsync(t, s, width, k, st));
   } else if (planes == 1) {
     OOC_CUDA_TRY(cudaMemcpy2DAsync(t, static_cast<size_t>(dst->stride[B]) * sizeof(double), s,

@@ -65,6 +65,7 @@ using namespace oocdev;
 namespace {
 
 constexpr int kRC = 128;  // ring row width in columns (TC owned + 2*HC halo)
+constexpr int kPad = 16;  // doubles of shared memory before/after the rings (edge lanes' neighbour reads)
 
 // Parameter block; the kernel source declares an identical struct.
 struct SweepParams {
@@ -130,7 +131,7 @@ struct SwPlan {
 long long smem_budget() {
   static long long b = [] {
     const char* e = std::getenv("OOC_SWEEP_SMEM");
-    return e ? std::atoll(e) : 110LL * 1024;
+    return e ? std::atoll(e) : 48LL * 1024;  // measured: occupancy beats fewer DRAM passes
   }();
   return b;
 }
@@ -306,7 +307,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
     D.off = off;
     off += D.W * kRC;
   }
-  pl.smem = off * 8;
+  pl.smem = (off + 2 * kPad) * 8;
   if (pl.smem > smem_budget()) return fail(why, "shared memory");
   // ---- warm-up depth: first correct row of every version (relative to the sweep start)
   const long long NONE = LLONG_MIN / 4;
@@ -381,10 +382,16 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   const int K = pl.K;
   o << "#define SW_MAXL " << SW_MAXL << "\n#define SW_MAXD " << SW_MAXD << "\n#define SW_MAXC " << SW_MAXC << "\n";
   o << kSweepDecl;
-  o << "extern \"C\" __global__ void __launch_bounds__(" << pl.NT << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p) {\n";
+  static const int min_blocks = [] {
+    const char* e = std::getenv("OOC_SWEEP_MINB");
+    return e ? std::atoi(e) : 0;
+  }();
+  o << "extern \"C\" __global__ void __launch_bounds__(" << pl.NT;
+  if (min_blocks > 0) o << ", " << min_blocks;
+  o << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p) {\n";
   o << "  extern __shared__ __align__(16) double sw_sm[];\n";
   o << "  const int lc = threadIdx.x;\n";
-  o << "  double* const B = sw_sm + lc;\n";
+  o << "  double* const B = sw_sm + " << kPad << " + lc;\n";
   o << "  const long long c0 = p.C0 + static_cast<long long>(blockIdx.x) * " << pl.TC << ";\n";
   o << "  const long long r_own0 = p.R0 + static_cast<long long>(blockIdx.y) * p.seg_rows;\n";
   o << "  const long long r_own1 = min(p.R1, r_own0 + p.seg_rows);\n";
@@ -412,28 +419,32 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     }
   }
   // column predicates of every loop / store, once per thread, as bit masks
-  o << "  unsigned long long colmask = 0ull;\n  unsigned stmask = 0u, stfast = 0u;\n";
+  o << "  unsigned long long colmask = 0ull;\n  unsigned stmask = 0u;\n";
   for (int i = 0; i < pl.n; ++i) {
     const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
     o << "  if (lc >= " << pl.HC - S.h << " && lc < " << pl.HC + pl.TC + S.h << " && c >= p.rng[" << i
       << "][2] && c < p.rng[" << i << "][3]) colmask |= 1ull << " << i << ";\n";
   }
   o << "  const bool own_col = lc >= " << pl.HC << " && lc < " << pl.HC + pl.TC << " && c < p.C1;\n";
+  // interior strip: all 128 ring columns inside every loop range and load box, every
+  // owned column inside the launch box — the fast steps then evaluate every loop on
+  // every lane without predicates (lanes outside a loop's halo produce values nobody
+  // reads; their neighbour reads stay inside the padded shared-memory window)
+  o << "  const long long cl = c0 - " << pl.HC << ", ch = cl + " << kRC << ";\n";
+  o << "  bool strip_in = c0 + " << pl.TC << " <= p.C1;\n";
+  for (int i = 0; i < pl.n; ++i)
+    o << "  strip_in = strip_in && p.rng[" << i << "][2] <= cl && p.rng[" << i << "][3] >= ch;\n";
+  for (int d = 0; d < nd; ++d) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    if (D.loaded || D.store)
+      o << "  strip_in = strip_in && p.box[" << d << "][2] <= cl && p.box[" << d << "][3] >= ch;\n";
+  }
   for (int d = 0; d < nd; ++d) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     if (D.loaded)
       o << "  const bool colok" << d << " = c >= p.box[" << d << "][2] && c < p.box[" << d << "][3];\n";
     if (D.store) {
-      o << "  if (own_col && c >= p.box[" << d << "][2] && c < p.box[" << d << "][3]) {\n    stmask |= 1u << " << d
-        << ";\n";
-      if (D.oop) {
-        o << "    stfast |= 1u << " << d << ";\n";
-      } else {
-        o << "    if (false";
-        for (int j : D.writers) o << " || (c >= p.rng[" << j << "][2] && c < p.rng[" << j << "][3])";
-        o << ") stfast |= 1u << " << d << ";\n";
-      }
-      o << "  }\n";
+      o << "  if (own_col && c >= p.box[" << d << "][2] && c < p.box[" << d << "][3]) stmask |= 1u << " << d << ";\n";
     }
   }
   o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
@@ -447,13 +458,27 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     e << "]";
     return e.str();
   };
-  auto loads = [&](const std::string& step, const char* ind, bool fast) {
+  // element offsets of this thread's column in the row a load (gl) / store (gs) of the
+  // current step touches; advanced by K rows per step
+  for (int d = 0; d < nd; ++d) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    if (D.loaded)
+      o << "  long long gl" << d << " = (rbase + " << static_cast<long long>(pl.P) * K - D.lagL << " - p.box[" << d
+        << "][0]) * p.s0[" << d << "] + (c - p.box[" << d << "][2]);\n";
+    if (D.store)
+      o << "  long long gs" << d << " = (rbase - " << D.lagS << " - p.box[" << d << "][0]) * p.s0[" << d
+        << "] + (c - p.box[" << d << "][2]);\n";
+  }
+  auto loads = [&](const std::string& step, const char* ind, bool fast, bool running) {
     for (int d = 0; d < nd; ++d) {
       const SwDs& D = pl.D[static_cast<std::size_t>(d)];
       if (!D.loaded) continue;
       o << ind << "{\n" << ind << "  const int ul = (" << step << ") * " << K << " - " << D.lagL << ";\n";
-      o << ind << "  const double* g = p.src[" << d << "] + (rbase + ul - p.box[" << d << "][0]) * p.s0[" << d
-        << "] + (c - p.box[" << d << "][2]);\n";
+      if (running)
+        o << ind << "  const double* g = p.src[" << d << "] + gl" << d << ";\n";
+      else
+        o << ind << "  const double* g = p.src[" << d << "] + (rbase + ul - p.box[" << d << "][0]) * p.s0[" << d
+          << "] + (c - p.box[" << d << "][2]);\n";
       o << ind << "#pragma unroll\n" << ind << "  for (int r = 0; r < " << K << "; ++r) {\n";
       if (fast) {
         o << ind << "    const bool ok = colok" << d << ";\n";
@@ -468,11 +493,151 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     }
     o << ind << "asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
   };
-  for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false);
+  for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false, false);
   int ci0 = 0;
+  // ---- fast steps: rows r = 0..K-1 unrolled at generation so values stay in named
+  // registers across loops. A read of a value this thread produced earlier in the step
+  // (same dataset version, same row, column offset 0) is forwarded from its register;
+  // repeated reads of one ring element are loaded once; a write skips its shared-memory
+  // store when every consumer is such a forwarded read (and a final row stored this
+  // step takes the register too). Shared-memory bandwidth is the sweep's bound.
+  std::vector<std::vector<int>> prevw(static_cast<std::size_t>(pl.n), std::vector<int>(static_cast<std::size_t>(nd), -1));
+  for (int k = 0; k < pl.n; ++k)
+    for (int d = 0; d < nd; ++d)
+      for (int j = k - 1; j >= 0 && prevw[static_cast<std::size_t>(k)][static_cast<std::size_t>(d)] < 0; --j)
+        for (int w : pl.L[static_cast<std::size_t>(j)].wds)
+          if (w == d) prevw[static_cast<std::size_t>(k)][static_cast<std::size_t>(d)] = j;
+  auto tape_reads = [&](int k, std::vector<std::tuple<int, long long, long long>>& out) {
+    const ooc_loop& L = Ls[k];
+    for (int t = 0; t < L.ntape; ++t)
+      if (L.tape[t].op == OOC_OP_READ)
+        for (int d = 0; d < nd; ++d)
+          if (pl.D[static_cast<std::size_t>(d)].v->data == L.args[L.tape[t].arg].data)
+            out.emplace_back(d, L.tape[t].offset[0], L.tape[t].offset[1]);
+  };
+  std::vector<std::vector<char>> need_sts(static_cast<std::size_t>(pl.n), std::vector<char>(static_cast<std::size_t>(nd), 0));
+  std::vector<int> last_writer(static_cast<std::size_t>(nd), -1);
+  for (int j = 0; j < pl.n; ++j)
+    for (int d : pl.L[static_cast<std::size_t>(j)].wds) last_writer[static_cast<std::size_t>(d)] = j;
+  // A value may reach a consumer from ANY earlier writer of the dataset (loop ranges
+  // differ: where the latest writer is inactive, an older one supplied the point), and
+  // slow steps always read shared memory. So a write skips its store only if every later
+  // read of the dataset, and the final-row store, happen in the same step at the same
+  // row and column (forwardable in fast steps; a slow step re-stores what it writes).
+  for (int k = 0; k < pl.n; ++k) {
+    std::vector<std::tuple<int, long long, long long>> rs;
+    tape_reads(k, rs);
+    for (const auto& [d, orow, ocol] : rs)
+      for (int j = 0; j < k; ++j)
+        for (int w : pl.L[static_cast<std::size_t>(j)].wds)
+          if (w == d && (ocol != 0 || orow - pl.L[static_cast<std::size_t>(k)].lag != -pl.L[static_cast<std::size_t>(j)].lag))
+            need_sts[static_cast<std::size_t>(j)][static_cast<std::size_t>(d)] = 1;
+  }
+  for (int d = 0; d < nd; ++d) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    if (!D.store) continue;
+    for (int j : D.writers)
+      if (pl.L[static_cast<std::size_t>(j)].lag != D.lagS) need_sts[static_cast<std::size_t>(j)][static_cast<std::size_t>(d)] = 1;
+  }
+  static const bool forward = !(std::getenv("OOC_SWEEP_FWD") && std::atoi(std::getenv("OOC_SWEEP_FWD")) == 0);
+  if (!forward)
+    for (auto& v : need_sts) std::fill(v.begin(), v.end(), 1);
+  auto fast_body = [&]() {
+    const char* ind = "      ";
+    loads("s + " + std::to_string(pl.P), ind, true, true);
+    o << ind << "const int u = s * " << K << ";\n";
+    std::map<std::tuple<int, long long, long long>, std::string> cache;  // (d, row, col) -> register
+    int ci = ci0;
+    for (int i = 0; i < pl.n; ++i) {
+      const ooc_loop& L = Ls[i];
+      const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+      if (S.barrier) o << ind << "__syncthreads();\n";
+      o << ind << "// loop " << i << " (lag " << S.lag << ", halo " << S.h << ")\n";
+      int dsof_arg[OOC_MAX_ARGS];
+      for (int a = 0; a < L.nargs; ++a) {
+        dsof_arg[a] = -1;
+        for (int d = 0; d < nd; ++d)
+          if (pl.D[static_cast<std::size_t>(d)].v->data == L.args[a].data) dsof_arg[a] = d;
+      }
+      std::vector<std::vector<std::string>> outs(static_cast<std::size_t>(K));
+      const int ci_loop = ci;
+      for (int r = 0; r < K; ++r) {
+        ci = ci_loop;
+        const long long q0 = r - S.lag;
+        int tmp = 0;
+        const ooc_ins* t = L.tape;
+        const std::string pre = "f" + std::to_string(i) + "_" + std::to_string(r) + "_";
+        for (int w = 0; w < L.nwrites; ++w) {
+          std::vector<std::string> st;
+          for (int k = 0; k < L.write_len[w]; ++k, ++t) {
+            const ooc_ins& in = *t;
+            if (in.op == OOC_OP_CONST) {
+              st.push_back("p.cst[" + std::to_string(ci++) + "]");
+            } else if (in.op == OOC_OP_READ) {
+              const int d = dsof_arg[in.arg];
+              const auto key = std::make_tuple(d, q0 + in.offset[0], static_cast<long long>(in.offset[1]));
+              auto it = forward ? cache.find(key) : cache.end();
+              if (it == cache.end()) {
+                const std::string name = pre + std::to_string(tmp++);
+                o << ind << "const double " << name << " = " << at(d, "u", q0 + in.offset[0], in.offset[1]) << ";\n";
+                it = cache.emplace(key, name).first;
+              }
+              st.push_back(it->second);
+            } else {
+              const std::string y = st.back();
+              st.pop_back();
+              const std::string x = st.back();
+              st.pop_back();
+              const std::string name = pre + std::to_string(tmp++);
+              o << ind << "const double " << name << " = ";
+              switch (in.op) {
+                case OOC_OP_ADD: o << x << " + " << y; break;
+                case OOC_OP_SUB: o << x << " - " << y; break;
+                case OOC_OP_MUL: o << x << " * " << y; break;
+                case OOC_OP_DIV: o << x << " / " << y; break;
+                case OOC_OP_MIN: o << "ooc_min(" << x << ", " << y << ")"; break;
+                default: o << "ooc_max(" << x << ", " << y << ")"; break;
+              }
+              o << ";\n";
+              st.push_back(name);
+            }
+          }
+          outs[static_cast<std::size_t>(r)].push_back(st.back());
+        }
+      }
+      // writes land after every tape of the point (and of every row) has been evaluated
+      for (int r = 0; r < K; ++r)
+        for (int w = 0; w < L.nwrites; ++w) {
+          const int d = S.wds[static_cast<std::size_t>(w)];
+          const long long q = r - S.lag;
+          const std::string& v = outs[static_cast<std::size_t>(r)][static_cast<std::size_t>(w)];
+          for (auto it = cache.begin(); it != cache.end();)
+            it = std::get<0>(it->first) == d && (std::get<1>(it->first) == q || std::get<2>(it->first) != 0)
+                     ? cache.erase(it) : std::next(it);
+          cache[std::make_tuple(d, q, 0LL)] = v;
+          if (need_sts[static_cast<std::size_t>(i)][static_cast<std::size_t>(d)])
+            o << ind << at(d, "u", q, 0) << " = " << v << ";\n";
+        }
+    }
+    for (int d = 0; d < nd; ++d) {
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (!D.store) continue;
+      const std::string ds = std::to_string(d);
+      o << ind << "if (own_col) {\n";
+      for (int r = 0; r < K; ++r) {
+        auto it = forward && last_writer[static_cast<std::size_t>(d)] >= 0 &&
+                          pl.L[static_cast<std::size_t>(last_writer[static_cast<std::size_t>(d)])].lag == D.lagS
+                      ? cache.find(std::make_tuple(d, static_cast<long long>(r) - D.lagS, 0LL))
+                      : cache.end();
+        const std::string v = it != cache.end() ? it->second : at(d, "u", r - D.lagS, 0);
+        o << ind << "  p.dst[" << ds << "][gs" << ds << " + " << r << " * p.s0[" << ds << "]] = " << v << ";\n";
+      }
+      o << ind << "}\n";
+    }
+  };
   auto body = [&](bool fast) {
     const char* ind = "      ";
-    loads("s + " + std::to_string(pl.P), ind, fast);
+    loads("s + " + std::to_string(pl.P), ind, fast, true);
     o << ind << "const int u = s * " << K << ";\n";
     int ci = ci0;
     for (int i = 0; i < pl.n; ++i) {
@@ -480,7 +645,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
       if (S.barrier) o << ind << "__syncthreads();\n";
       const std::string is = std::to_string(i);
-      o << ind << "if (colmask & (1ull << " << i << ")) {  // loop " << i << " (lag " << S.lag << ", halo " << S.h << ")\n";
+      if (fast)
+        o << ind << "{  // loop " << i << " (lag " << S.lag << ", halo " << S.h << ")\n";
+      else
+        o << ind << "if (colmask & (1ull << " << i << ")) {  // loop " << i << " (lag " << S.lag << ", halo " << S.h
+          << ")\n";
       o << "#pragma unroll\n" << ind << "  for (int r = 0; r < " << K << "; ++r) {\n";
       if (!fast) {
         o << ind << "    const long long row = rbase + u + r - " << S.lag << ";\n";
@@ -541,10 +710,10 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       const SwDs& D = pl.D[static_cast<std::size_t>(d)];
       if (!D.store) continue;
       const std::string ds = std::to_string(d);
-      o << ind << "if (" << (fast ? "stfast" : "stmask") << " & (1u << " << ds << ")) {\n#pragma unroll\n" << ind
+      o << ind << "if (" << (fast ? std::string("own_col") : "stmask & (1u << " + ds + ")") << ") {\n#pragma unroll\n" << ind
         << "  for (int r = 0; r < " << K << "; ++r) {\n";
-      o << ind << "    const long long row = rbase + u + r - " << D.lagS << ";\n";
       if (!fast) {
+        o << ind << "    const long long row = rbase + u + r - " << D.lagS << ";\n";
         o << ind << "    if (row >= r_own0 && row < r_own1 && row >= p.box[" << ds << "][0] && row < p.box[" << ds
           << "][1]";
         if (!D.oop) {
@@ -556,18 +725,24 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         }
         o << ")\n";
       }
-      o << ind << "      p.dst[" << ds << "][(row - p.box[" << ds << "][0]) * p.s0[" << ds << "] + (c - p.box[" << ds
-        << "][2])] = " << at(d, "u + r", -D.lagS, 0) << ";\n" << ind << "  }\n" << ind << "}\n";
+      o << ind << "      p.dst[" << ds << "][gs" << ds << " + r * p.s0[" << ds << "]] = " << at(d, "u + r", -D.lagS, 0)
+        << ";\n" << ind << "  }\n" << ind << "}\n";
     }
   };
   o << "  for (int s = 0; s < nsteps; ++s) {\n";
   o << "    asm volatile(\"cp.async.wait_group " << pl.P - 1 << ";\" ::: \"memory\");\n";
   o << "    __syncthreads();\n";
-  o << "    if (s >= s_lo && s < s_hi) {\n";
-  body(true);
+  o << "    if (strip_in && s >= s_lo && s < s_hi) {\n";
+  fast_body();
   o << "    } else {\n";
   body(false);
-  o << "    }\n  }\n  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n}\n";
+  o << "    }\n";
+  for (int d = 0; d < nd; ++d) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    if (D.loaded) o << "    gl" << d << " += " << K << " * p.s0[" << d << "];\n";
+    if (D.store) o << "    gs" << d << " += " << K << " * p.s0[" << d << "];\n";
+  }
+  o << "  }\n  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n}\n";
   return o.str();
 }
 
@@ -583,16 +758,16 @@ std::mutex g_sw_mu;
 int sweep_K() {
   static int k = [] {
     const char* e = std::getenv("OOC_SWEEP_K");
-    const int v = e ? std::atoi(e) : 2;
-    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 2;
+    const int v = e ? std::atoi(e) : 1;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 1;
   }();
   return k;
 }
 int sweep_P() {
   static int pp = [] {
     const char* e = std::getenv("OOC_SWEEP_P");
-    const int v = e ? std::atoi(e) : 2;
-    return v >= 1 && v <= 4 ? v : 2;
+    const int v = e ? std::atoi(e) : 1;
+    return v >= 1 && v <= 4 ? v : 1;
   }();
   return pp;
 }

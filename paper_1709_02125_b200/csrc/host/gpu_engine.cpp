@@ -598,7 +598,10 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
         }
       }
     if (big.empty()) continue;
-    lay[static_cast<std::size_t>(d)] = padded_layout(big);
+    // rows padded to 16 B only (TMA stride rule): an arena row then matches the host
+    // row whenever the tile box spans the dataset's full inner extent, and the box
+    // copies collapse to 1-D DMA (ooc_copy_box)
+    lay[static_cast<std::size_t>(d)] = padded_layout(big, 2);
     off[static_cast<std::size_t>(d)] = slot_elems;
     slot_elems += (lay[static_cast<std::size_t>(d)].elems + 31) / 32 * 32;  // 256-B aligned
   }
@@ -800,7 +803,7 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     for (DatasetId d : used) {
       const auto& pd = P(d);
       if (pd.write_first || pd.full[0].empty()) continue;
-      st_lay.push_back({d, padded_layout(pd.full[0])});
+      st_lay.push_back({d, padded_layout(pd.full[0], 2)});
       need += (st_lay.back().second.elems + 31) / 32 * 32;
     }
     ensure_staging(need);
