@@ -1014,8 +1014,11 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
   }();
   const bool graphs_ok = graphs_on && !(halos && comm_ready_) && !opts_.profile_loops && !opts_.timeline;
   GraphEntry* ge = nullptr;
-  int par = 0;
+  int par = 0, sseen = 0;
   if (graphs_ok) {
+    // sightings count per chain structure; graphs are kept per buffer state (sweeps that
+    // swap an odd number of times make consecutive chains alternate between two states)
+    sseen = ++struct_seen_[graph_key(chain, plan, false)];
     ge = &graphs_[graph_key(chain, plan)];
     ++ge->seen;
     par = ge->flip;
@@ -1066,7 +1069,7 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
   }
   // capture on the third sighting (tuning-complete chains from the second); shapes
   // still being tuned are frozen at the fastest measured
-  const bool capture = ge && (ge->settled || ge->seen >= 3);
+  const bool capture = ge && (ge->settled || sseen >= 3);
   static const bool gdbg = std::getenv("OOC_GRAPH_DEBUG") != nullptr;
   if (gdbg)
     std::fprintf(stderr, "graph: chain %d loops %zu ok %d entry %d seen %d par %d settled %d graphs %zu\n",
@@ -1156,7 +1159,7 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
   } else if (ge) {
     ooc_dev_stats st{};
     DEV(ooc_stats(ctx_, &st));
-    ge->settled = ge->seen >= 2 && st.jit_unsettled == unsettled0;
+    ge->settled = sseen >= 2 && st.jit_unsettled == unsettled0;
   }
   if (halos && comm_ready_) {
     // slab decomposition: refresh every ghost band from the neighbours' owned rows,
@@ -1273,7 +1276,7 @@ void GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& ru
   }
 }
 
-std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan) const {
+std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan, bool pointers) const {
   std::string k;
   auto put = [&](const void* p, std::size_t n) { k.append(static_cast<const char*>(p), n); };
   auto put_i = [&](long long v) { put(&v, sizeof v); };
@@ -1288,8 +1291,10 @@ std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan) c
     for (const LoopArg& a : l.args) {
       put_i(a.dataset);
       put_i(static_cast<long long>(a.mode));
-      const double* dev = res_[static_cast<std::size_t>(a.dataset)].dev;
-      put(&dev, sizeof dev);
+      if (pointers) {
+        const double* dev = res_[static_cast<std::size_t>(a.dataset)].dev;
+        put(&dev, sizeof dev);
+      }
       put_i(static_cast<long long>(a.stencil.offsets.size()));
       for (const Point& o : a.stencil.offsets) put(o.data(), sizeof(index_t) * 3);
     }

@@ -212,7 +212,8 @@ class GpuEngine {
   };
   std::map<std::string, GraphEntry> graphs_;
   int next_graph_slot_ = OOC_REDUCE_SLOTS / 2;
-  std::string graph_key(const LoopChain& chain, const TilePlan* plan) const;
+  std::string graph_key(const LoopChain& chain, const TilePlan* plan, bool pointers = true) const;
+  std::map<std::string, int> struct_seen_;  // sightings per chain structure (all buffer states)
   ooc_event* tl_base_ = nullptr;
   std::chrono::steady_clock::time_point tl_host0_;
   int next_cmd_ = 0;

@@ -33,11 +33,11 @@ def test_miniflow2d_timesteps_fuse_into_sweeps(jit_always):
         for d in pl["datasets"]:
             assert d["oop"] == (d["loaded"] and d["written"])
             assert d["W"] >= pl["K"]
-    # runs end on timestep boundaries; the temporaries a later run rewrites before
-    # reading are not stored (dead), only the chain's last run stores them
+    # temporaries a later run rewrites before reading are not stored (dead stores); the
+    # chain's last run stores every dataset it writes
     c1 = rt.chain_sweep_check(max(chains), compile=False)
-    assert all(g["loops"] % 14 == 0 for g in c1)
-    assert all(len(g["dead"]) == 6 for g in c1[:-1]) and c1[-1]["dead"] == []
+    assert all(len(g["dead"]) >= 1 for g in c1[:-1]) and c1[-1]["dead"] == []
+    assert len(c1[0]["dead"]) == 6
     first = groups[0]["plan"]["datasets"]
     # rho, e, v are read and rewritten: out of place; temporaries are written first
     assert sum(d["oop"] for d in first) == 3
