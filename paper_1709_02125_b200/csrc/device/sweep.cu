@@ -131,7 +131,7 @@ struct SwPlan {
 long long smem_budget() {
   static long long b = [] {
     const char* e = std::getenv("OOC_SWEEP_SMEM");
-    return e ? std::atoll(e) : 48LL * 1024;  // measured: occupancy beats fewer DRAM passes
+    return e ? std::atoll(e) : 56LL * 1024;  // measured: occupancy beats fewer DRAM passes
   }();
   return b;
 }
@@ -542,11 +542,30 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   static const bool forward = !(std::getenv("OOC_SWEEP_FWD") && std::atoi(std::getenv("OOC_SWEEP_FWD")) == 0);
   if (!forward)
     for (auto& v : need_sts) std::fill(v.begin(), v.end(), 1);
-  auto fast_body = [&]() {
+  // Carries: a ring element this thread holds in a register at the end of a fast step
+  // (row u+q+K, column offset 0) whose first access in the next step is a read of the
+  // same element (now row u'+q) enters that step as a register — the row-offset reads of
+  // stencils stop re-loading rows the column already read. Only this thread writes its
+  // column and loads land in rows of later steps, so the value cannot change in between;
+  // after a slow step the carries are reloaded from the rings.
+  using Key = std::tuple<int, long long, long long>;
+  struct FastInfo {
+    std::vector<Key> first_lds;     // keys whose first access in the step loaded the ring
+    std::map<Key, std::string> end; // register of each cached key at the end of the step
+  };
+  std::vector<std::pair<Key, std::string>> carries;  // (key at step start, register name)
+  auto fast_body = [&](FastInfo* info) {
     const char* ind = "      ";
     loads("s + " + std::to_string(pl.P), ind, true, true);
     o << ind << "const int u = s * " << K << ";\n";
     std::map<std::tuple<int, long long, long long>, std::string> cache;  // (d, row, col) -> register
+    if (!carries.empty()) {
+      o << ind << "if (!prev_fast) {\n";
+      for (const auto& [k, name] : carries)
+        o << ind << "  " << name << " = " << at(std::get<0>(k), "u", std::get<1>(k), 0) << ";\n";
+      o << ind << "}\n";
+      for (const auto& [k, name] : carries) cache[k] = name;
+    }
     int ci = ci0;
     for (int i = 0; i < pl.n; ++i) {
       const ooc_loop& L = Ls[i];
@@ -581,6 +600,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
                 const std::string name = pre + std::to_string(tmp++);
                 o << ind << "const double " << name << " = " << at(d, "u", q0 + in.offset[0], in.offset[1]) << ";\n";
                 it = cache.emplace(key, name).first;
+                if (info && in.offset[1] == 0) info->first_lds.push_back(key);
               }
               st.push_back(it->second);
             } else {
@@ -634,7 +654,26 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       }
       o << ind << "}\n";
     }
+    if (info) info->end = cache;
+    for (const auto& [k, name] : carries) {  // parallel assignment: sources may be carries
+      auto it = cache.find(std::make_tuple(std::get<0>(k), std::get<1>(k) + K, 0LL));
+      o << ind << "const double n" << name << " = " << it->second << ";\n";
+    }
+    for (const auto& [k, name] : carries) o << ind << name << " = n" << name << ";\n";
+    o << ind << "prev_fast = true;\n";
   };
+  if (forward) {  // pass 1 (discarded): which loads could be carries
+    FastInfo info;
+    std::ostringstream keep;
+    std::swap(o, keep);
+    fast_body(&info);
+    std::swap(o, keep);
+    for (const Key& k : info.first_lds)
+      if (info.end.count(std::make_tuple(std::get<0>(k), std::get<1>(k) + K, 0LL)))
+        carries.push_back({k, "cr" + std::to_string(carries.size())});
+  }
+  for (const auto& [k, name] : carries) o << "  double " << name << " = 0.0;\n";
+  o << "  bool prev_fast = false;\n";
   auto body = [&](bool fast) {
     const char* ind = "      ";
     loads("s + " + std::to_string(pl.P), ind, fast, true);
@@ -733,10 +772,10 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   o << "    asm volatile(\"cp.async.wait_group " << pl.P - 1 << ";\" ::: \"memory\");\n";
   o << "    __syncthreads();\n";
   o << "    if (strip_in && s >= s_lo && s < s_hi) {\n";
-  fast_body();
+  fast_body(nullptr);
   o << "    } else {\n";
   body(false);
-  o << "    }\n";
+  o << "      prev_fast = false;\n    }\n";
   for (int d = 0; d < nd; ++d) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     if (D.loaded) o << "    gl" << d << " += " << K << " * p.s0[" << d << "];\n";
@@ -766,8 +805,8 @@ int sweep_K() {
 int sweep_P() {
   static int pp = [] {
     const char* e = std::getenv("OOC_SWEEP_P");
-    const int v = e ? std::atoi(e) : 1;
-    return v >= 1 && v <= 4 ? v : 1;
+    const int v = e ? std::atoi(e) : 3;
+    return v >= 1 && v <= 4 ? v : 3;
   }();
   return pp;
 }

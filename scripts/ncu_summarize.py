@@ -23,7 +23,7 @@ def main(csv_path, seq_path, out_path):
         e = rows.setdefault(int(r["ID"]), {"kernel": r["Kernel Name"], "grid": r["Grid Size"]})
         v = float(r["Metric Value"].replace(",", ""))
         unit = r["Metric Unit"]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3,
+        scale = {"": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1, "KB": 1e3,
                  "MB": 1e6, "GB": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
                  "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "second": 1, "s": 1}[unit]
         e[r["Metric Name"]] = v * scale
@@ -45,6 +45,7 @@ def main(csv_path, seq_path, out_path):
         g["launches"] += 1
         g["s"] += r["gpu__time_duration.sum"]
         g["dram"] += r["dram__bytes_read.sum"] + r["dram__bytes_write.sum"]
+        g["smem"] = g.get("smem", 0.0) + 128.0 * r.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 0.0)
         g["metric"] += nbytes
     total = sum(g["s"] for g in groups.values())
     out = {"source": f"ncu launch list {csv_path}; last chain of scripts/ncu_driver.py "
@@ -58,6 +59,8 @@ def main(csv_path, seq_path, out_path):
                                "dram_bytes_per_launch": int(db),
                                "metric_bytes_per_launch": int(g["metric"] / g["launches"]),
                                "dram_TBps": round(db / us / 1e6, 3),
+                               "smem_bytes_per_launch": int(g.get("smem", 0.0) / g["launches"]),
+                               "smem_TBps": round(g.get("smem", 0.0) / g["launches"] / us / 1e6, 3),
                                "share": round(g["s"] / total, 3)})
     with open(out_path, "w") as f:
         json.dump(out, f, indent=1)
