@@ -145,8 +145,9 @@ def _nloops(group):
         return 1
 
 
-def profiled_traffic(group):
-    """DRAM bytes per launch of `group` from the committed ncu launch list
+def profiled_traffic(group, key="dram_bytes_per_launch"):
+    """Bytes per launch of `group` (DRAM, or shared memory with key=
+    "smem_bytes_per_launch") from the committed ncu launch list
     (profiles/*_traffic.json, produced from the same bench command)."""
     import glob
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), reverse=True):
@@ -156,8 +157,8 @@ def profiled_traffic(group):
         except Exception:
             continue
         for k in prof.get("kernels", []):
-            if k.get("group", "").split(" ")[0] == group:
-                return k["dram_bytes_per_launch"], os.path.relpath(f, ROOT)
+            if k.get("group", "").split(" ")[0] == group and k.get(key):
+                return k[key], os.path.relpath(f, ROOT)
     return None, None
 
 
@@ -360,6 +361,20 @@ def main():
     achieved = (kinds[dom]["bytes"] / kinds[dom]["seconds"] / 1e9) if dom else None
     total_k = sum(k["seconds"] for k in kinds.values())
     traffic, traffic_src = profiled_traffic(dom) if dom else (None, None)
+    # the row-sweep kernels move their operands through shared memory: its bandwidth
+    # (148 SMs x 128 B/clk at the measured SM clock) is the ceiling that binds them
+    limiter = None
+    smem_b, _ = profiled_traffic(dom, "smem_bytes_per_launch") if dom else (None, None)
+    if smem_b and dom:
+        launch_s = kinds[dom]["seconds"] / kinds[dom]["launches"]
+        mhz = (inc.get("clocks") or {}).get("sm_mhz") or 1965.0
+        smem_peak = 148 * 128 * mhz * 1e6 / 1e9
+        dram_gbps = traffic / launch_s / 1e9 if traffic else None
+        limiter = {"smem_bytes_per_launch": smem_b, "smem_GBps": smem_b / launch_s / 1e9,
+                   "smem_peak_GBps": smem_peak, "smem_frac": smem_b / launch_s / 1e9 / smem_peak,
+                   "dram_frac": dram_gbps / peak if dram_gbps else None,
+                   "binding": ("shared memory" if dram_gbps is None or
+                               smem_b / launch_s / 1e9 / smem_peak > dram_gbps / peak else "hbm")}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": warm, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
@@ -389,7 +404,8 @@ def main():
                                 f"ooc_jit_kernel [{dom}] (fused sm_100a par_loop kernel)"),
                      "kernel_share_of_step": kinds[dom]["seconds"] / total_k if dom else None,
                      "bytes_per_launch": kinds[dom]["bytes"] / kinds[dom]["launches"] if dom else None,
-                     "launch_ms": 1e3 * kinds[dom]["seconds"] / kinds[dom]["launches"] if dom else None},
+                     "launch_ms": 1e3 * kinds[dom]["seconds"] / kinds[dom]["launches"] if dom else None,
+                     "limiter": limiter},
         "kernels": {k: {"launches": v["launches"], "GBps": round(v["bytes"] / v["seconds"] / 1e9),
                         "share": round(v["seconds"] / total_k, 3)} for k, v in sorted(kinds.items())},
         "tile_shapes": B.jit_report(),

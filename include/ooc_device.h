@@ -208,6 +208,8 @@ int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int len, int com
  * (interpreter only), 1: for launches of >= min_points points (default 2^18),
  * 2: always (error if NVRTC is unavailable). Env: OOC_JIT, OOC_JIT_MIN_POINTS. */
 int ooc_jit_config(int mode, long long min_points);
+/* Current specialisation policy (mode, threshold) as set by ooc_jit_config / OOC_JIT. */
+int ooc_jit_policy(int* mode, long long* min_points);
 /* Generate + NVRTC-compile (no load, no GPU needed) the specialised kernel of a
  * group; `log` receives the generated body or the compiler log. */
 int ooc_jit_compile_check(const ooc_loop* loops, int n, char* log, int len);

@@ -1742,6 +1742,12 @@ extern "C" int ooc_jit_settled(void) {
   return 1;
 }
 
+extern "C" int ooc_jit_policy(int* m, long long* min_points) {
+  const int mm = jit_policy(min_points);
+  if (m) *m = mm;
+  return OOC_OK;
+}
+
 extern "C" int ooc_jit_config(int m, long long min_points) {
   g_mode = m;
   if (min_points >= 0) g_min_points = min_points;

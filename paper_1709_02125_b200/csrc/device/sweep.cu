@@ -952,10 +952,27 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   }
   const long long rows = pl.box[1] - pl.box[0];
   const long long strips = (pl.box[3] - pl.box[2] + pl.TC - 1) / pl.TC;
-  const long long want = static_cast<long long>(c->prop.multiProcessorCount) * k->occ * 4;
-  long long nseg = std::max<long long>(1, (want + strips - 1) / strips);
+  // Row segments per strip: whole waves of CTAs (the grid is strips x segments; a
+  // partial last wave idles SMs), at least ~4 waves, segments >= 8 warm-up depths.
+  const long long cap = static_cast<long long>(c->prop.multiProcessorCount) * k->occ;
   const long long min_seg = std::max<long long>(64, 8 * (pl.warm + pl.lagS_max + pl.K));
-  nseg = std::max<long long>(1, std::min(nseg, rows / min_seg));
+  const long long max_nseg = std::max<long long>(1, rows / min_seg);
+  long long nseg = 1;
+  double best = -1.0;
+  for (long long ns = 1; ns <= std::min<long long>(max_nseg, 4096); ++ns) {
+    const long long seg = (rows + ns - 1) / ns, real = (rows + seg - 1) / seg, ctas = strips * real;
+    const long long waves = (ctas + cap - 1) / cap;
+    // wave efficiency, with a mild preference for >= 4 waves (dynamic balance)
+    const double overhead = static_cast<double>(pl.warm + pl.lagS_max + pl.P * pl.K);  // rows swept, not stored
+    const double eff = static_cast<double>(ctas) / static_cast<double>(waves * cap) * static_cast<double>(seg) /
+                           (static_cast<double>(seg) + overhead) -
+                       (waves < 4 ? 0.05 * (4 - waves) : 0.0);
+    if (eff > best + 1e-9) {
+      best = eff;
+      nseg = real;
+    }
+    if (waves > 16) break;
+  }
   sp->seg_rows = (rows + nseg - 1) / nseg;
   nseg = (rows + sp->seg_rows - 1) / sp->seg_rows;
   c->stats.sweep_launches++;

@@ -1117,7 +1117,11 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
   const std::vector<SweepRun>* sweeps = nullptr;
   static const std::vector<SweepRun> no_sweeps;
   if (T == 1 && opts_.fuse && sweep_enabled()) {
-    const std::string key = sweep_key(mesh, chain);
+    // the partition depends on the specialisation policy too (size threshold, OOC_JIT)
+    int jm = 1;
+    long long jmin = 0;
+    ooc_jit_policy(&jm, &jmin);
+    const std::string key = sweep_key(mesh, chain) + "|" + std::to_string(jm) + "|" + std::to_string(jmin);
     auto it = sweep_cache.find(key);
     if (it == sweep_cache.end()) {
       std::vector<ooc_loop> calls;

@@ -117,6 +117,9 @@ def test_native_app_equals_program_on_gpu():
     for d in range(a.num_datasets):
         assert np.array_equal(a.host(d).view(np.uint64), b.host(d).view(np.uint64))
     assert a.fetch_reduction("fieldsum") == b.fetch_reduction("fieldsum")
+    if jit == 2:
+        assert a.device()["sweep_launches"] > 0
+        B.set_jit(1, 1 << 18)
 
 
 def test_l2_budget_tiling_miniflow():
@@ -298,17 +301,26 @@ def test_graph_replay_parity(budget, jit_always):
     assert rt.device()["graph_launches"] >= 2
 
 
-def test_slab_runtime_with_nccl_single_rank():
+@pytest.mark.parametrize("jit", [1, 2])
+def test_slab_runtime_with_nccl_single_rank(jit):
     """The multi-GPU path on one GPU: a 1-rank NCCL communicator, a dim-0 window with
-    ghost rows, all-reduce of the fieldsum — same bits / same reduction as plain."""
+    ghost rows, all-reduce of the fieldsum — same bits / same reduction as plain. jit=2:
+    every launch specialised, so the slab runtime runs row-sweep kernels with buffer
+    swaps and exchanges ghost rows from the current buffers."""
     from paper_1709_02125_b200 import dist as D
-    n, iters = 96, 20
-    ghost = D.chain_depth("miniflow2d", iters)
-    a = B.Runtime("resident", dist=(0, 1), own=(0, n), ghost=ghost)
-    a.comm_init(D.unique_id())
-    a.run_app("miniflow2d", n, n, 0, iters)
-    b = B.Runtime("resident")
-    b.run_app("miniflow2d", n, n, 0, iters)
-    for d in range(b.num_datasets):
-        assert np.array_equal(a.fetch_dataset(d).view(np.uint64), b.fetch_dataset(d).view(np.uint64))
-    assert a.fetch_reduction("fieldsum") == b.fetch_reduction("fieldsum")
+    B.set_jit(jit, 0 if jit == 2 else 1 << 18)
+    try:
+        n, iters = 96, 20
+        ghost = D.chain_depth("miniflow2d", iters)
+        a = B.Runtime("resident", dist=(0, 1), own=(0, n), ghost=ghost)
+        a.comm_init(D.unique_id())
+        a.run_app("miniflow2d", n, n, 0, iters)
+        b = B.Runtime("resident")
+        b.run_app("miniflow2d", n, n, 0, iters)
+        for d in range(b.num_datasets):
+            assert np.array_equal(a.fetch_dataset(d).view(np.uint64), b.fetch_dataset(d).view(np.uint64))
+        assert a.fetch_reduction("fieldsum") == b.fetch_reduction("fieldsum")
+        if jit == 2:
+            assert a.device()["sweep_launches"] > 0
+    finally:
+        B.set_jit(1, 1 << 18)
