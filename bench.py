@@ -431,11 +431,15 @@ def main():
                                      "d2h": e2e["downloaded"] / e2e["wall"] / 1e9}}
         if link and "concurrent" in link:
             # SURVEY §8(d) out-of-core roofline: min(in-core, BW_h2d·metric/up, BW_d2h·metric/down)
-            # with the pinned-copy bandwidths measured concurrently on this box
-            bw = link["concurrent"]
+            # with the pinned-copy bandwidths measured on this box: each direction alone
+            # bounds its own bytes, and the two directions together share the duplex link
+            # (sum of the concurrently measured rates) — the engine's up/down mix is not 1:1
+            bw, alone = link["concurrent"], link["alone"]
             lim = {"incore": value / world,
-                   "h2d": bw["h2d"] * e2e["bytes"] / max(e2e["uploaded"], 1),
-                   "d2h": bw["d2h"] * e2e["bytes"] / max(e2e["downloaded"], 1)}
+                   "h2d": alone["h2d"] * e2e["bytes"] / max(e2e["uploaded"], 1),
+                   "d2h": alone["d2h"] * e2e["bytes"] / max(e2e["downloaded"], 1),
+                   "duplex": (bw["h2d"] + bw["d2h"]) * e2e["bytes"] /
+                             max(e2e["uploaded"] + e2e["downloaded"], 1)}
             bound = min(lim, key=lim.get)
             line["e2e"]["roofline"] = {"bound": bound, "limit": lim[bound] * world, "unit": UNIT,
                                        "frac": e2e_val / (lim[bound] * world), "limits": lim,
