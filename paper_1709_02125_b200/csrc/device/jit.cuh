@@ -38,6 +38,8 @@ int jit_launch_group(ooc_ctx* c, int q, const ooc_loop* loops, int n, int* block
 // dependent launch on queue q (counts one specialised launch).
 int jit_policy(long long* min_points);  // OOC_JIT mode (0/1/2) and its size threshold
 bool jit_available(bool load, std::string& why);
+// acc[slot] = combine(acc[slot], fixed-order fold of the queue's `blocks` partials)
+int launch_fold(ooc_ctx* c, int q, int blocks, int slot, int op);
 bool jit_build_kernel(const std::string& src, const char* kname, int block, long long smem, void** fn,
                       int* occ, std::string& err, bool load);
 int jit_launch_kernel(ooc_ctx* c, int q, void* fn, unsigned gx, unsigned gy, unsigned block, unsigned smem,

@@ -695,3 +695,13 @@ int ooc_reduce_fetch(ooc_ctx* c, int q, int slot, double* dst) {
 }
 
 }  // extern "C"
+
+
+namespace oocdev {
+int launch_fold(ooc_ctx* c, int q, int blocks, int slot, int op) {
+  k_fold<<<1, 1024, 0, c->q[q]>>>(c->red_part[q], blocks, c->red_acc + slot, op);
+  OOC_CUDA_TRY(cudaGetLastError());
+  ++c->stats.kernel_launches;
+  return OOC_OK;
+}
+}  // namespace oocdev

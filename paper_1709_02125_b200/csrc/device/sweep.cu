@@ -69,6 +69,7 @@ constexpr int kPad = 16;  // doubles of shared memory before/after the rings (ed
 
 // Parameter block; the kernel source declares an identical struct.
 struct SweepParams {
+  double* part;              // reduction: one partial per CTA
   long long R0, R1, C0, C1;  // launch box: rows [R0,R1) x columns [C0,C1), absolute
   long long seg_rows;        // rows owned per CTA row-segment
   long long rng[SW_MAXL][4];  // per loop: rows [0,1), columns [2,3), absolute
@@ -81,6 +82,7 @@ struct SweepParams {
 
 const char* kSweepDecl = R"CUDA(
 struct SweepParams {
+  double* part;
   long long R0, R1, C0, C1;
   long long seg_rows;
   long long rng[SW_MAXL][4];
@@ -92,6 +94,11 @@ struct SweepParams {
 };
 __device__ __forceinline__ double ooc_min(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double ooc_max(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double ooc_red(int op, double acc, double v) {
+  if (op == 1) return acc + v;
+  if (op == 2) return v < acc ? v : acc;
+  return acc < v ? v : acc;
+}
 __device__ __forceinline__ long long sw_floordiv(long long a, long long k) {
   return a >= 0 ? a / k : -((-a + k - 1) / k);
 }
@@ -123,6 +130,8 @@ struct SwDs {
 struct SwPlan {
   int n = 0, K = 2, P = 2, NT = 256;
   long long HC = 0, TC = 0, warm = 0, lagS_max = 0, smem = 0;
+  int red_op = OOC_RED_NONE;  // the run's last loop reduces (no writes): folded per CTA
+  long long red_lag = 0;
   long long box[4] = {0, 0, 0, 0};  // launch box rows/cols
   std::vector<SwLoop> L;
   std::vector<SwDs> D;
@@ -173,7 +182,8 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
     const ooc_loop& L = Ls[i];
     SwLoop& S = pl.L[static_cast<std::size_t>(i)];
     if (L.ndim != 2) return fail(why, "not 2-D");
-    if (L.reduce_op != OOC_RED_NONE) return fail(why, "reduction");
+    if (L.reduce_op != OOC_RED_NONE && (i != n - 1 || L.nwrites != 0 || n < 2))
+      return fail(why, "reduction (only as the last, write-free loop of a run)");
     if (L.lo[2] != 0 || L.hi[2] != 1 || L.hi[0] <= L.lo[0] || L.hi[1] <= L.lo[1]) return fail(why, "range");
     tape_total += L.ntape;
     for (int t = 0; t < L.ntape; ++t) {
@@ -314,6 +324,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   std::vector<long long> F(static_cast<std::size_t>(nd), NONE);
   for (int d = 0; d < nd; ++d)
     if (pl.D[static_cast<std::size_t>(d)].loaded) F[static_cast<std::size_t>(d)] = -pl.D[static_cast<std::size_t>(d)].lagL;
+  long long F_red = NONE;
   for (int i = 0; i < n; ++i) {
     const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
     long long Fi = -S.lag;
@@ -322,9 +333,18 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
       Fi = std::max(Fi, F[static_cast<std::size_t>(d)] - r.omin);
     }
     for (int d : S.wds) F[static_cast<std::size_t>(d)] = F[static_cast<std::size_t>(d)] == NONE ? Fi : std::max(F[static_cast<std::size_t>(d)], Fi);
+    if (Ls[i].reduce_op != OOC_RED_NONE) {
+      F_red = Fi;
+      pl.red_op = Ls[i].reduce_op;
+      pl.red_lag = S.lag;
+    }
   }
   pl.warm = 0;
   pl.lagS_max = 0;
+  if (pl.red_op != OOC_RED_NONE) {  // the reduction counts owned rows only: they must be exact
+    pl.warm = std::max(pl.warm, F_red);
+    pl.lagS_max = std::max(pl.lagS_max, pl.red_lag);
+  }
   for (int d = 0; d < nd; ++d)
     if (pl.D[static_cast<std::size_t>(d)].store) {
       pl.warm = std::max(pl.warm, F[static_cast<std::size_t>(d)]);
@@ -417,6 +437,13 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         for (int j : D.writers)
           fast_rows(-D.lagS, "p.rng[" + std::to_string(j) + "][0]", "p.rng[" + std::to_string(j) + "][1]");
     }
+  }
+  if (pl.red_op != OOC_RED_NONE) {
+    const std::string ri = std::to_string(pl.n - 1);
+    fast_rows(-pl.red_lag, "max(r_own0, p.rng[" + ri + "][0])", "min(r_own1, p.rng[" + ri + "][1])");
+    o << "  double racc = " << (pl.red_op == OOC_RED_SUM ? "0.0" : pl.red_op == OOC_RED_MIN ? "__longlong_as_double(0x7ff0000000000000LL)"
+                                                                                           : "__longlong_as_double(0xfff0000000000000LL)")
+      << ";\n";
   }
   // column predicates of every loop / store, once per thread, as bit masks
   o << "  unsigned long long colmask = 0ull;\n  unsigned stmask = 0u;\n";
@@ -586,9 +613,9 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         int tmp = 0;
         const ooc_ins* t = L.tape;
         const std::string pre = "f" + std::to_string(i) + "_" + std::to_string(r) + "_";
-        for (int w = 0; w < L.nwrites; ++w) {
+        for (int w = 0; w < L.nwrites + (L.reduce_op != OOC_RED_NONE ? 1 : 0); ++w) {
           std::vector<std::string> st;
-          for (int k = 0; k < L.write_len[w]; ++k, ++t) {
+          for (int k = 0; k < (w < L.nwrites ? L.write_len[w] : L.reduce_len); ++k, ++t) {
             const ooc_ins& in = *t;
             if (in.op == OOC_OP_CONST) {
               st.push_back("p.cst[" + std::to_string(ci++) + "]");
@@ -638,6 +665,10 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
           if (need_sts[static_cast<std::size_t>(i)][static_cast<std::size_t>(d)])
             o << ind << at(d, "u", q, 0) << " = " << v << ";\n";
         }
+      if (L.reduce_op != OOC_RED_NONE)  // fast rows are owned rows (see s_lo / s_hi)
+        for (int r = 0; r < K; ++r)
+          o << ind << "if (own_col) racc = ooc_red(" << L.reduce_op << ", racc, "
+            << outs[static_cast<std::size_t>(r)][static_cast<std::size_t>(L.nwrites)] << ");\n";
     }
     for (int d = 0; d < nd; ++d) {
       const SwDs& D = pl.D[static_cast<std::size_t>(d)];
@@ -706,9 +737,9 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       int tmp = 0;
       std::vector<std::string> outs;
       const ooc_ins* t = L.tape;
-      for (int w = 0; w < L.nwrites; ++w) {
+      for (int w = 0; w < L.nwrites + (L.reduce_op != OOC_RED_NONE ? 1 : 0); ++w) {
         std::vector<std::string> st;
-        for (int k = 0; k < L.write_len[w]; ++k, ++t) {
+        for (int k = 0; k < (w < L.nwrites ? L.write_len[w] : L.reduce_len); ++k, ++t) {
           const ooc_ins& in = *t;
           if (in.op == OOC_OP_CONST) {
             if (cst && !fast) cst->push_back(in.value);
@@ -742,6 +773,9 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       for (int w = 0; w < L.nwrites; ++w)
         o << ind << "      " << at(S.wds[static_cast<std::size_t>(w)], ur, 0, 0) << " = "
           << outs[static_cast<std::size_t>(w)] << ";\n";
+      if (L.reduce_op != OOC_RED_NONE)
+        o << ind << "      if (own_col && row >= r_own0 && row < r_own1) racc = ooc_red(" << L.reduce_op << ", racc, "
+          << outs[static_cast<std::size_t>(L.nwrites)] << ");\n";
       o << ind << "    }\n" << ind << "  }\n" << ind << "}\n";
     }
     // stores of the final rows (each thread stores the elements it wrote: no barrier)
@@ -781,7 +815,17 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     if (D.loaded) o << "    gl" << d << " += " << K << " * p.s0[" << d << "];\n";
     if (D.store) o << "    gs" << d << " += " << K << " * p.s0[" << d << "];\n";
   }
-  o << "  }\n  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n}\n";
+  o << "  }\n  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
+  if (pl.red_op != OOC_RED_NONE) {  // warp tree, then the CTA's warps in order: one partial per CTA
+    o << "#pragma unroll\n  for (int w = 16; w > 0; w >>= 1) racc = ooc_red(" << pl.red_op
+      << ", racc, __shfl_down_sync(0xffffffffu, racc, w));\n";
+    o << "  __shared__ double red_warp[" << pl.NT / 32 << "];\n";
+    o << "  if ((threadIdx.x & 31) == 0) red_warp[threadIdx.x >> 5] = racc;\n  __syncthreads();\n";
+    o << "  if (threadIdx.x == 0) {\n    double b = red_warp[0];\n";
+    o << "    for (int w = 1; w < " << pl.NT / 32 << "; ++w) b = ooc_red(" << pl.red_op << ", b, red_warp[w]);\n";
+    o << "    p.part[static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x] = b;\n  }\n";
+  }
+  o << "}\n";
   return o.str();
 }
 
@@ -961,6 +1005,7 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   double best = -1.0;
   for (long long ns = 1; ns <= std::min<long long>(max_nseg, 4096); ++ns) {
     const long long seg = (rows + ns - 1) / ns, real = (rows + seg - 1) / seg, ctas = strips * real;
+    if (pl.red_op != OOC_RED_NONE && ctas > c->red_part_cap) break;  // one partial per CTA
     const long long waves = (ctas + cap - 1) / cap;
     // wave efficiency, with a mild preference for >= 4 waves (dynamic balance)
     const double overhead = static_cast<double>(pl.warm + pl.lagS_max + pl.P * pl.K);  // rows swept, not stored
@@ -975,10 +1020,19 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   }
   sp->seg_rows = (rows + nseg - 1) / nseg;
   nseg = (rows + sp->seg_rows - 1) / sp->seg_rows;
+  if (pl.red_op != OOC_RED_NONE) {
+    if (strips * nseg > c->red_part_cap) {
+      delete sp;
+      set_error("ooc_launch_sweep: too many CTAs for the reduction partials");
+      return OOC_ERR_UNSUPPORTED;
+    }
+    sp->part = c->red_part[q];
+  }
   c->stats.sweep_launches++;
   void* args[] = {sp};
   const int rc = jit_launch_kernel(c, q, k->fn, static_cast<unsigned>(strips), static_cast<unsigned>(nseg),
                                    static_cast<unsigned>(pl.NT), static_cast<unsigned>(pl.smem), args);
   delete sp;
-  return rc;
+  if (rc != OOC_OK || pl.red_op == OOC_RED_NONE) return rc;
+  return launch_fold(c, q, static_cast<int>(strips * nseg), loops[n - 1].reduce_slot, pl.red_op);
 }

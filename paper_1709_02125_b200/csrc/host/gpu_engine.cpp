@@ -1142,7 +1142,7 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
         const std::size_t b = run.b;
         ++next_sweep;
         flush_group(OOC_Q_COMPUTE);
-        run_sweep(mesh, chain, run, lowered_store, flipped);
+        run_sweep(mesh, chain, run, lowered_store, flipped, out.reduction_slot);
         j = b - 1;
         continue;
       }
@@ -1224,7 +1224,8 @@ std::string sweep_key(const Mesh& mesh, const LoopChain& chain) {
 }
 
 void GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run,
-                          const std::vector<LoweredLoop>& lowered, std::vector<DatasetId>& flipped) {
+                          const std::vector<LoweredLoop>& lowered, std::vector<DatasetId>& flipped,
+                          const std::map<int, int>& red_slots) {
   std::vector<ooc_loop> calls;
   std::vector<const ParLoop*> loops;
   std::vector<index_t> bytes;
@@ -1235,7 +1236,8 @@ void GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& ru
       const Resident& r = res_[static_cast<std::size_t>(x.dataset)];
       v.push_back(view_at(r.dev, mesh[x.dataset].alloc(), r.layout.stride));
     }
-    calls.push_back(make_call(lowered[j], l.range, v, 0));
+    auto rs = red_slots.find(l.id);
+    calls.push_back(make_call(lowered[j], l.range, v, rs == red_slots.end() ? 0 : rs->second));
     loops.push_back(&l);
     bytes.push_back(l.range.size() * loop_bytes_per_point_views(l));
   }

@@ -153,7 +153,7 @@ class GpuEngine {
   void issue_instrumented(int queue, const std::vector<const ParLoop*>& loops, const std::vector<index_t>& bytes,
                           const std::function<void()>& issue);
   void run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run, const std::vector<LoweredLoop>& lowered,
-                 std::vector<DatasetId>& flipped);
+                 std::vector<DatasetId>& flipped, const std::map<int, int>& red_slots);
   index_t loop_bytes_per_point_views(const ParLoop& loop) const;
   void ensure_pool(index_t elems);
   void ensure_resident(Mesh& mesh, DatasetId d);

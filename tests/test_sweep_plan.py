@@ -24,7 +24,7 @@ def test_miniflow2d_timesteps_fuse_into_sweeps(jit_always):
     groups = [g for c in chains for g in rt.chain_sweep_check(c, compile=True)]
     assert groups and all(g["ok"] for g in groups)
     covered = sum(g["loops"] for g in groups)
-    assert covered == 140  # 10 iterations x 14 loops: every loop except the fieldsum
+    assert covered == 141  # 10 iterations x 14 loops + the fieldsum (folded into the last run)
     assert max(g["loops"] for g in groups) >= 14  # at least one whole timestep per launch
     for g in groups:
         pl = g["plan"]
@@ -43,7 +43,7 @@ def test_miniflow2d_timesteps_fuse_into_sweeps(jit_always):
     assert sum(d["oop"] for d in first) == 3
 
 
-def test_reductions_and_3d_are_not_swept(jit_always):
+def test_3d_chains_are_not_swept(jit_always):
     rt, chains = _chains(P.app_program("miniflow3d", 12, 10, 8, iters=3))
     for c in chains:
         assert rt.chain_sweep_check(c, compile=False) == []
