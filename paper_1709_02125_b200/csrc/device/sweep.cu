@@ -64,7 +64,15 @@ using namespace oocdev;
 
 namespace {
 
-constexpr int kRC = 128;  // ring row width in columns (TC owned + 2*HC halo)
+// ring row width in columns (TC owned + 2*HC halo) = threads per CTA; OOC_SWEEP_RC
+int ring_cols() {
+  static int rc = [] {
+    const char* e = std::getenv("OOC_SWEEP_RC");
+    const int v = e ? std::atoi(e) : 256;  // measured: 256 > 128 (+3 %) > 64
+    return v == 64 || v == 128 || v == 256 ? v : 256;
+  }();
+  return rc;
+}
 constexpr int kPad = 16;  // doubles of shared memory before/after the rings (edge lanes' neighbour reads)
 
 // Parameter block; the kernel source declares an identical struct.
@@ -128,7 +136,7 @@ struct SwDs {
 };
 
 struct SwPlan {
-  int n = 0, K = 2, P = 2, NT = 256;
+  int n = 0, K = 2, P = 2, NT = 256, RC = 128;
   long long HC = 0, TC = 0, warm = 0, lagS_max = 0, smem = 0;
   int red_op = OOC_RED_NONE;  // the run's last loop reduces (no writes): folded per CTA
   long long red_lag = 0;
@@ -140,7 +148,8 @@ struct SwPlan {
 long long smem_budget() {
   static long long b = [] {
     const char* e = std::getenv("OOC_SWEEP_SMEM");
-    return e ? std::atoll(e) : 56LL * 1024;  // measured: occupancy beats fewer DRAM passes
+    // measured: occupancy beats fewer DRAM passes (56 KB per 128 ring columns)
+    return e ? std::atoll(e) : 56LL * 1024 * ring_cols() / 128;
   }();
   return b;
 }
@@ -158,7 +167,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   pl.n = n;
   pl.K = K;
   pl.P = P;
-  pl.NT = kRC;
+  pl.NT = pl.RC = ring_cols();
   if (n < 1 || n > SW_MAXL) return fail(why, "group size");
   pl.L.resize(static_cast<std::size_t>(n));
   int ncst = 0;
@@ -236,9 +245,9 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
     HC = std::max(HC, S.h);
     for (const auto& [d, r] : S.rd) HC = std::max(HC, S.h + r.oc);
   }
-  if (HC > 16) return fail(why, "column halo");
+  if (HC > 16 || 2 * HC >= pl.RC / 2) return fail(why, "column halo");
   pl.HC = HC;
-  pl.TC = kRC - 2 * HC;
+  pl.TC = pl.RC - 2 * HC;
   // ---- loaded / written / out-of-place
   for (int d = 0; d < nd; ++d) {
     SwDs& D = pl.D[static_cast<std::size_t>(d)];
@@ -315,7 +324,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
     D.W = 1;
     while (D.W < std::max<long long>(A + B + 1, K)) D.W *= 2;  // power of two: slot = row & (W-1)
     D.off = off;
-    off += D.W * kRC;
+    off += D.W * pl.RC;
   }
   pl.smem = (off + 2 * kPad) * 8;
   if (pl.smem > smem_budget()) return fail(why, "shared memory");
@@ -457,7 +466,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // owned column inside the launch box — the fast steps then evaluate every loop on
   // every lane without predicates (lanes outside a loop's halo produce values nobody
   // reads; their neighbour reads stay inside the padded shared-memory window)
-  o << "  const long long cl = c0 - " << pl.HC << ", ch = cl + " << kRC << ";\n";
+  o << "  const long long cl = c0 - " << pl.HC << ", ch = cl + " << pl.RC << ";\n";
   o << "  bool strip_in = c0 + " << pl.TC << " <= p.C1;\n";
   for (int i = 0; i < pl.n; ++i)
     o << "  strip_in = strip_in && p.rng[" << i << "][2] <= cl && p.rng[" << i << "][3] >= ch;\n";
@@ -480,7 +489,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   auto at = [&](int d, const std::string& u, long long q, long long oc) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     std::ostringstream e;
-    e << "B[" << D.off << " + (((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << kRC;
+    e << "B[" << D.off << " + (((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RC;
     if (oc) e << " + (" << oc << ")";
     e << "]";
     return e.str();
