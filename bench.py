@@ -409,6 +409,7 @@ def main():
         "kernels": {k: {"launches": v["launches"], "GBps": round(v["bytes"] / v["seconds"] / 1e9),
                         "share": round(v["seconds"] / total_k, 3)} for k, v in sorted(kinds.items())},
         "tile_shapes": B.jit_report(),
+        "sweep_tuning": B.sweep_report(),
         "jit_compile_ms": inc["device"].get("jit_compile_ms"),
         "gpu_launches": inc["launches"],
         "clocks": inc["clocks"],

@@ -202,6 +202,8 @@ int ooc_launch_sweep(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n, cons
 /* JSON description of the sweep plan (lags, halos, rings); compile = 1 also builds the
  * kernel with NVRTC for sm_100a (no GPU needed). */
 int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int len, int compile);
+/* JSON: the prefetch depth chosen per sweep structure and the measured ms per candidate. */
+int ooc_sweep_report(char* buf, int len);
 
 /* Specialised kernels: the par_loop kernel template instantiated per loop body
  * (or fused group) with NVRTC at first use, cached per process. mode 0: never

@@ -437,6 +437,15 @@ def jit_report():
     return json.loads(buf.value.decode())
 
 
+def sweep_report():
+    """Prefetch depth autotuned per row-sweep structure (ooc_sweep_report)."""
+    _native.lib()
+    dev = ctypes.CDLL(_native.device_lib_path())
+    buf = ctypes.create_string_buffer(1 << 16)
+    dev.ooc_sweep_report(buf, 1 << 16)
+    return json.loads(buf.value.decode())
+
+
 def jit_status() -> str:
     _native.lib()
     dev = ctypes.CDLL(_native.device_lib_path())

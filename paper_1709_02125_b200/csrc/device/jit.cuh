@@ -40,6 +40,7 @@ int jit_policy(long long* min_points);  // OOC_JIT mode (0/1/2) and its size thr
 bool jit_available(bool load, std::string& why);
 // acc[slot] = combine(acc[slot], fixed-order fold of the queue's `blocks` partials)
 int launch_fold(ooc_ctx* c, int q, int blocks, int slot, int op);
+extern bool g_frozen;  // graph capture in progress: no tuning launches (ooc_jit_freeze)
 bool jit_build_kernel(const std::string& src, const char* kname, int block, long long smem, void** fn,
                       int* occ, std::string& err, bool load);
 int jit_launch_kernel(ooc_ctx* c, int q, void* fn, unsigned gx, unsigned gy, unsigned block, unsigned smem,

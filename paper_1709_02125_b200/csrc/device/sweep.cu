@@ -855,6 +855,7 @@ int sweep_K() {
   }();
   return k;
 }
+bool sweep_P_forced() { return std::getenv("OOC_SWEEP_P") != nullptr; }
 int sweep_P() {
   static int pp = [] {
     const char* e = std::getenv("OOC_SWEEP_P");
@@ -936,6 +937,39 @@ extern "C" int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int l
   return OOC_OK;
 }
 
+namespace {
+// Prefetch-depth autotuning per sweep structure (the run's kernel source at the default
+// depth): every depth whose rings fit the budget is tried on one real launch, timed with
+// CUDA events, and the fastest is kept — the same scheme as the tile shapes of jit.cu.
+struct SwTune {
+  std::vector<int> cands;
+  std::vector<float> ms;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<char> issued;
+  int best = -1;
+  int loops = 0;
+};
+std::unordered_map<std::string, SwTune> g_sw_tune;
+}  // namespace
+
+extern "C" int ooc_sweep_report(char* buf, int len) {
+  std::lock_guard<std::mutex> lk(g_sw_mu);
+  std::ostringstream o;
+  o << "[";
+  bool first = true;
+  for (const auto& [key, T] : g_sw_tune) {
+    o << (first ? "" : ",") << "{\"loops\":" << T.loops << ",\"key\":\"" << std::hex
+      << std::hash<std::string>{}(key) << std::dec << "\",\"P\":" << (T.best >= 0 ? T.cands[static_cast<std::size_t>(T.best)] : -1)
+      << ",\"ms\":{";
+    for (std::size_t i = 0; i < T.cands.size(); ++i) o << (i ? "," : "") << "\"" << T.cands[i] << "\":" << T.ms[i];
+    o << "}}";
+    first = false;
+  }
+  o << "]";
+  std::snprintf(buf, static_cast<size_t>(len), "%s", o.str().c_str());
+  return OOC_OK;
+}
+
 extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n, const ooc_redirect* red,
                                 int nred) {
   OOC_ARG_CHECK(c && loops && n > 0 && q >= 0 && q < OOC_NUM_QUEUES, "ooc_launch_sweep: bad args");
@@ -947,6 +981,56 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   if (!analyze(loops, n, sweep_K(), sweep_P(), pl, &why, &dead)) {
     set_error("ooc_launch_sweep: group not sweepable: " + why);
     return OOC_ERR_UNSUPPORTED;
+  }
+  // ---- prefetch depth: forced (OOC_SWEEP_P), tuned, or being tuned on this launch
+  SwTune* tune = nullptr;
+  int pick = -1;
+  bool timing = false;
+  if (!sweep_P_forced()) {
+    std::lock_guard<std::mutex> lk(g_sw_mu);
+    tune = &g_sw_tune[generate(loops, pl, nullptr)];
+    SwTune& T = *tune;
+    if (T.cands.empty()) {
+      T.loops = n;
+      for (int P = 1; P <= 4; ++P) {
+        SwPlan tp;
+        if (analyze(loops, n, sweep_K(), P, tp, nullptr, &dead)) T.cands.push_back(P);
+      }
+      T.ms.assign(T.cands.size(), -1.f);
+      T.ev.assign(T.cands.size(), {nullptr, nullptr});
+      T.issued.assign(T.cands.size(), 0);
+      if (T.cands.size() <= 1) T.best = 0;
+    }
+    if (T.best < 0) {  // resolve finished timings without blocking
+      bool all = true;
+      for (std::size_t i = 0; i < T.cands.size(); ++i) {
+        if (T.ms[i] < 0 && T.issued[i] && cudaEventQuery(T.ev[i].second) == cudaSuccess)
+          cudaEventElapsedTime(&T.ms[i], T.ev[i].first, T.ev[i].second);
+        all = all && T.ms[i] >= 0;
+      }
+      if (all) {
+        T.best = 0;
+        for (std::size_t i = 1; i < T.ms.size(); ++i)
+          if (T.ms[i] < T.ms[static_cast<std::size_t>(T.best)]) T.best = static_cast<int>(i);
+      }
+    }
+    if (T.best >= 0) {
+      pick = T.best;
+    } else {
+      c->stats.jit_unsettled++;
+      for (std::size_t i = 0; i < T.cands.size() && pick < 0 && !g_frozen; ++i)
+        if (!T.issued[i]) pick = static_cast<int>(i);
+      timing = pick >= 0;
+      if (pick < 0)  // frozen for a graph capture, or all in flight: fastest measured so far
+        for (std::size_t i = 0; i < T.cands.size(); ++i)
+          if (T.ms[i] >= 0 && (pick < 0 || T.ms[i] < T.ms[static_cast<std::size_t>(pick)])) pick = static_cast<int>(i);
+    }
+    if (pick >= 0 && T.cands[static_cast<std::size_t>(pick)] != pl.P) {
+      if (!analyze(loops, n, sweep_K(), T.cands[static_cast<std::size_t>(pick)], pl, &why, &dead)) {
+        set_error("ooc_launch_sweep: tuned plan failed: " + why);
+        return OOC_ERR_UNSUPPORTED;
+      }
+    }
   }
   auto* sp = new SweepParams;
   std::memset(sp, 0, sizeof *sp);
@@ -1039,8 +1123,20 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   }
   c->stats.sweep_launches++;
   void* args[] = {sp};
+  if (timing) {
+    auto& e = tune->ev[static_cast<std::size_t>(pick)];
+    if (!e.first) {
+      cudaEventCreate(&e.first);
+      cudaEventCreate(&e.second);
+    }
+    cudaEventRecord(e.first, c->q[q]);
+  }
   const int rc = jit_launch_kernel(c, q, k->fn, static_cast<unsigned>(strips), static_cast<unsigned>(nseg),
                                    static_cast<unsigned>(pl.NT), static_cast<unsigned>(pl.smem), args);
+  if (timing) {
+    cudaEventRecord(tune->ev[static_cast<std::size_t>(pick)].second, c->q[q]);
+    tune->issued[static_cast<std::size_t>(pick)] = 1;
+  }
   delete sp;
   if (rc != OOC_OK || pl.red_op == OOC_RED_NONE) return rc;
   return launch_fold(c, q, static_cast<int>(strips * nseg), loops[n - 1].reduce_slot, pl.red_op);
