@@ -421,6 +421,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   o << "  extern __shared__ __align__(16) double sw_sm[];\n";
   o << "  const int lc = threadIdx.x;\n";
   o << "  double* const B = sw_sm + " << kPad << " + lc;\n";
+  // one restrict-qualified base per ring: rings never overlap, so the compiler may move
+  // a ring's loads across another ring's stores (instruction-level parallelism)
+  static const bool restrict_rings = !(std::getenv("OOC_SWEEP_RESTRICT") && std::atoi(std::getenv("OOC_SWEEP_RESTRICT")) == 0);
+  for (int d = 0; d < nd; ++d)
+    o << "  double* " << (restrict_rings ? "__restrict__ " : "") << "const R" << d << " = B + " << pl.D[static_cast<std::size_t>(d)].off << ";\n";
   o << "  const long long c0 = p.C0 + static_cast<long long>(blockIdx.x) * " << pl.TC << ";\n";
   o << "  const long long r_own0 = p.R0 + static_cast<long long>(blockIdx.y) * p.seg_rows;\n";
   o << "  const long long r_own1 = min(p.R1, r_own0 + p.seg_rows);\n";
@@ -489,7 +494,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   auto at = [&](int d, const std::string& u, long long q, long long oc) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     std::ostringstream e;
-    e << "B[" << D.off << " + (((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RC;
+    e << "R" << d << "[(((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RC;
     if (oc) e << " + (" << oc << ")";
     e << "]";
     return e.str();
