@@ -962,7 +962,10 @@ extern "C" int ooc_sweep_report(char* buf, int len) {
   std::ostringstream o;
   o << "[";
   bool first = true;
-  for (const auto& [key, T] : g_sw_tune) {
+  for (auto& [key, T] : g_sw_tune) {
+    for (std::size_t i = 0; i < T.cands.size(); ++i)  // timings that finished since the last launch
+      if (T.ms[i] < 0 && T.issued[i] && cudaEventQuery(T.ev[i].second) == cudaSuccess)
+        cudaEventElapsedTime(&T.ms[i], T.ev[i].first, T.ev[i].second);
     o << (first ? "" : ",") << "{\"loops\":" << T.loops << ",\"key\":\"" << std::hex
       << std::hash<std::string>{}(key) << std::dec << "\",\"P\":" << (T.best >= 0 ? T.cands[static_cast<std::size_t>(T.best)] : -1)
       << ",\"ms\":{";

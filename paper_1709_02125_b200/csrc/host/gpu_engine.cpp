@@ -1142,9 +1142,11 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
         const std::size_t b = run.b;
         ++next_sweep;
         flush_group(OOC_Q_COMPUTE);
-        run_sweep(mesh, chain, run, lowered_store, flipped, out.reduction_slot);
-        j = b - 1;
-        continue;
+        if (run_sweep(mesh, chain, run, lowered_store, flipped, out.reduction_slot)) {
+          j = b - 1;
+          continue;
+        }
+        // no HBM left for a shadow buffer: this run's loops go through the fused launches
       }
       const ParLoop& l = chain.loops[j];
       const Extent sub = plan ? plan->subrange(static_cast<int>(j), t) : l.range;
@@ -1223,7 +1225,7 @@ std::string sweep_key(const Mesh& mesh, const LoopChain& chain) {
   return k;
 }
 
-void GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run,
+bool GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run,
                           const std::vector<LoweredLoop>& lowered, std::vector<DatasetId>& flipped,
                           const std::map<int, int>& red_slots) {
   std::vector<ooc_loop> calls;
@@ -1259,11 +1261,7 @@ void GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& ru
     if (!r.shadow) {
       void* p = nullptr;
       int rc = ooc_mem_alloc(ctx_, static_cast<std::size_t>(r.layout.elems) * sizeof(double), &p);
-      if (rc == OOC_ERR_CAPACITY) {
-        long long in_use = 0;
-        ooc_mem_usage(ctx_, &in_use, nullptr);
-        throw CapacityError(in_use + r.layout.elems * 8, props_.hbm_bytes);
-      }
+      if (rc == OOC_ERR_CAPACITY) return false;  // caller falls back to the fused launches
       DEV(rc);
       r.shadow = static_cast<double*>(p);
     }
@@ -1280,6 +1278,7 @@ void GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& ru
     if (it == flipped.end()) flipped.push_back(d);
     else flipped.erase(it);
   }
+  return true;
 }
 
 std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan, bool pointers) const {

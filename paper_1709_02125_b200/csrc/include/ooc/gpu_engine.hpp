@@ -152,7 +152,8 @@ class GpuEngine {
   void flush_group(int queue);
   void issue_instrumented(int queue, const std::vector<const ParLoop*>& loops, const std::vector<index_t>& bytes,
                           const std::function<void()>& issue);
-  void run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run, const std::vector<LoweredLoop>& lowered,
+  /// One row-sweep launch; false (nothing launched) when HBM has no room for a shadow.
+  bool run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& run, const std::vector<LoweredLoop>& lowered,
                  std::vector<DatasetId>& flipped, const std::map<int, int>& red_slots);
   index_t loop_bytes_per_point_views(const ParLoop& loop) const;
   void ensure_pool(index_t elems);

@@ -32,5 +32,14 @@ for seed in range(30):
     want.pop("_rt", None)
     if compare(want, got, check_audit=False, check_totals=False):
         bad.append(("random", seed))
+for seed in range(12):  # larger meshes: interior strips take the fast steps
+    prog = P.random_program(seed, max_loops=12, min_size=300, max_size=700, allow_3d=False, flushes=True)
+    want = oracle_record(prog, "reference")
+    got = product_record(prog, "resident")
+    rt = got.pop("_rt")
+    swept += rt.device()["sweep_launches"]
+    want.pop("_rt", None)
+    if compare(want, got, check_audit=False, check_totals=False):
+        bad.append(("large random", seed))
 print("sweeps", swept, "BAD", bad)
 sys.exit(1 if bad or swept == 0 else 0)

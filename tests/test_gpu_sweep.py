@@ -67,6 +67,26 @@ def test_sweep_random_programs_vs_golden(golden_random, jit_always):
     assert swept > 0
 
 
+def test_sweep_large_random_programs(jit_always):
+    """Random 2-D chains on 300-700 point meshes (partial ranges, read-write loops, mixed
+    stencils, flushes, reductions): enough rows and columns for interior strips, so the
+    predicate-free fast steps, register forwarding and carries run against the oracle."""
+    bad, swept = [], 0
+    for seed in range(40):
+        prog = P.random_program(seed, max_loops=12, min_size=300, max_size=700, allow_3d=False, flushes=True)
+        want = oracle_record(prog, "reference")
+        got = product_record(prog, "resident")
+        rt = got.pop("_rt", None)
+        want.pop("_rt", None)
+        if rt is not None:
+            swept += rt.device()["sweep_launches"]
+        diff = compare(want, got, check_audit=False, check_totals=False)
+        if diff:
+            bad.append((seed, diff))
+    assert not bad, bad[:5]
+    assert swept > 0
+
+
 def test_sweep_graph_replay_flips(jit_always):
     """Captured chains replay with the recorded buffer swaps: 112 iterations (an odd number
     of swaps per chain, so consecutive chains alternate between two graphs) stay
@@ -93,13 +113,14 @@ def test_sweep_fetch_between_chains(jit_always):
     assert rt.device()["sweep_launches"] > 0
 
 
-@pytest.mark.parametrize("K,P_,smem", [("1", "1", "60000"), ("4", "2", "200000"), ("2", "3", "40000"),
-                                       ("8", "1", "220000")])
-def test_sweep_variants(K, P_, smem):
-    """Rows per step K, prefetch depth P and the shared-memory budget (which sets how
-    many loops one sweep spans) change the schedule, never the bits (child process:
-    read once per process)."""
-    env = dict(os.environ, OOC_SWEEP_K=K, OOC_SWEEP_P=P_, OOC_SWEEP_SMEM=smem)
+@pytest.mark.parametrize("K,P_,smem,rc", [("1", "1", "60000", "128"), ("4", "2", "200000", "256"),
+                                          ("2", "3", "40000", "64"), ("8", "1", "220000", "128"),
+                                          ("1", "2", "30000", "64")])
+def test_sweep_variants(K, P_, smem, rc):
+    """Rows per step K, prefetch depth P, ring width and the shared-memory budget (which
+    sets how many loops one sweep spans) change the schedule, never the bits (child
+    process: read once per process)."""
+    env = dict(os.environ, OOC_SWEEP_K=K, OOC_SWEEP_P=P_, OOC_SWEEP_SMEM=smem, OOC_SWEEP_RC=rc)
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "sweep_parity_child.py")],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
