@@ -381,7 +381,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference closed-form fills, proj/src/apps.cpp:61-67)",
         "config": {"workload": f"miniflow2d {n}x{n} fp64 in-core (CloverLeaf-2D analogue, "
-                               "BASELINE configs[1], untiled)",
+                               "BASELINE configs[1]; tiled on chip: one row-sweep launch per timestep)",
                    "step": f"one chain = {ITERS_PER_STEP} iterations, 141 par_loops",
                    "problem_bytes": B.problem_bytes("miniflow2d", n, n),
                    "l2": "inputs (18.9 GB) >> L2 (126 MB); no flush needed",

@@ -167,6 +167,8 @@ const char* ooc_rt_chain_sweep_check(ooc_runtime* rt, int chain, int compile);
  * row-recompute groups (neighbour reads along the row dimension of values written
  * earlier in the launch, re-evaluated in-thread). */
 void ooc_rt_set_row_recompute(int on);
+/* Process-wide: row-sweep kernels for resident untiled 2-D chains (default on; OOC_SWEEP=0). */
+void ooc_rt_set_sweep(int on);
 /* dependency_oracle over recorded chain `chain` planned with `tiles`. */
 const char* ooc_rt_chain_oracle_json(ooc_runtime* rt, int chain, int tiles);
 

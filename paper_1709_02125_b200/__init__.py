@@ -423,6 +423,11 @@ def set_jit(mode: int, min_points: int = -1) -> None:
         raise OocError("ooc_jit_config failed")
 
 
+def set_sweep(on: bool) -> None:
+    """Process-wide: row-sweep kernels for resident untiled 2-D chains (ooc_rt_set_sweep)."""
+    _native.lib().ooc_rt_set_sweep(int(bool(on)))
+
+
 def set_row_recompute(on: bool) -> None:
     """Process-wide fusion policy (ooc_rt_set_row_recompute)."""
     _native.lib().ooc_rt_set_row_recompute(int(bool(on)))

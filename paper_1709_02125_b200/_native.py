@@ -85,6 +85,7 @@ def lib():
         "ooc_rt_report_csv": (cp, [vp, cp, cp, ctypes.c_int]),
         "ooc_rt_loops_csv": (cp, [vp]),
         "ooc_rt_set_row_recompute": (None, [i]),
+        "ooc_rt_set_sweep": (None, [i]),
         "ooc_rt_audit_csv": (cp, [vp]),
         "ooc_rt_timeline_csv": (cp, [vp]),
         "ooc_rt_chain_timings_json": (cp, [vp]),

@@ -333,6 +333,7 @@ const char* ooc_rt_audit_json(ooc_runtime* h) {
 }
 
 void ooc_rt_set_row_recompute(int on) { ooc::set_row_recompute(on != 0); }
+void ooc_rt_set_sweep(int on) { ooc::set_sweep(on != 0); }
 
 const char* ooc_rt_report_csv(ooc_runtime* h, const char* app, const char* size, int iters) {
   std::string s;

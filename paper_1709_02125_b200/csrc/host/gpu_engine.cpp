@@ -506,13 +506,17 @@ std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& 
   return out;
 }
 
-bool sweep_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("OOC_SWEEP");
-    return !(e && std::atoi(e) == 0);
-  }();
-  return on;
+namespace {
+int g_sweep = -1;  // -1: from the environment (OOC_SWEEP=0 disables)
 }
+bool sweep_enabled() {
+  if (g_sweep < 0) {
+    const char* e = std::getenv("OOC_SWEEP");
+    g_sweep = !(e && std::atoi(e) == 0);
+  }
+  return g_sweep != 0;
+}
+void set_sweep(bool on) { g_sweep = on ? 1 : 0; }
 
 void GpuEngine::launch(int queue, bool group_start, int tile, const ParLoop& loop,
                        const LoweredLoop& lw, const Extent& sub,

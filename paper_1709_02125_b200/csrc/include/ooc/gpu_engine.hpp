@@ -64,6 +64,7 @@ std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& 
                                   const std::vector<ooc_loop>& calls);
 std::string sweep_key(const Mesh& mesh, const LoopChain& chain);
 bool sweep_enabled();  // OOC_SWEEP=0 disables
+void set_sweep(bool on);  // process-wide override
 
 class GpuEngine {
  public:

@@ -55,10 +55,16 @@ CYCLIC = [False]
 def main():
     which = sys.argv[1:] or ["2", "3", "4", "5"]
     lines = []
-    if "2" in which:  # in-core, untiled vs L2-tiled
-        lines.append(dict(config=2, mode="in-core untiled", **run("miniflow2d", "resident")))
-        lines.append(dict(config=2, mode="in-core L2-tiled (slot <= 96 MB)",
+    if "2" in which:  # in-core, tiled vs untiled
+        # tiled on chip: row sweeps (CTA segments are skewed tiles of whole timesteps)
+        lines.append(dict(config=2, mode="in-core tiled: row sweeps through shared memory",
+                          **run("miniflow2d", "resident")))
+        B.set_sweep(False)  # untiled: every loop group sweeps the whole mesh through HBM
+        lines.append(dict(config=2, mode="in-core untiled: fused loop-group launches",
+                          **run("miniflow2d", "resident")))
+        lines.append(dict(config=2, mode="in-core tiled through L2: reference skew tiles (slot <= 96 MB)",
                           **run("miniflow2d", "resident", resident_budget=96 << 20, steps=1, warmup=1)))
+        B.set_sweep(True)
     for cfg, app, cyc in (("3", "miniflow2d", False), ("3", "miniflow2d", True),
                           ("4", "miniflow3d", True), ("5", "rk3chain3d", False)):
         if cfg not in which:
