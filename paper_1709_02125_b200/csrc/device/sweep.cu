@@ -47,6 +47,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -592,14 +593,22 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   using Key = std::tuple<int, long long, long long>;
   struct FastInfo {
     std::vector<Key> first_lds;     // keys whose first access in the step loaded the ring
+    std::vector<Key> first_read;    // keys whose first access in the step is a read
+    std::vector<char> miss;         // per dataset: some fast-step value came from its ring
     std::map<Key, std::string> end; // register of each cached key at the end of the step
   };
   std::vector<std::pair<Key, std::string>> carries;  // (key at step start, register name)
+  // datasets whose fast steps never read their ring (every value forwarded or carried):
+  // their fast-step writes skip the shared-memory store, and the last fast step spills
+  // the carries so the predicated steps after it find the rows in the ring
+  std::vector<char> no_smem(static_cast<std::size_t>(nd), 0);
   auto fast_body = [&](FastInfo* info) {
     const char* ind = "      ";
     loads("s + " + std::to_string(pl.P), ind, true, true);
     o << ind << "const int u = s * " << K << ";\n";
     std::map<std::tuple<int, long long, long long>, std::string> cache;  // (d, row, col) -> register
+    std::set<Key> touched;
+    if (info) info->miss.assign(static_cast<std::size_t>(nd), 0);
     if (!carries.empty()) {
       o << ind << "if (!prev_fast) {\n";
       for (const auto& [k, name] : carries)
@@ -636,12 +645,14 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
             } else if (in.op == OOC_OP_READ) {
               const int d = dsof_arg[in.arg];
               const auto key = std::make_tuple(d, q0 + in.offset[0], static_cast<long long>(in.offset[1]));
+              if (info && touched.insert(key).second && in.offset[1] == 0) info->first_read.push_back(key);
               auto it = forward ? cache.find(key) : cache.end();
               if (it == cache.end()) {
                 const std::string name = pre + std::to_string(tmp++);
                 o << ind << "const double " << name << " = " << at(d, "u", q0 + in.offset[0], in.offset[1]) << ";\n";
                 it = cache.emplace(key, name).first;
                 if (info && in.offset[1] == 0) info->first_lds.push_back(key);
+                if (info) info->miss[static_cast<std::size_t>(d)] = 1;
               }
               st.push_back(it->second);
             } else {
@@ -676,7 +687,8 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
             it = std::get<0>(it->first) == d && (std::get<1>(it->first) == q || std::get<2>(it->first) != 0)
                      ? cache.erase(it) : std::next(it);
           cache[std::make_tuple(d, q, 0LL)] = v;
-          if (need_sts[static_cast<std::size_t>(i)][static_cast<std::size_t>(d)])
+          touched.insert(std::make_tuple(d, q, 0LL));
+          if (need_sts[static_cast<std::size_t>(i)][static_cast<std::size_t>(d)] && !no_smem[static_cast<std::size_t>(d)])
             o << ind << at(d, "u", q, 0) << " = " << v << ";\n";
         }
       if (L.reduce_op != OOC_RED_NONE)  // fast rows are owned rows (see s_lo / s_hi)
@@ -694,6 +706,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
                           pl.L[static_cast<std::size_t>(last_writer[static_cast<std::size_t>(d)])].lag == D.lagS
                       ? cache.find(std::make_tuple(d, static_cast<long long>(r) - D.lagS, 0LL))
                       : cache.end();
+        if (it == cache.end() && info) info->miss[static_cast<std::size_t>(d)] = 1;
         const std::string v = it != cache.end() ? it->second : at(d, "u", r - D.lagS, 0);
         o << ind << "  p.dst[" << ds << "][gs" << ds << " + " << r << " * p.s0[" << ds << "]] = " << v << ";\n";
       }
@@ -705,17 +718,39 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       o << ind << "const double n" << name << " = " << it->second << ";\n";
     }
     for (const auto& [k, name] : carries) o << ind << name << " = n" << name << ";\n";
+    bool spill = false;
+    for (const auto& [k, name] : carries) spill = spill || no_smem[static_cast<std::size_t>(std::get<0>(k))];
+    if (spill) {  // the next step is predicated: it reads these rows from the rings
+      o << ind << "if (s + 1 == s_hi) {\n";
+      for (const auto& [k, name] : carries)
+        if (no_smem[static_cast<std::size_t>(std::get<0>(k))])
+          o << ind << "  " << at(std::get<0>(k), "u + " + std::to_string(K), std::get<1>(k), 0) << " = " << name << ";\n";
+      o << ind << "}\n";
+    }
     o << ind << "prev_fast = true;\n";
   };
-  if (forward) {  // pass 1 (discarded): which loads could be carries
+  static const bool skip_stores = !(std::getenv("OOC_SWEEP_NOSMEM") && std::atoi(std::getenv("OOC_SWEEP_NOSMEM")) == 0);
+  if (forward) {  // discarded passes: carries to a fixpoint (a carried key stays cached, so
+                  // it can feed the next step's carry), then the ring-free datasets
     FastInfo info;
-    std::ostringstream keep;
-    std::swap(o, keep);
-    fast_body(&info);
-    std::swap(o, keep);
-    for (const Key& k : info.first_lds)
-      if (info.end.count(std::make_tuple(std::get<0>(k), std::get<1>(k) + K, 0LL)))
-        carries.push_back({k, "cr" + std::to_string(carries.size())});
+    for (int iter = 0; iter < 8; ++iter) {
+      info = FastInfo{};
+      std::ostringstream keep;
+      std::swap(o, keep);
+      fast_body(&info);
+      std::swap(o, keep);
+      std::vector<Key> next;
+      for (const Key& k : info.first_read)
+        if (info.end.count(std::make_tuple(std::get<0>(k), std::get<1>(k) + K, 0LL))) next.push_back(k);
+      std::vector<Key> cur;
+      for (const auto& [k, name] : carries) cur.push_back(k);
+      if (next == cur) break;
+      carries.clear();
+      for (const Key& k : next) carries.push_back({k, "cr" + std::to_string(carries.size())});
+    }
+    if (skip_stores)
+      for (int d = 0; d < nd; ++d)
+        no_smem[static_cast<std::size_t>(d)] = pl.D[static_cast<std::size_t>(d)].written && !info.miss[static_cast<std::size_t>(d)];
   }
   for (const auto& [k, name] : carries) o << "  double " << name << " = 0.0;\n";
   o << "  bool prev_fast = false;\n";
