@@ -1003,9 +1003,9 @@ extern "C" int ooc_sweep_report(char* buf, int len) {
         cudaEventElapsedTime(&T.ms[i], T.ev[i].first, T.ev[i].second);
     o << (first ? "" : ",") << "{\"loops\":" << T.loops << ",\"key\":\"" << std::hex
       << std::hash<std::string>{}(key) << std::dec << "\",\"P\":" << (T.best >= 0 ? T.cands[static_cast<std::size_t>(T.best)] : -1)
-      << ",\"ms\":{";
-    for (std::size_t i = 0; i < T.cands.size(); ++i) o << (i ? "," : "") << "\"" << T.cands[i] << "\":" << T.ms[i];
-    o << "}}";
+      << ",\"ms\":[";
+    for (std::size_t i = 0; i < T.cands.size(); ++i) o << (i ? "," : "") << "[" << T.cands[i] << "," << T.ms[i] << "]";
+    o << "]}";
     first = false;
   }
   o << "]";
@@ -1035,10 +1035,11 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
     SwTune& T = *tune;
     if (T.cands.empty()) {
       T.loops = n;
-      for (int P = 1; P <= 4; ++P) {
-        SwPlan tp;
-        if (analyze(loops, n, sweep_K(), P, tp, nullptr, &dead)) T.cands.push_back(P);
-      }
+      for (int round = 0; round < 2; ++round)  // two timed launches per depth: the faster counts
+        for (int P = 1; P <= 4; ++P) {
+          SwPlan tp;
+          if (analyze(loops, n, sweep_K(), P, tp, nullptr, &dead)) T.cands.push_back(P);
+        }
       T.ms.assign(T.cands.size(), -1.f);
       T.ev.assign(T.cands.size(), {nullptr, nullptr});
       T.issued.assign(T.cands.size(), 0);
