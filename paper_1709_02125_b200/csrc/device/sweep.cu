@@ -998,9 +998,17 @@ extern "C" int ooc_sweep_report(char* buf, int len) {
   o << "[";
   bool first = true;
   for (auto& [key, T] : g_sw_tune) {
-    for (std::size_t i = 0; i < T.cands.size(); ++i)  // timings that finished since the last launch
+    bool all = !T.cands.empty();
+    for (std::size_t i = 0; i < T.cands.size(); ++i) {  // timings that finished since the last launch
       if (T.ms[i] < 0 && T.issued[i] && cudaEventQuery(T.ev[i].second) == cudaSuccess)
         cudaEventElapsedTime(&T.ms[i], T.ev[i].first, T.ev[i].second);
+      all = all && T.ms[i] >= 0;
+    }
+    if (T.best < 0 && all) {
+      T.best = 0;
+      for (std::size_t i = 1; i < T.ms.size(); ++i)
+        if (T.ms[i] < T.ms[static_cast<std::size_t>(T.best)]) T.best = static_cast<int>(i);
+    }
     o << (first ? "" : ",") << "{\"loops\":" << T.loops << ",\"key\":\"" << std::hex
       << std::hash<std::string>{}(key) << std::dec << "\",\"P\":" << (T.best >= 0 ? T.cands[static_cast<std::size_t>(T.best)] : -1)
       << ",\"ms\":[";
