@@ -592,7 +592,6 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // after a slow step the carries are reloaded from the rings.
   using Key = std::tuple<int, long long, long long>;
   struct FastInfo {
-    std::vector<Key> first_lds;     // keys whose first access in the step loaded the ring
     std::vector<Key> first_read;    // keys whose first access in the step is a read
     std::vector<char> miss;         // per dataset: some fast-step value came from its ring
     std::map<Key, std::string> end; // register of each cached key at the end of the step
@@ -651,7 +650,6 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
                 const std::string name = pre + std::to_string(tmp++);
                 o << ind << "const double " << name << " = " << at(d, "u", q0 + in.offset[0], in.offset[1]) << ";\n";
                 it = cache.emplace(key, name).first;
-                if (info && in.offset[1] == 0) info->first_lds.push_back(key);
                 if (info) info->miss[static_cast<std::size_t>(d)] = 1;
               }
               st.push_back(it->second);
