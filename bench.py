@@ -421,6 +421,10 @@ def main():
         line["e2e"] = {"value": e2e_val, "unit": UNIT,
                        "h2d_bytes_per_step": e2e["uploaded"] // args.steps,
                        "d2h_bytes_per_step": e2e["downloaded"] // args.steps,
+                       # physical DMA bytes (uploads are whole allocation rows: a few halo
+                       # columns more than the reference's audited boxes, one contiguous DMA)
+                       "dma_h2d_bytes_per_step": e2e["h2d_dev"] // args.steps,
+                       "dma_d2h_bytes_per_step": e2e["d2h_dev"] // args.steps,
                        "mode": "out-of-core streamed, capacity = problem/3 (artificial cap "
                                f"{e2e['capacity']} B per GPU), cyclic, T={e2e['tiles']}" +
                                (f"; {world} GPUs each stream their own {n}x{n} problem over "

@@ -587,10 +587,27 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
   std::vector<BoxLayout> lay(mesh.datasets.size());
   std::vector<index_t> off(mesh.datasets.size(), 0);
   index_t slot_elems = 0;
+  // Arena boxes span the dataset's full allocation across the non-tiled dimensions: a
+  // tile box that stops a column or two short of the allocation (e.g. a dataset read
+  // through a row-only stencil) would make every upload a pitched copy; uploading the
+  // whole rows instead is one contiguous DMA at full PCIe rate (the extra columns are
+  // never read, never downloaded, and not counted: audit and timeline keep the
+  // reference's boxes).
+  auto widen = [&](DatasetId d, const Extent& e) {
+    Extent w = e;
+    if (e.empty()) return w;
+    const Extent a = mesh[d].alloc();
+    for (int k = 0; k < e.ndim; ++k)
+      if (k != dim) {
+        w.lo[k] = a.lo[k];
+        w.hi[k] = a.hi[k];
+      }
+    return w;
+  };
   for (DatasetId d : used) {
     Extent big = Extent::none(mesh[d].core.ndim);
-    for (const Extent& f : P(d).full)
-      if (!f.empty()) {
+    for (const Extent& f0 : P(d).full)
+      if (const Extent f = widen(d, f0); !f.empty()) {
         if (big.empty()) {
           big = f;
         } else {
@@ -616,7 +633,7 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
   auto slot_of = [&](int t) { return (slot_cursor_ + t) % 3; };
   auto arena = [&](DatasetId d, int t) {
     return view_at(pool_ + static_cast<index_t>(slot_of(t)) * slot_elems + off[static_cast<std::size_t>(d)],
-                   P(d).full[t], lay[static_cast<std::size_t>(d)].stride);
+                   widen(d, P(d).full[t]), lay[static_cast<std::size_t>(d)].stride);
   };
   std::map<std::pair<DatasetId, int>, AuditRow> audit;
   auto row = [&](DatasetId d, int t) -> AuditRow& {
@@ -626,11 +643,11 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     return r;
   };
   auto copy = [&](int q, int kind, const ooc_view& s, const ooc_view& dv, const Extent& region,
-                  DatasetId d, int tile) {
+                  DatasetId d, int tile, const Extent* dma = nullptr) {
     int64_t lo[3], hi[3];
     for (int k = 0; k < 3; ++k) {
-      lo[k] = region.lo[k];
-      hi[k] = region.hi[k];
+      lo[k] = dma ? dma->lo[k] : region.lo[k];
+      hi[k] = dma ? dma->hi[k] : region.hi[k];
     }
     const int cmd = kind == OOC_COPY_H2D ? 0 : kind == OOC_COPY_D2H ? 1 : 2;  // CmdKind order
     timeline_cmd(cmd, q, region.size() * mesh[d].elem_bytes, d, tile, {},
@@ -721,12 +738,14 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
           for (const Extent& part : {lo_part, hi_part})
             if (part.lo[dim] < part.hi[dim]) {
               wait_host_rows(d, part);
-              copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), part, d, 0);
+              const Extent wpart = widen(d, part);
+              copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), part, d, 0, &wpart);
               row(d, 0).uploaded += part.size() * eb;
             }
         } else {
           wait_host_rows(d, region);
-          copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), region, d, 0);
+          const Extent wregion = widen(d, region);
+          copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, 0), region, d, 0, &wregion);
           row(d, 0).uploaded += region.size() * eb;
         }
       }
@@ -740,8 +759,9 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
         const auto& pd = P(d);
         if (pd.write_first || pd.right_fp[t + 1].empty()) continue;
         wait_host_rows(d, pd.right_fp[t + 1]);
+        const Extent wfp = widen(d, pd.right_fp[t + 1]);
         copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], arena(d, t + 1), pd.right_fp[t + 1], d,
-             t + 1);
+             t + 1, &wfp);
         row(d, t + 1).uploaded += pd.right_fp[t + 1].size() * mesh[d].elem_bytes;
       }
       DEV(ooc_event_record(ctx_, E(ev_h2d_, t + 1), OOC_Q_H2D));
