@@ -827,22 +827,23 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
     for (DatasetId d : used) {
       const auto& pd = P(d);
       if (pd.write_first || pd.full[0].empty()) continue;
-      st_lay.push_back({d, padded_layout(pd.full[0], 2)});
+      st_lay.push_back({d, padded_layout(widen(d, pd.full[0]), 2)});
       need += (st_lay.back().second.elems + 31) / 32 * 32;
     }
     ensure_staging(need);
     index_t at = 0;
     for (const auto& [d, L] : st_lay) {
       const Extent& region = P(d).full[0];
+      const Extent wregion = widen(d, region);  // whole rows: one contiguous DMA
       int last = -1;
       for (const auto& [box, t] : this_down[static_cast<std::size_t>(d)])
-        if (!box.intersect(region).empty()) last = std::max(last, t);
+        if (!box.intersect(wregion).empty()) last = std::max(last, t);
       if (last >= 0) DEV(ooc_queue_wait(ctx_, OOC_Q_H2D, E(ev_d2h_, last)));
       Staged s;
       s.region = region;
-      s.view = view_at(staging_ + at, region, L.stride);
+      s.view = view_at(staging_ + at, wregion, L.stride);
       at += (L.elems + 31) / 32 * 32;
-      copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], s.view, region, d, T);
+      copy(OOC_Q_H2D, OOC_COPY_H2D, hviews[static_cast<std::size_t>(d)], s.view, region, d, T, &wregion);
       row(d, T).uploaded += region.size() * mesh[d].elem_bytes;
       staged_[d] = s;
     }
