@@ -395,6 +395,9 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   const double pts = static_cast<double>(bx[1] - bx[0]) * static_cast<double>(bx[3] - bx[2]);
   if (pts > 1.25 * pts_loops + 4096) return fail(why, "out-of-place allocation much larger than the loops");
   for (int k = 0; k < 4; ++k) pl.box[k] = bx[k];
+  // a reducing run writes one partial per CTA into the queue's partial buffer (8192)
+  if (pl.red_op != OOC_RED_NONE && (bx[3] - bx[2] + pl.TC - 1) / pl.TC > 4096)
+    return fail(why, "reduction over too many strips");
   return true;
 }
 
