@@ -1292,10 +1292,18 @@ bool GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& ru
     }
     red.push_back({r.dev, r.shadow});
   }
+  int rc = OOC_OK;
   issue_instrumented(OOC_Q_COMPUTE, loops, bytes, [&] {
-    DEV(ooc_launch_sweep(ctx_, OOC_Q_COMPUTE, calls.data(), static_cast<int>(calls.size()), red.data(),
-                         static_cast<int>(red.size())));
+    rc = ooc_launch_sweep(ctx_, OOC_Q_COMPUTE, calls.data(), static_cast<int>(calls.size()), red.data(),
+                          static_cast<int>(red.size()));
   });
+  if (rc == OOC_ERR_UNSUPPORTED) {  // e.g. the kernel could not be built: fused launches instead
+    static bool warned = false;
+    if (!warned) std::fprintf(stderr, "ooc: row sweep unavailable (%s); using fused launches\n", ooc_dev_last_error());
+    warned = true;
+    return false;
+  }
+  DEV(rc);
   for (DatasetId d : outs) {
     Resident& r = res_[static_cast<std::size_t>(d)];
     std::swap(r.dev, r.shadow);
