@@ -59,3 +59,19 @@ def test_random_2d_chains_compile(jit_always):
                 assert g["ok"], (seed, g)
                 n += 1
     assert n > 5
+
+
+def test_sweep_plans_of_other_apps(jit_always):
+    """heat2d and the 2-D RK3 chain: whole chains become sweep runs; read-and-rewritten
+    datasets are out of place, temporaries in place; lags never negative; every run's
+    kernel compiles."""
+    for app, kw in (("heat2d", dict(iters=8, span=4)), ("rk3chain", dict(iters=6, span=3))):
+        rt, chains = _chains(P.app_program(app, 120, 96, 0, **kw))
+        runs = [g for c in chains for g in rt.chain_sweep_check(c, compile=True)]
+        assert runs and all(g["ok"] for g in runs), app
+        for g in runs:
+            pl = g["plan"]
+            assert min(pl["lags"]) >= 0 and len(pl["lags"]) == g["loops"]
+            assert all(d["oop"] == (d["loaded"] and d["written"]) for d in pl["datasets"])
+            assert pl["HC"] >= max(pl["halos"])
+
