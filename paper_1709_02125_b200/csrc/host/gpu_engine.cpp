@@ -1301,6 +1301,16 @@ bool GpuEngine::run_sweep(Mesh& mesh, const LoopChain& chain, const SweepRun& ru
     static bool warned = false;
     if (!warned) std::fprintf(stderr, "ooc: row sweep unavailable (%s); using fused launches\n", ooc_dev_last_error());
     warned = true;
+    // the instrumented span bracketed no launch: drop it, the fused launches record their own
+    if (opts_.timeline && !tl_pending_.empty()) {
+      recycle(tl_pending_.back().a);
+      recycle(tl_pending_.back().b);
+      tl_pending_.pop_back();
+    } else if (opts_.profile_loops && !pending_loops_.empty()) {
+      recycle(pending_loops_.back().a);
+      recycle(pending_loops_.back().b);
+      pending_loops_.pop_back();
+    }
     return false;
   }
   DEV(rc);
