@@ -1121,6 +1121,13 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
       sp->dst[d] = to;
     }
   }
+  // test hook: every sweep kernel "fails to build", exercising the engine's fallback
+  static const bool fail_build = std::getenv("OOC_SWEEP_FAIL_BUILD") != nullptr;
+  if (fail_build) {
+    delete sp;
+    set_error("ooc_launch_sweep: build disabled (OOC_SWEEP_FAIL_BUILD)");
+    return OOC_ERR_UNSUPPORTED;
+  }
   SwKernel* k = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_sw_mu);

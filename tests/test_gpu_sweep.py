@@ -124,3 +124,13 @@ def test_sweep_variants(K, P_, smem, rc):
     r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "sweep_parity_child.py")],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def test_sweep_build_failure_falls_back():
+    """A row-sweep kernel that cannot be built (forced by OOC_SWEEP_FAIL_BUILD) falls back
+    to the fused loop-group launches: bits unchanged, each loop's bytes billed once."""
+    env = dict(os.environ, OOC_SWEEP_FAIL_BUILD="1")
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "sweep_fallback_child.py")],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "row sweep unavailable" in r.stderr
