@@ -19,8 +19,10 @@ Inputs are far larger than L2 (126 MB), so no L2 flush is needed between steps.
           reference executor, on a bounded sample of the same app.
 
 --impl reference runs only the reference CPU path (rank 0) and prints its line.
-Multi-GPU (torchrun, N>1): each rank runs the workload on its own GPU (replicas,
-weak scaling); times are the max over ranks.
+Multi-GPU (torchrun, N>1): weak scaling — an (N*n) x n grid, each rank owns a dim-0
+slab of n rows on its own GPU (ghost rows recomputed, NCCL ghost exchange + fieldsum
+all-reduce per chain); times are the max over ranks. OOC_BENCH_FORCE_DIST=1 under
+torchrun with one rank runs the same slab path (NCCL, one rank) on one GPU.
 """
 from __future__ import annotations
 
@@ -37,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "stencil-chain effective GB/s & out-of-core/in-core efficiency at 1–3× HBM"
+OUT = sys.stdout  # replaced in main() by a private dup of fd 1
 UNIT = "GB/s"
 ITERS_PER_STEP = 10
 
@@ -166,7 +169,7 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or os.environ.get("OOC_BENCH_FORCE_DIST") == "1":
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -213,12 +216,12 @@ def cpu_reference(steps, n_sample=1920, warmup=1):
 
 
 # ------------------------------------------------------------------ GPU arm
-def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, world=1):
+def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, world=1, slab=False):
     """In-core miniflow2d. With world > 1 the grid is (world*n) x n and each rank owns a
     slab of n rows (weak scaling): ghost rows recomputed, ghost bands exchanged with
     NCCL after every chain, fieldsum all-reduced (paper_1709_02125_b200/dist.py)."""
     nx = n * world
-    if world > 1:
+    if world > 1 or slab:
         from paper_1709_02125_b200 import dist as D
         ghost = D.chain_depth("miniflow2d", 2 * ITERS_PER_STEP)
         rt = B.Runtime("resident", profile=profile, gpu=gpu, dist=(rank, world),
@@ -310,6 +313,12 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", type=int, default=1)
     args = ap.parse_args()
+    # stdout carries exactly the one JSON line: anything the libraries print there
+    # (NCCL's version banner, ...) goes to stderr
+    global OUT
+    OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     rank, world, local, dist = dist_init()
 
     if args.impl == "reference":
@@ -326,17 +335,18 @@ def main():
                 "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": ref["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        print(json.dumps(line), file=OUT, flush=True)
         return
 
     import paper_1709_02125_b200 as B
-    gpu = local if world > 1 else 0
+    gpu = local if dist is not None else 0
     n = args.n
     barrier(dist)
     # at least 5 untimed warm-up chains: the first sight of every fused-kernel structure
     # compiles its tile-shape candidates and the next launches time them
     warm = max(args.warmup, 5)
-    inc = run_incore(B, n, args.steps, warm, bool(args.profile), gpu, rank=rank, world=world)
+    inc = run_incore(B, n, args.steps, warm, bool(args.profile), gpu, rank=rank, world=world,
+                     slab=dist is not None)
     dt = max_over_ranks(inc["seconds"], dist, local)
     # every rank's metric counts only its owned rows, so the job total is their sum
     value = world * inc["bytes"] / dt / 1e9
@@ -387,7 +397,7 @@ def main():
                    "l2": "inputs (18.9 GB) >> L2 (126 MB); no flush needed",
                    "parallelism": (f"dp{world} dim-0 slabs of {n} rows (grid {n * world}x{n}), "
                                    "ghost rows recomputed, NCCL ghost exchange + all-reduce per chain"
-                                   if world > 1 else "single GPU")},
+                                   if dist is not None else "single GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
                      "traffic_source": traffic_src,
@@ -458,7 +468,7 @@ def main():
             line["cpu_baseline"].pop("loop_time_s", None)
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": str(e)}
-    print(json.dumps(line))
+    print(json.dumps(line), file=OUT, flush=True)
 
 
 if __name__ == "__main__":
