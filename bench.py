@@ -173,7 +173,7 @@ def dist_init():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         return rank, world, local, dist
     return rank, world, local, None
 
@@ -472,4 +472,9 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    finally:
+        _d = sys.modules.get("torch.distributed")
+        if _d is not None and _d.is_available() and _d.is_initialized():
+            _d.destroy_process_group()
