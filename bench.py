@@ -308,7 +308,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=15360)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=15360)  # --size under torchrun (--n is ambiguous there)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", type=int, default=1)

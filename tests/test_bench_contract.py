@@ -25,3 +25,20 @@ def test_reference_arm_prints_one_json_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+
+
+@pytest.mark.gpu
+def test_slab_bench_under_torchrun_single_rank():
+    """The multi-GPU bench path (torchrun, NCCL, dim-0 slabs, ghost exchange after every
+    chain) on one GPU (OOC_BENCH_FORCE_DIST=1), small grid: one JSON line, dp1 slabs."""
+    env = dict(os.environ, OOC_BENCH_FORCE_DIST="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", "29541", "bench.py", "--gpus", "1",
+           "--size", "2048", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = r.stdout.splitlines()
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["config"]["parallelism"].startswith("dp1 dim-0 slabs")
