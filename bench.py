@@ -148,10 +148,13 @@ def _nloops(group):
         return 1
 
 
-def profiled_traffic(group, key="dram_bytes_per_launch"):
+def profiled_traffic(group, key="dram_bytes_per_launch", gen_hashes=()):
     """Bytes per launch of `group` (DRAM, or shared memory with key=
     "smem_bytes_per_launch") from the committed ncu launch list
-    (profiles/*_traffic.json, produced from the same bench command)."""
+    (profiles/*_traffic.json). Used only when that capture was taken of the kernels this
+    run built: every generator hash of this run's sweep kernels of that size must be
+    listed in the file (a changed kernel never pairs new timings with old bytes).
+    Returns (bytes, file, state)."""
     import glob
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), reverse=True):
         try:
@@ -161,8 +164,11 @@ def profiled_traffic(group, key="dram_bytes_per_launch"):
             continue
         for k in prof.get("kernels", []):
             if k.get("group", "").split(" ")[0] == group and k.get(key):
-                return k[key], os.path.relpath(f, ROOT)
-    return None, None
+                have = set(prof.get("gen_hashes", []))
+                if not gen_hashes or not set(gen_hashes) <= have:
+                    return None, os.path.relpath(f, ROOT), "stale: captured from other kernel sources"
+                return k[key], os.path.relpath(f, ROOT), "generator hash matches"
+    return None, None, "no capture"
 
 
 def dist_init():
@@ -216,7 +222,8 @@ def cpu_reference(steps, n_sample=1920, warmup=1):
 
 
 # ------------------------------------------------------------------ GPU arm
-def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, world=1, slab=False):
+def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, world=1, slab=False,
+               keep=False):
     """In-core miniflow2d. With world > 1 the grid is (world*n) x n and each rank owns a
     slab of n rows (weak scaling): ghost rows recomputed, ghost bands exchanged with
     NCCL after every chain, fieldsum all-reduced (paper_1709_02125_b200/dist.py)."""
@@ -229,7 +236,7 @@ def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, wor
         D.init_comm(rt, rank)
     else:
         ghost = 0
-        rt = B.Runtime("resident", profile=profile, gpu=gpu, resident_budget=resident_budget)
+        rt = B.Runtime("resident", profile=profile, gpu=gpu, resident_budget=resident_budget, record=True)
     t_decl = time.perf_counter()
     rt.declare_app("miniflow2d", nx, n)
     t_decl = time.perf_counter() - t_decl
@@ -264,17 +271,55 @@ def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, wor
            "tiles": rep1["tiles"], "device": dev1}
     red = rt.fetch_reduction("fieldsum")
     out["fieldsum"] = red
-    rt.close()
+    out["chains"] = warmup + steps
+    # compulsory DRAM bytes of every row-sweep launch of a steady-state chain, by launch
+    # label (the sweep planner's own accounting: inputs read once, live outputs written once)
+    out["sweep_dram"] = {}
+    try:
+        for c in range(rt.num_chains()):
+            if rt.chain_plan(c, tiles=1)["loops"] == 141:
+                for g in rt.chain_sweep_check(c, compile=False):
+                    if not g["ok"]:
+                        continue
+                    a, nl = g["first"], g["loops"]
+                    key = f"L{a % 14 + 1}-L{a % 14 + nl}"
+                    db = g["plan"]["dram_bytes"]
+                    out["sweep_dram"].setdefault(key, []).append(db["loaded"] + db["stored"])
+                break
+    except Exception as ex:  # noqa: BLE001
+        out["sweep_dram_error"] = str(ex)
+    if keep:
+        out["rt"] = rt
+    else:
+        rt.close()
     return out
 
 
-def run_e2e(B, n, steps, warmup, gpu, ratio=3.0, cyclic=True, prefetch=True):
-    pb = B.problem_bytes("miniflow2d", n, n)
-    cap = int(pb / ratio)
-    # speculative prefetch of the next chain's first tile (reference ExecOptions::prefetch)
-    rt = B.Runtime("explicit", capacity=cap, gpu=gpu, prefetch=prefetch)
-    rt.declare_app("miniflow2d", n, n)
-    rt.app_iterations("miniflow2d", n, n, 0, 0, ITERS_PER_STEP * warmup, cyclic=False)
+def run_e2e(B, n, steps, warmup, gpu, ratio=3.0, cyclic=True, prefetch=True, keep=False, rank=0, world=1,
+            slab=False):
+    """Out of core through the reference-facing API. With world > 1 (or slab) ONE mesh of
+    (world*n) x n is decomposed: every rank streams its own dim-0 slab of n rows over its
+    own host link through 3 HBM slots under its own cap (slab bytes / ratio), ghost bands
+    refreshed from the neighbours' host slabs after every chain (NCCL, or CUDA IPC with
+    OOC_COMM=ipc), fieldsum all-reduced."""
+    nx = n * world
+    if world > 1 or slab:
+        from paper_1709_02125_b200 import dist as D
+        ghost = D.chain_depth("miniflow2d", 2 * ITERS_PER_STEP)
+        own = D.slab(rank, world, nx)
+        # the slab's datasets: owned rows + ghost rows on each side
+        pb = B.problem_bytes("miniflow2d", own[1] - own[0] + 2 * ghost, n)
+        cap = int(pb / ratio)
+        rt = B.Runtime("explicit", capacity=cap, gpu=gpu, prefetch=prefetch, dist=(rank, world), own=own,
+                       ghost=ghost)
+        D.init_comm(rt, rank)
+    else:
+        pb = B.problem_bytes("miniflow2d", n, n)
+        cap = int(pb / ratio)
+        # speculative prefetch of the next chain's first tile (reference ExecOptions::prefetch)
+        rt = B.Runtime("explicit", capacity=cap, gpu=gpu, prefetch=prefetch)
+    rt.declare_app("miniflow2d", nx, n)
+    rt.app_iterations("miniflow2d", nx, n, 0, 0, ITERS_PER_STEP * warmup, cyclic=False)
     if cyclic:
         rt.set_cyclic_flag(True)
     rt.sync()
@@ -283,7 +328,7 @@ def run_e2e(B, n, steps, warmup, gpu, ratio=3.0, cyclic=True, prefetch=True):
     with ClockSampler(gpu) as clk:
         m0 = rt.mark()
         t0 = time.perf_counter()
-        rt.app_iterations("miniflow2d", n, n, 0, ITERS_PER_STEP * warmup,
+        rt.app_iterations("miniflow2d", nx, n, 0, ITERS_PER_STEP * warmup,
                           ITERS_PER_STEP * (warmup + steps), cyclic=cyclic)
         m1 = rt.mark()
         rt.sync()
@@ -297,9 +342,121 @@ def run_e2e(B, n, steps, warmup, gpu, ratio=3.0, cyclic=True, prefetch=True):
            "d2d": rep1["d2d"] - rep0["d2d"], "tiles": rep1["tiles"], "capacity": cap,
            "problem_bytes": pb, "launches": dev1["kernel_launches"] - dev0["kernel_launches"],
            "clocks": clk.summary(), "h2d_dev": dev1["h2d_bytes"] - dev0["h2d_bytes"],
-           "d2h_dev": dev1["d2h_bytes"] - dev0["d2h_bytes"]}
-    rt.close()
+           "d2h_dev": dev1["d2h_bytes"] - dev0["d2h_bytes"],
+           "fieldsum": rt.fetch_reduction("fieldsum")}
+    if keep:
+        out["rt"] = rt
+    else:
+        rt.close()
     return out
+
+
+# ------------------------------------------------------------------ parity at the benched size
+def _memeq(a, b):
+    """Bitwise equality of two float64 arrays (libc memcmp: seconds for 2.4 GB arrays)."""
+    import ctypes
+    import numpy as np
+    a = np.ascontiguousarray(a).reshape(-1)
+    b = np.ascontiguousarray(b).reshape(-1)
+    if a.size != b.size:
+        return False
+    libc = ctypes.CDLL(None)
+    libc.memcmp.restype = ctypes.c_int
+    libc.memcmp.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]
+    return libc.memcmp(a.ctypes.data, b.ctypes.data, a.nbytes) == 0
+
+
+def _ulp_diff(a, b):
+    """Largest ULP distance between two float64 arrays (0 = bitwise equal)."""
+    import numpy as np
+    ia = np.asarray(a).reshape(-1).view(np.int64)
+    ib = np.asarray(b).reshape(-1).view(np.int64)
+    step = 1 << 26
+    worst = 0
+    for i in range(0, ia.size, step):
+        d = np.abs(ia[i:i + step] - ib[i:i + step])
+        worst = max(worst, int(d.max()) if d.size else 0)
+    return worst
+
+
+def parity_incore_vs_ooc(inc_rt, ooc_rt, inc_sum, ooc_sum):
+    """The same chains run resident (row sweeps) and streamed (3 HBM slots, capacity =
+    problem/3, cyclic): every dataset the streamed run keeps fresh on the host must be
+    bitwise equal (fields follow the reference's operation order on both paths); the
+    field summaries, folded in different orders, within 1e-12."""
+    inc_rt.finish()
+    ooc_rt.finish()
+    out = {"datasets": {}, "fields_bitwise": True}
+    for d in range(inc_rt.num_datasets):
+        name = f"d{d}"
+        if ooc_rt.dataset_info(d)["stale"]:
+            out["datasets"][name] = "stale (cyclic temporary: never downloaded)"
+            continue
+        eq = _memeq(inc_rt.host(d), ooc_rt.host(d))
+        out["datasets"][name] = "bitwise" if eq else f"differs (max {_ulp_diff(inc_rt.host(d), ooc_rt.host(d))} ulp)"
+        out["fields_bitwise"] = out["fields_bitwise"] and eq
+    out["fieldsum_rel_err"] = abs(inc_sum - ooc_sum) / max(abs(ooc_sum), 1e-300)
+    out["ok"] = out["fields_bitwise"] and out["fieldsum_rel_err"] <= 1e-12
+    return out
+
+
+def parity_vs_reference(B, n, gpu):
+    """One 10-iteration miniflow2d chain at the benched size: the unmodified reference
+    (oracle/_ref, OpenMP on every host core, reference executor — proj/tools/ooc_cli.cpp:186-207
+    --verify compares the same way) against this engine resident on the GPU: every field
+    bitwise, the fieldsum within 1e-12 relative (the reference folds sequentially,
+    proj/src/kernel_exec.cpp:193-197)."""
+    from oracle import refo
+    if not refo.available():
+        return {"ok": None, "skipped": "oracle/_ref/libooc_ref.so not built"}
+    t0 = time.perf_counter()
+    ref = refo.RefRuntime("reference", openmp=True)
+    ref.run_app("miniflow2d", n, n, ITERS_PER_STEP)
+    t_ref = time.perf_counter() - t0
+    rt = B.Runtime("resident", gpu=gpu)
+    rt.declare_app("miniflow2d", n, n)
+    rt.app_iterations("miniflow2d", n, n, 0, 0, ITERS_PER_STEP)
+    rt.finish()
+    out = {"size": n, "iterations": ITERS_PER_STEP, "datasets": {}, "fields_bitwise": True,
+           "reference_wall_s": t_ref, "reference_threads": os.cpu_count()}
+    names = ref.datasets()
+    for d in range(rt.num_datasets):
+        eq = _memeq(rt.host(d), ref.host_view(d))
+        out["datasets"][names[d]] = "bitwise" if eq else f"differs (max {_ulp_diff(rt.host(d), ref.host_view(d))} ulp)"
+        out["fields_bitwise"] = out["fields_bitwise"] and eq
+    a, b = rt.fetch_reduction("fieldsum"), ref.fetch_reduction("fieldsum")
+    out["fieldsum"] = a
+    out["fieldsum_reference"] = b
+    out["fieldsum_rel_err"] = abs(a - b) / max(abs(b), 1e-300)
+    out["ok"] = out["fields_bitwise"] and out["fieldsum_rel_err"] <= 1e-12
+    rt.close()
+    ref.close()
+    return out
+
+
+def cpu_config1():
+    """BASELINE configs[0] as specified: the reference's *tiled explicit* CPU executor
+    (proj/src/explicit_exec.cpp:55-281) on miniflow2d 960x960, 87 iterations, capacity =
+    problem/3 (proj/src/apps.cpp:219-228), OpenMP on every host core."""
+    from oracle import refo
+    n, iters = 960, 87
+    cap = refo.app_problem_bytes("miniflow2d", n, n) // 3
+    ref = refo.RefRuntime("explicit", capacity=cap, openmp=True)
+    t0 = time.perf_counter()
+    ref.run_app("miniflow2d", n, n, iters)
+    wall = time.perf_counter() - t0
+    tot = ref.totals()
+    ref.close()
+    return {"value": tot["metric_bytes"] / wall / 1e9, "unit": UNIT, "cores": os.cpu_count(),
+            "kind": "reference", "sample": f"configs[0]: miniflow2d {n}x{n}, {iters} iterations, "
+            f"tiled explicit executor, capacity = problem/3 ({cap} B), T={tot['last_tiles']}; "
+            f"metric bytes / wall {wall:.2f} s",
+            "loop_time_GBps": tot["metric_bytes"] / tot["loop_time_s"] / 1e9}
+
+
+def sweep_gen_hashes(B, nloops):
+    """Generator hashes of the row-sweep kernels of `nloops` loops built in this process."""
+    return sorted({e["gen_hash"] for e in B.sweep_report() if e.get("loops") == nloops})
 
 
 def main():
@@ -311,6 +468,8 @@ def main():
     ap.add_argument("--n", "--size", dest="n", type=int, default=15360)  # --size under torchrun (--n is ambiguous there)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the full-size parity leg (in-core vs streamed, and the reference)")
     ap.add_argument("--profile", type=int, default=1)
     args = ap.parse_args()
     # stdout carries exactly the one JSON line: anything the libraries print there
@@ -341,19 +500,21 @@ def main():
     import paper_1709_02125_b200 as B
     gpu = local if dist is not None else 0
     n = args.n
+    parity_on = not args.no_parity and dist is None
     barrier(dist)
     # at least 5 untimed warm-up chains: the first sight of every fused-kernel structure
     # compiles its tile-shape candidates and the next launches time them
     warm = max(args.warmup, 5)
     inc = run_incore(B, n, args.steps, warm, bool(args.profile), gpu, rank=rank, world=world,
-                     slab=dist is not None)
+                     slab=dist is not None, keep=parity_on and not args.no_e2e)
     dt = max_over_ranks(inc["seconds"], dist, local)
     # every rank's metric counts only its owned rows, so the job total is their sum
     value = world * inc["bytes"] / dt / 1e9
     e2e = None
     if not args.no_e2e:
         barrier(dist)
-        e2e = run_e2e(B, n, args.steps, warm, gpu)
+        e2e = run_e2e(B, n, args.steps, warm, gpu, keep=parity_on, rank=rank, world=world,
+                      slab=dist is not None)
         e2e_wall = max_over_ranks(e2e["wall"], dist, local)
     link = None
     if e2e:
@@ -364,27 +525,30 @@ def main():
     if rank != 0:
         return
     peak, peak_kind = measured_peaks()
-    # dominant kernel = the (fused) par_loop kernel with the largest share of the step;
-    # achieved = its algorithmic (metric) bytes per launch / its mean launch time
+    # ---- dominant kernel: the launch kind with the largest share of the step.
+    # achieved = its compulsory DRAM bytes per launch (every array it loads read once,
+    # every live output written once — the sweep planner's accounting) /
+    # its mean launch time (CUDA events on the compute queue); frac against the measured
+    # HBM copy peak. The reference's metric bytes of the fused loops (which count every
+    # loop's operands, proj/src/metrics.cpp:10-12) are reported beside it as
+    # effective_over_hbm — a fused kernel moves far fewer DRAM bytes than that.
     kinds = inc["kinds"]
     dom = max(kinds, key=lambda k: kinds[k]["seconds"]) if kinds else None
-    achieved = (kinds[dom]["bytes"] / kinds[dom]["seconds"] / 1e9) if dom else None
     total_k = sum(k["seconds"] for k in kinds.values())
-    traffic, traffic_src = profiled_traffic(dom) if dom else (None, None)
-    # the row-sweep kernels move their operands through shared memory: its bandwidth
-    # (148 SMs x 128 B/clk at the measured SM clock) is the ceiling that binds them
+    launch_s = kinds[dom]["seconds"] / kinds[dom]["launches"] if dom else None
+    metric_per_launch = kinds[dom]["bytes"] / kinds[dom]["launches"] if dom else None
+    comp = inc.get("sweep_dram", {}).get(dom) if dom else None
+    comp_per_launch = sum(comp) / len(comp) if comp else None
+    gen = sweep_gen_hashes(B, _nloops(dom)) if dom else []
+    traffic, traffic_src, traffic_state = profiled_traffic(dom, gen_hashes=gen) if dom else (None, None, None)
+    smem_b, _, _ = profiled_traffic(dom, "smem_bytes_per_launch", gen_hashes=gen) if dom else (None, None, None)
+    achieved = comp_per_launch / launch_s / 1e9 if comp_per_launch else None
     limiter = None
-    smem_b, _ = profiled_traffic(dom, "smem_bytes_per_launch") if dom else (None, None)
     if smem_b and dom:
-        launch_s = kinds[dom]["seconds"] / kinds[dom]["launches"]
         mhz = (inc.get("clocks") or {}).get("sm_mhz") or 1965.0
         smem_peak = 148 * 128 * mhz * 1e6 / 1e9
-        dram_gbps = traffic / launch_s / 1e9 if traffic else None
         limiter = {"smem_bytes_per_launch": smem_b, "smem_GBps": smem_b / launch_s / 1e9,
-                   "smem_peak_GBps": smem_peak, "smem_frac": smem_b / launch_s / 1e9 / smem_peak,
-                   "dram_frac": dram_gbps / peak if dram_gbps else None,
-                   "binding": ("shared memory" if dram_gbps is None or
-                               smem_b / launch_s / 1e9 / smem_peak > dram_gbps / peak else "hbm")}
+                   "smem_peak_GBps": smem_peak, "smem_frac": smem_b / launch_s / 1e9 / smem_peak}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": warm, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
@@ -399,28 +563,29 @@ def main():
                                    "ghost rows recomputed, NCCL ghost exchange + all-reduce per chain"
                                    if dist is not None else "single GPU")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "traffic_source": traffic_src,
-                     "dram_GBps": (traffic / (kinds[dom]["seconds"] / kinds[dom]["launches"]) / 1e9
-                                   if traffic and dom else None),
-                     "dram_frac": (traffic / (kinds[dom]["seconds"] / kinds[dom]["launches"]) / 1e9 / peak
-                                   if traffic and dom else None),
-                     "note": "achieved counts the reference's metric bytes of every loop fused into the "
-                             "kernel (proj/src/metrics.cpp:10-12); traffic/dram_* are the DRAM bytes the "
-                             "fused kernel really moves (ncu)",
+                     "frac": achieved / peak if achieved else None,
+                     "traffic": traffic, "traffic_source": traffic_src, "traffic_check": traffic_state,
+                     "traffic_frac": traffic / launch_s / 1e9 / peak if traffic and launch_s else None,
+                     "algorithmic_bytes_per_launch": comp_per_launch,
+                     "algorithmic_bytes": "compulsory DRAM bytes of the fused launch: each array it loads "
+                                          "read once + each live output written once (56 B per point per "
+                                          "timestep for miniflow2d: rho, e, v, gamma in; rho, e, v out)",
+                     "effective_over_hbm": metric_per_launch / launch_s / 1e9 / peak if dom else None,
+                     "metric_bytes_per_launch": metric_per_launch,
                      "peak_source": peak_kind,
-                     "kernel": (f"ooc_sweep_kernel [{dom}] (row-sweep: the loops stream through "
-                                "shared-memory rings in one sm_100a launch)" if _nloops(dom) > 8 else
-                                f"ooc_jit_kernel [{dom}] (fused sm_100a par_loop kernel)"),
+                     "kernel": (f"ooc_sweep_kernel [{dom}] (row sweep: the loops stream through "
+                                "shared-memory rings in one sm_100a launch; TMA bulk-copy loads)" if _nloops(dom) > 8
+                                else f"ooc_jit_kernel [{dom}] (fused sm_100a par_loop kernel)"),
                      "kernel_share_of_step": kinds[dom]["seconds"] / total_k if dom else None,
-                     "bytes_per_launch": kinds[dom]["bytes"] / kinds[dom]["launches"] if dom else None,
-                     "launch_ms": 1e3 * kinds[dom]["seconds"] / kinds[dom]["launches"] if dom else None,
+                     "launch_ms": 1e3 * launch_s if dom else None,
                      "limiter": limiter},
-        "kernels": {k: {"launches": v["launches"], "GBps": round(v["bytes"] / v["seconds"] / 1e9),
+        "kernels": {k: {"launches": v["launches"], "GBps_metric": round(v["bytes"] / v["seconds"] / 1e9),
                         "share": round(v["seconds"] / total_k, 3)} for k, v in sorted(kinds.items())},
         "tile_shapes": B.jit_report(),
         "sweep_tuning": B.sweep_report(),
         "jit_compile_ms": inc["device"].get("jit_compile_ms"),
+        "sweep_host_us_per_launch": (inc["device"].get("sweep_host_us", 0) /
+                                     max(inc["device"].get("sweep_launches", 1), 1)),
         "gpu_launches": inc["launches"],
         "clocks": inc["clocks"],
         "incore": {"seconds": inc["seconds"], "metric_bytes": inc["bytes"],
@@ -437,8 +602,9 @@ def main():
                        "dma_d2h_bytes_per_step": e2e["d2h_dev"] // args.steps,
                        "mode": "out-of-core streamed, capacity = problem/3 (artificial cap "
                                f"{e2e['capacity']} B per GPU), cyclic, T={e2e['tiles']}" +
-                               (f"; {world} GPUs each stream their own {n}x{n} problem over "
-                                "their own host link" if world > 1 else ""),
+                               (f"; one {n * world}x{n} mesh in {world} dim-0 slabs, each GPU streams its "
+                                "own slab over its own host link, ghost bands refreshed host to host "
+                                "between chains" if dist is not None else ""),
                        "device_s": e2e["device_s"], "wall_s": e2e["wall"],
                        "ooc_over_incore": e2e_val / value, "launches": e2e["launches"],
                        "clocks": e2e["clocks"],
@@ -461,11 +627,35 @@ def main():
                                        "pinned_copy_GBps": link}
         elif link:
             line["e2e"]["roofline"] = link
+    # ---- parity at the benched size (after every timed region)
+    if parity_on:
+        par = {"size": n}
+        if e2e and "rt" in inc and "rt" in e2e:
+            try:
+                par["incore_vs_streamed"] = parity_incore_vs_ooc(inc["rt"], e2e["rt"], inc["fieldsum"],
+                                                                 e2e["fieldsum"])
+                par["incore_vs_streamed"]["chains"] = inc["chains"]
+            except Exception as ex:  # noqa: BLE001
+                par["incore_vs_streamed"] = {"ok": False, "error": str(ex)}
+        for r in (inc.get("rt"), (e2e or {}).get("rt")):
+            if r is not None:
+                r.close()
+        inc.pop("rt", None)
+        if e2e:
+            e2e.pop("rt", None)
+        try:
+            par["reference"] = parity_vs_reference(B, n, gpu)
+        except Exception as ex:  # noqa: BLE001
+            par["reference"] = {"ok": False, "error": str(ex)}
+        checks = [v.get("ok") for v in par.values() if isinstance(v, dict)]
+        par["ok"] = all(c for c in checks if c is not None) and any(c is not None for c in checks)
+        line["parity"] = par
     if not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_reference(1, n_sample=1920, warmup=0)
             line["cpu_baseline"].pop("metric_bytes", None)
             line["cpu_baseline"].pop("loop_time_s", None)
+            line["cpu_baseline"]["config1_tiled_explicit"] = cpu_config1()
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     print(json.dumps(line), file=OUT, flush=True)

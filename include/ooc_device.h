@@ -199,9 +199,12 @@ typedef struct {
 int ooc_sweep_check(const ooc_loop* loops, int n, int* flags);
 int ooc_launch_sweep(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n, const ooc_redirect* redirects,
                      int nredirects);
-/* JSON description of the sweep plan (lags, halos, rings); compile = 1 also builds the
- * kernel with NVRTC for sm_100a (no GPU needed). */
-int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int len, int compile);
+/* JSON description of the sweep plan (lags, halos, rings, load mode) and its compulsory
+ * DRAM bytes — every array the run loads read once, every live output written once
+ * (redirects mark dead outputs as in ooc_launch_sweep; may be NULL); compile = 1 also
+ * builds the kernel with NVRTC for sm_100a (no GPU needed). */
+int ooc_sweep_describe(const ooc_loop* loops, int n, const ooc_redirect* redirects, int nredirects, char* log,
+                       int len, int compile);
 /* JSON: the prefetch depth chosen per sweep structure and the measured ms per candidate. */
 int ooc_sweep_report(char* buf, int len);
 
@@ -239,6 +242,14 @@ typedef struct {
 } ooc_xfer;
 int ooc_comm_unique_id(void* out128);
 int ooc_comm_init(ooc_ctx* ctx, int rank, int world, const void* id128);
+/* CUDA-IPC transport (new): the ranks of one node rendezvous in a POSIX shared-memory
+ * segment named by `name` (same string on every rank, unique per job); exchanges pack
+ * the sends into a device outbox the peers map with cudaIpcOpenMemHandle and pull from
+ * after a host barrier (peer-to-peer over NVLink; a device copy when ranks share a GPU).
+ * Collective: every rank makes the same sequence of exchange / all-reduce calls. */
+int ooc_comm_init_ipc(ooc_ctx* ctx, int rank, int world, const char* name);
+/* Host barrier of the IPC transport (OOC_ERR_UNSUPPORTED for NCCL communicators). */
+int ooc_comm_barrier(ooc_ctx* ctx);
 int ooc_comm_exchange(ooc_ctx* ctx, int queue, const ooc_xfer* xfers, int n);
 /* All-reduce of one reduction accumulator across the communicator (sum/min/max). */
 int ooc_reduce_allreduce(ooc_ctx* ctx, int queue, int slot, int op);
@@ -257,6 +268,7 @@ typedef struct {
   long long graph_launches;
   long long jit_unsettled;  /* specialised launches made while their shape was still being tuned */
   long long sweep_launches; /* row-sweep launches (ooc_launch_sweep) */
+  long long sweep_host_us;  /* host time spent inside ooc_launch_sweep (plan lookup, parameters, launch) */
 } ooc_dev_stats;
 int ooc_stats(ooc_ctx* ctx, ooc_dev_stats* out);
 int ooc_stats_reset(ooc_ctx* ctx);

@@ -155,6 +155,11 @@ const char* ooc_rt_chain_plan_text(ooc_runtime* rt, int chain, int tiles);
  * ooc_device.h); export a recorded chain's (window-clipped) loops; its ghost depth
  * and the ghost-band exchange it triggers. */
 int ooc_rt_comm_init(ooc_runtime* rt, const void* unique_id128);
+/* Join the CUDA-IPC transport instead of NCCL: the ranks of one node rendezvous in a
+ * shared-memory segment named `name` (same on every rank), ghost bands move by
+ * cudaMemcpyAsync out of the neighbours' IPC-mapped outboxes (NVLink peer copies; ranks
+ * may also share one GPU). */
+int ooc_rt_comm_init_ipc(ooc_runtime* rt, const char* name);
 const char* ooc_rt_chain_export_json(ooc_runtime* rt, int chain);
 const char* ooc_rt_dist_plan_json(ooc_runtime* rt, int chain);
 /* Group recorded chain `chain` as the engine would (fuse = 1: loop fusion) and

@@ -209,6 +209,10 @@ int refo_copy_dataset(void* p, int d, double* out) {
   std::memcpy(out, h.data(), h.size() * sizeof(double));
   return 0;
 }
+// Zero-copy address of the buffer the reference holds (bench parity at full size).
+const double* refo_dataset_ptr(void* p, int d) {
+  return static_cast<Handle*>(p)->rt->mesh().datasets.at(d).host.data();
+}
 // Flushing fetch with the reference's stale semantics (runtime.cpp:13-19).
 int refo_fetch_dataset(void* p, int d, double* out) {
   Runtime& rt = *static_cast<Handle*>(p)->rt;

@@ -49,6 +49,7 @@ def lib():
             "refo_dataset_len": (ll, [vp, i]),
             "refo_dataset_stale": (i, [vp, i]),
             "refo_copy_dataset": (i, [vp, i, dp]),
+            "refo_dataset_ptr": (dp, [vp, i]),
             "refo_fetch_dataset": (i, [vp, i, dp]),
             "refo_fetch_reduction": (i, [vp, cp, dp]),
             "refo_totals": (i, [vp, ctypes.POINTER(ll), dp]),
@@ -121,6 +122,11 @@ class RefRuntime:
         out = np.empty(n, dtype=np.float64)
         lib().refo_copy_dataset(self._h, d, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
         return out
+
+    def host_view(self, d) -> np.ndarray:
+        """Zero-copy view of the reference's host buffer (valid until close())."""
+        n = lib().refo_dataset_len(self._h, d)
+        return np.ctypeslib.as_array(lib().refo_dataset_ptr(self._h, d), shape=(n,))
 
     def stale(self, d) -> bool:
         return bool(lib().refo_dataset_stale(self._h, d))

@@ -336,6 +336,11 @@ class Runtime:
         """Join the NCCL communicator of the slab decomposition (128-byte id)."""
         _check(_native.lib().ooc_rt_comm_init(self._h, unique_id))
 
+    def comm_init_ipc(self, name: str):
+        """Join the CUDA-IPC transport of the slab decomposition (ranks of one node,
+        same `name` on every rank; ranks may share a GPU)."""
+        _check(_native.lib().ooc_rt_comm_init_ipc(self._h, name.encode()))
+
     def chain_export(self, chain):
         """A recorded chain's loops as this rank runs them (window-clipped)."""
         return self._json(_native.lib().ooc_rt_chain_export_json, chain)

@@ -27,9 +27,9 @@ INC = ["-I" + os.path.join(ROOT, "include"), "-I" + os.path.join(CSRC, "include"
 DEV_SRCS = ["device/ooc_device.cu", "device/loop_kernels.cu", "device/jit.cu", "device/sweep.cu",
             "device/comm.cu"]
 HOST_SRCS = ["host/core.cpp", "host/tiler.cpp", "host/runtime.cpp", "host/gpu_engine.cpp",
-             "host/apps.cpp", "host/capi.cpp"]
+             "host/apps.cpp", "host/capi.cpp", "host/metrics.cpp", "host/chain_file.cpp", "host/seams.cpp"]
 HEADERS_DEV = ["device/internal.cuh", "device/jit.cuh"]
-HEADERS_HOST = ["host/json_writer.hpp"] + [os.path.join("include/ooc", h)
+HEADERS_HOST = ["host/json_writer.hpp", "host/json_reader.hpp"] + [os.path.join("include/ooc", h)
                                             for h in os.listdir(os.path.join(CSRC, "include/ooc"))]
 
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

@@ -50,8 +50,10 @@ struct ooc_ctx {
   double* red_part[OOC_NUM_QUEUES] = {nullptr, nullptr, nullptr};
   int red_part_cap = 0;
   ooc_dev_stats stats{};
-  // multi-GPU (comm.cu): NCCL communicator of the slab decomposition
+  // multi-GPU (comm.cu): NCCL communicator of the slab decomposition, or the CUDA-IPC
+  // transport (shared-memory rendezvous + peer-mapped outboxes)
   void* comm = nullptr;
+  void* ipc = nullptr;
   int rank = 0, world = 1;
   long long capture_launches0 = 0;  // kernel-launch count when a graph capture began
 };

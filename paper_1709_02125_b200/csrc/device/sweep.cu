@@ -74,7 +74,7 @@ int ring_cols() {
   }();
   return rc;
 }
-constexpr int kPad = 16;  // doubles of shared memory before/after the rings (edge lanes' neighbour reads)
+constexpr int kPad = 32;  // doubles of shared memory before/after the rings (edge lanes' neighbour reads)
 
 // Parameter block; the kernel source declares an identical struct.
 struct SweepParams {
@@ -111,6 +111,46 @@ __device__ __forceinline__ double ooc_red(int op, double acc, double v) {
 __device__ __forceinline__ long long sw_floordiv(long long a, long long k) {
   return a >= 0 ? a / k : -((-a + k - 1) / k);
 }
+// TMA (bulk async copy) loads: one thread arms an mbarrier with the step's byte count and
+// issues one row copy per loaded dataset; every thread waits on the barrier's phase.
+__device__ __forceinline__ unsigned sw_saddr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void sw_wait(unsigned bar, unsigned parity) {
+  for (unsigned tries = 0;; ++tries) {
+    unsigned done;
+    asm volatile("{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, P1;\n}\n" : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    if (done) return;
+    if (tries > (1u << 28)) asm volatile("trap;");  // a byte count that never completes: a loud launch error, not a hang
+  }
+}
+__device__ __forceinline__ void sw_bulk(unsigned dst, const double* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+struct SwLd {  // one loaded dataset's row copies: source column, rows, ring placement
+  const double* src;
+  long long s0, vrb, nrows;  // view row of ring row u = vrb + u + lagL; rows in [0, nrows)
+  unsigned dst, tn;          // ring byte offset of the copy (row 0), bytes per row copy
+  int wmask, lagL;
+};
+__device__ __noinline__ void sw_issue(const SwLd* t, int nl, int sn, int K, unsigned bar, unsigned sbase, int pitch8) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#pragma unroll 1
+  for (int i = 0; i < nl; ++i) {
+    const SwLd L = t[i];
+    for (int r = 0; r < K; ++r) {
+      const long long vr = L.vrb + static_cast<long long>(sn) * K + r;
+      if (L.tn && vr >= 0 && vr < L.nrows) {
+        const int u = sn * K + r - L.lagL;
+        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(L.tn) : "memory");
+        sw_bulk(sbase + L.dst + static_cast<unsigned>((u & L.wmask) * pitch8), L.src + vr * L.s0, L.tn, bar);
+      }
+    }
+  }
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
 __device__ __forceinline__ void sw_cp8(double* dst, const double* src, bool ok) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(s), "l"(src), "r"(ok ? 8 : 0) : "memory");
@@ -138,6 +178,8 @@ struct SwDs {
 
 struct SwPlan {
   int n = 0, K = 2, P = 2, NT = 256, RC = 128;
+  bool tma = false;  // loads: bulk async copies (one thread, mbarrier ring) instead of per-thread cp.async
+  int RCp = 128;     // ring row pitch in doubles (RC, or RC + 2 with TMA: even-column row copies)
   long long HC = 0, TC = 0, warm = 0, lagS_max = 0, smem = 0;
   int red_op = OOC_RED_NONE;  // the run's last loop reduces (no writes): folded per CTA
   long long red_lag = 0;
@@ -163,12 +205,15 @@ bool fail(std::string* why, const std::string& m) {
 // Analyse a group for the sweep template with K rows per step (NT = 128*K threads)
 // and a P-step load prefetch. Fills the plan (lags, halos, rings, barriers).
 bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* why,
-             const std::vector<const double*>* dead = nullptr) {
+             const std::vector<const double*>* dead = nullptr, bool tma = false) {
   pl = SwPlan{};
   pl.n = n;
   pl.K = K;
   pl.P = P;
   pl.NT = pl.RC = ring_cols();
+  pl.tma = tma;
+  pl.RCp = tma ? pl.RC + 2 : pl.RC;
+  if (tma) pl.NT = pl.RC + 32;  // + one producer warp issuing the bulk-copy loads
   if (n < 1 || n > SW_MAXL) return fail(why, "group size");
   pl.L.resize(static_cast<std::size_t>(n));
   int ncst = 0;
@@ -325,7 +370,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
     D.W = 1;
     while (D.W < std::max<long long>(A + B + 1, K)) D.W *= 2;  // power of two: slot = row & (W-1)
     D.off = off;
-    off += D.W * pl.RC;
+    off += D.W * pl.RCp;
   }
   pl.smem = (off + 2 * kPad) * 8;
   if (pl.smem > smem_budget()) return fail(why, "shared memory");
@@ -413,24 +458,39 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   std::ostringstream o;
   const int nd = static_cast<int>(pl.D.size());
   const int K = pl.K;
+  // barrier among the ring threads (the TMA producer warp only joins the step barriers)
+  const std::string cbar = pl.tma ? "asm volatile(\"bar.sync 1, " + std::to_string(pl.RC) + ";\" ::: \"memory\");"
+                                  : std::string("__syncthreads();");
   o << "#define SW_MAXL " << SW_MAXL << "\n#define SW_MAXD " << SW_MAXD << "\n#define SW_MAXC " << SW_MAXC << "\n";
   o << kSweepDecl;
   static const int min_blocks = [] {
     const char* e = std::getenv("OOC_SWEEP_MINB");
     return e ? std::atoi(e) : 0;
   }();
+  // resident CTAs the shared memory allows (228 KB per SM, 1 KB reserved per CTA): ask
+  // ptxas to fit that many in the register file too
+  const long long smem_occ = std::min<long long>(8, 233472 / (pl.smem + 1024 + 256));
   o << "extern \"C\" __global__ void __launch_bounds__(" << pl.NT;
   if (min_blocks > 0) o << ", " << min_blocks;
+  else if (smem_occ > 1) o << ", " << smem_occ;
   o << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p) {\n";
   o << "  extern __shared__ __align__(16) double sw_sm[];\n";
+  if (pl.tma) o << "  __shared__ __align__(8) unsigned long long sw_bar[8];\n";
   o << "  const int lc = threadIdx.x;\n";
   o << "  double* const B = sw_sm + " << kPad << " + lc;\n";
+  o << "  const long long c0 = p.C0 + static_cast<long long>(blockIdx.x) * " << pl.TC << ";\n";
   // one restrict-qualified base per ring: rings never overlap, so the compiler may move
   // a ring's loads across another ring's stores (instruction-level parallelism)
   static const bool restrict_rings = !(std::getenv("OOC_SWEEP_RESTRICT") && std::atoi(std::getenv("OOC_SWEEP_RESTRICT")) == 0);
-  for (int d = 0; d < nd; ++d)
-    o << "  double* " << (restrict_rings ? "__restrict__ " : "") << "const R" << d << " = B + " << pl.D[static_cast<std::size_t>(d)].off << ";\n";
-  o << "  const long long c0 = p.C0 + static_cast<long long>(blockIdx.x) * " << pl.TC << ";\n";
+  // TMA: a loaded dataset's ring rows start at the even view column at or below the
+  // CTA's first ring column (16-byte aligned row copies); lanes read one element further
+  // when that column is odd
+  for (int d = 0; d < nd; ++d) {
+    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+    o << "  double* " << (restrict_rings ? "__restrict__ " : "") << "const R" << d << " = B + " << D.off;
+    if (pl.tma && D.loaded) o << " + static_cast<int>((c0 - " << pl.HC << " - p.box[" << d << "][2]) & 1)";
+    o << ";\n";
+  }
   o << "  const long long r_own0 = p.R0 + static_cast<long long>(blockIdx.y) * p.seg_rows;\n";
   o << "  const long long r_own1 = min(p.R1, r_own0 + p.seg_rows);\n";
   o << "  const long long rbase = r_own0 - " << pl.warm << ";\n";
@@ -486,11 +546,18 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   }
   for (int d = 0; d < nd; ++d) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
-    if (D.loaded)
+    if (D.loaded && !pl.tma)
       o << "  const bool colok" << d << " = c >= p.box[" << d << "][2] && c < p.box[" << d << "][3];\n";
     if (D.store) {
       o << "  if (own_col && c >= p.box[" << d << "][2] && c < p.box[" << d << "][3]) stmask |= 1u << " << d << ";\n";
     }
+  }
+  if (pl.tma) {
+    o << "  if (threadIdx.x == " << pl.RC << ") {\n";
+    o << "    for (int b = 0; b < 8; ++b)\n";
+    o << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(sw_saddr(&sw_bar[b])) : \"memory\");\n";
+    o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+    o << "  }\n  __syncthreads();\n";
   }
   o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
@@ -498,7 +565,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   auto at = [&](int d, const std::string& u, long long q, long long oc) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     std::ostringstream e;
-    e << "R" << d << "[(((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RC;
+    e << "R" << d << "[(((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RCp;
     if (oc) e << " + (" << oc << ")";
     e << "]";
     return e.str();
@@ -507,14 +574,15 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // current step touches; advanced by K rows per step
   for (int d = 0; d < nd; ++d) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
-    if (D.loaded)
+    if (D.loaded && !pl.tma)
       o << "  long long gl" << d << " = (rbase + " << static_cast<long long>(pl.P) * K - D.lagL << " - p.box[" << d
         << "][0]) * p.s0[" << d << "] + (c - p.box[" << d << "][2]);\n";
     if (D.store)
-      o << "  long long gs" << d << " = (rbase - " << D.lagS << " - p.box[" << d << "][0]) * p.s0[" << d
+      o << "  double* gs" << d << " = p.dst[" << d << "] + (rbase - " << D.lagS << " - p.box[" << d << "][0]) * p.s0[" << d
         << "] + (c - p.box[" << d << "][2]);\n";
   }
   auto loads = [&](const std::string& step, const char* ind, bool fast, bool running) {
+    if (pl.tma) return;  // issued once per step by one thread (tma_issue)
     for (int d = 0; d < nd; ++d) {
       const SwDs& D = pl.D[static_cast<std::size_t>(d)];
       if (!D.loaded) continue;
@@ -538,7 +606,57 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     }
     o << ind << "asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n";
   };
-  for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false, false);
+  // TMA issue of the rows of step `step` (thread 0): per loaded dataset and row, one bulk
+  // copy of the ring's columns clipped to the view (even start and length: 16-byte
+  // aligned), completing on mbarrier step & 7. Rows outside the view are not copied:
+  // nothing in range reads them (validate_loop), so stale ring contents only reach
+  // values that are never stored.
+  // TMA issue of the rows of step `step` (thread 0, sw_issue): per loaded dataset and row,
+  // one bulk copy of the ring's columns clipped to the view (even start and length:
+  // 16-byte aligned) from the CTA's descriptor table, completing on mbarrier step & 7.
+  // Rows outside the view are not copied: nothing in range reads them (validate_loop), so
+  // stale ring contents only reach values that are never stored.
+  int nload = 0;
+  for (const SwDs& D : pl.D) nload += D.loaded ? 1 : 0;
+  auto tma_issue = [&](const std::string& step, const char* ind) {
+    o << ind << "if (threadIdx.x == " << pl.RC << " && (" << step << ") < nsteps) sw_issue(sw_ld, " << nload << ", " << step << ", " << K
+      << ", sw_saddr(sw_bar) + static_cast<unsigned>(((" << step << ") & 7) * 8), sw_saddr(sw_sm), " << pl.RCp * 8 << ");\n";
+  };
+  if (pl.tma) {  // the CTA's load descriptors (computed once by the issuing thread)
+    o << "  __shared__ SwLd sw_ld[" << std::max(nload, 1) << "];\n";
+    o << "  if (threadIdx.x == " << pl.RC << ") {\n";
+    int i = 0;
+    for (int d = 0; d < nd; ++d) {
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (!D.loaded) continue;
+      const std::string ds = std::to_string(d);
+      o << "    {\n";
+      o << "      const long long cs = c0 - " << pl.HC << " - p.box[" << ds << "][2];\n";
+      o << "      const long long a0 = cs > 0 ? (cs & ~1LL) : 0LL;\n";
+      o << "      const long long a1 = (min(cs + " << pl.RC << "LL, p.box[" << ds << "][3] - p.box[" << ds << "][2]) + 1) & ~1LL;\n";
+      o << "      SwLd& L = sw_ld[" << i << "];\n";
+      o << "      L.src = p.src[" << ds << "] + a0;\n      L.s0 = p.s0[" << ds << "];\n";
+      o << "      L.vrb = rbase - p.box[" << ds << "][0] - " << D.lagL << ";\n";
+      o << "      L.nrows = p.box[" << ds << "][1] - p.box[" << ds << "][0];\n";
+      o << "      L.dst = static_cast<unsigned>((" << kPad + D.off << " + a0 - (cs - (cs & 1))) * 8);\n";
+      o << "      L.tn = a1 > a0 ? static_cast<unsigned>(a1 - a0) * 8u : 0u;\n";
+      o << "      L.wmask = " << D.W - 1 << ";\n      L.lagL = " << D.lagL << ";\n";
+      o << "    }\n";
+      ++i;
+    }
+    o << "  }\n";
+  }
+  if (pl.tma) {
+    // the producer warp: loads of steps 0..P-1, then per step (after the consumers'
+    // step barrier, which frees the ring rows the next loads overwrite) those of step s+P;
+    // the consumers' other barriers are named barrier 1 over the ring threads only
+    for (int t = 0; t < pl.P; ++t) tma_issue(std::to_string(t), "  ");
+    o << "  if (threadIdx.x >= " << pl.RC << ") {\n";
+    o << "    for (int s = 0; s < nsteps; ++s) {\n      __syncthreads();\n";
+    tma_issue("s + " + std::to_string(pl.P), "      ");
+    o << "    }\n    return;\n  }\n";
+  } else
+    for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false, false);
   int ci0 = 0;
   // ---- fast steps: rows r = 0..K-1 unrolled at generation so values stay in named
   // registers across loops. A read of a value this thread produced earlier in the step
@@ -604,10 +722,10 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // their fast-step writes skip the shared-memory store, and the last fast step spills
   // the carries so the predicated steps after it find the rows in the ring
   std::vector<char> no_smem(static_cast<std::size_t>(nd), 0);
-  auto fast_body = [&](FastInfo* info) {
+  auto fast_body = [&](FastInfo* info, const std::string& uexpr) {
     const char* ind = "      ";
     loads("s + " + std::to_string(pl.P), ind, true, true);
-    o << ind << "const int u = s * " << K << ";\n";
+    o << ind << "const int u = " << uexpr << ";\n";
     std::map<std::tuple<int, long long, long long>, std::string> cache;  // (d, row, col) -> register
     std::set<Key> touched;
     if (info) info->miss.assign(static_cast<std::size_t>(nd), 0);
@@ -622,7 +740,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     for (int i = 0; i < pl.n; ++i) {
       const ooc_loop& L = Ls[i];
       const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
-      if (S.barrier) o << ind << "__syncthreads();\n";
+      if (S.barrier) o << ind << cbar << "\n";
       o << ind << "// loop " << i << " (lag " << S.lag << ", halo " << S.h << ")\n";
       int dsof_arg[OOC_MAX_ARGS];
       for (int a = 0; a < L.nargs; ++a) {
@@ -709,7 +827,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
                       : cache.end();
         if (it == cache.end() && info) info->miss[static_cast<std::size_t>(d)] = 1;
         const std::string v = it != cache.end() ? it->second : at(d, "u", r - D.lagS, 0);
-        o << ind << "  p.dst[" << ds << "][gs" << ds << " + " << r << " * p.s0[" << ds << "]] = " << v << ";\n";
+        o << ind << "  gs" << ds << "[" << r << " * p.s0[" << ds << "]] = " << v << ";\n";
       }
       o << ind << "}\n";
     }
@@ -738,7 +856,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       info = FastInfo{};
       std::ostringstream keep;
       std::swap(o, keep);
-      fast_body(&info);
+      fast_body(&info, "s * " + std::to_string(K));
       std::swap(o, keep);
       std::vector<Key> next;
       for (const Key& k : info.first_read)
@@ -763,7 +881,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     for (int i = 0; i < pl.n; ++i) {
       const ooc_loop& L = Ls[i];
       const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
-      if (S.barrier) o << ind << "__syncthreads();\n";
+      if (S.barrier) o << ind << cbar << "\n";
       const std::string is = std::to_string(i);
       if (fast)
         o << ind << "{  // loop " << i << " (lag " << S.lag << ", halo " << S.h << ")\n";
@@ -848,31 +966,72 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         }
         o << ")\n";
       }
-      o << ind << "      p.dst[" << ds << "][gs" << ds << " + r * p.s0[" << ds << "]] = " << at(d, "u + r", -D.lagS, 0)
+      o << ind << "      gs" << ds << "[r * p.s0[" << ds << "]] = " << at(d, "u + r", -D.lagS, 0)
         << ";\n" << ind << "  }\n" << ind << "}\n";
     }
   };
-  o << "  for (int s = 0; s < nsteps; ++s) {\n";
-  o << "    asm volatile(\"cp.async.wait_group " << pl.P - 1 << ";\" ::: \"memory\");\n";
-  o << "    __syncthreads();\n";
+  auto step_top = [&](const std::string& ind) {
+    if (pl.tma) {
+      o << ind << "sw_wait(sw_saddr(sw_bar) + static_cast<unsigned>((s & 7) * 8), static_cast<unsigned>((s >> 3) & 1));\n";
+      o << ind << "__syncthreads();\n";
+    } else {
+      o << ind << "asm volatile(\"cp.async.wait_group " << pl.P - 1 << ";\" ::: \"memory\");\n";
+      o << ind << "__syncthreads();\n";
+    }
+  };
+  auto advance = [&](const std::string& ind) {
+    for (int d = 0; d < nd; ++d) {
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (D.loaded && !pl.tma) o << ind << "gl" << d << " += " << K << " * p.s0[" << d << "];\n";
+      if (D.store) o << ind << "gs" << d << " += " << K << " * p.s0[" << d << "];\n";
+    }
+  };
+  // Unrolled fast steps: U consecutive steps starting at a multiple of U, U a power of
+  // two >= every ring length (and >= the 8 load barriers). Every ring slot
+  // ((u + q) & (W - 1)) and barrier index then folds to a constant, so the interior
+  // sweep addresses shared memory with immediate offsets instead of per-step slot
+  // arithmetic (OOC_SWEEP_UNROLL=0 disables).
+  static const int unroll_env = [] {
+    const char* e = std::getenv("OOC_SWEEP_UNROLL");
+    return e ? std::atoi(e) : 1;
+  }();
+  long long U = pl.tma ? 8 : 1;
+  for (const SwDs& D : pl.D) U = std::max(U, D.W);
+  if (unroll_env == 0 || U > 16) U = 0;
+  int logU = 0;
+  while (U > 0 && (1LL << logU) < U) ++logU;
+  o << "  for (int s = 0; s < nsteps;) {\n";
+  if (U > 1) {
+    o << "    if (strip_in && (s & " << U - 1 << ") == 0 && s >= s_lo && s + " << U << " <= s_hi) {\n";
+    o << "      const int sbl = s >> " << logU << ";\n";
+    for (long long j = 0; j < U; ++j) {
+      o << "      {  // unrolled fast step " << j << "\n";
+      o << "        const int s = (sbl << " << logU << ") + " << j << ";\n";
+      step_top("        ");
+      o << "        {\n";
+      fast_body(nullptr, "((sbl << " + std::to_string(logU) + ") + " + std::to_string(j) + ") * " + std::to_string(K));
+      o << "        }\n";
+      advance("        ");
+      o << "      }\n";
+    }
+    o << "      s += " << U << ";\n      continue;\n    }\n";
+  }
+  step_top("    ");
   o << "    if (strip_in && s >= s_lo && s < s_hi) {\n";
-  fast_body(nullptr);
+  fast_body(nullptr, "s * " + std::to_string(K));
   o << "    } else {\n";
   body(false);
   o << "      prev_fast = false;\n    }\n";
-  for (int d = 0; d < nd; ++d) {
-    const SwDs& D = pl.D[static_cast<std::size_t>(d)];
-    if (D.loaded) o << "    gl" << d << " += " << K << " * p.s0[" << d << "];\n";
-    if (D.store) o << "    gs" << d << " += " << K << " * p.s0[" << d << "];\n";
-  }
-  o << "  }\n  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
+  advance("    ");
+  o << "    ++s;\n  }\n";
+  if (!pl.tma) o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
   if (pl.red_op != OOC_RED_NONE) {  // warp tree, then the CTA's warps in order: one partial per CTA
     o << "#pragma unroll\n  for (int w = 16; w > 0; w >>= 1) racc = ooc_red(" << pl.red_op
       << ", racc, __shfl_down_sync(0xffffffffu, racc, w));\n";
-    o << "  __shared__ double red_warp[" << pl.NT / 32 << "];\n";
-    o << "  if ((threadIdx.x & 31) == 0) red_warp[threadIdx.x >> 5] = racc;\n  __syncthreads();\n";
+    o << "  __shared__ double red_warp[" << pl.RC / 32 << "];\n";
+    o << "  if ((threadIdx.x & 31) == 0) red_warp[threadIdx.x >> 5] = racc;\n  " << cbar << "\n";
     o << "  if (threadIdx.x == 0) {\n    double b = red_warp[0];\n";
-    o << "    for (int w = 1; w < " << pl.NT / 32 << "; ++w) b = ooc_red(" << pl.red_op << ", b, red_warp[w]);\n";
+    o << "    for (int w = 1; w < " << pl.RC / 32 << "; ++w) b = ooc_red(" << pl.red_op << ", b, red_warp[w]);\n";
     o << "    p.part[static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x] = b;\n  }\n";
   }
   o << "}\n";
@@ -885,7 +1044,6 @@ struct SwKernel {
   bool ok = false;
   std::string err;
 };
-std::unordered_map<std::string, SwKernel> g_sw_cache;
 std::mutex g_sw_mu;
 
 int sweep_K() {
@@ -905,6 +1063,196 @@ int sweep_P() {
   }();
   return pp;
 }
+// bulk-copy (TMA) loads: on unless OOC_SWEEP_TMA=0 (then per-thread cp.async)
+bool sweep_tma() {
+  static const bool t = !(std::getenv("OOC_SWEEP_TMA") && std::atoi(std::getenv("OOC_SWEEP_TMA")) == 0);
+  return t;
+}
+
+// ---- structural key of a run: everything analyze() and generate() depend on — loop
+// ranges, each argument's dataset identity (first-seen order of view pointers) and view
+// box, the tapes without constant values, the dead datasets — hashed to 128 bits, so a
+// launch of a known structure does no analysis, code generation or string hashing.
+struct Key128 {
+  std::uint64_t a = 0, b = 0;
+  bool operator==(const Key128& o) const { return a == o.a && b == o.b; }
+};
+struct Key128Hash {
+  std::size_t operator()(const Key128& k) const { return static_cast<std::size_t>(k.a ^ (k.b * 0x9E3779B97F4A7C15ull)); }
+};
+struct KeyMix {
+  std::uint64_t a = 1469598103934665603ull, b = 0x6a09e667f3bcc909ull;
+  void put(long long v) {
+    const std::uint64_t x = static_cast<std::uint64_t>(v);
+    a = (a ^ x) * 1099511628211ull;
+    b ^= x + 0x9E3779B97F4A7C15ull + (b << 6) + (b >> 2);
+    b *= 0xff51afd7ed558ccdull;
+  }
+};
+// tma_ok: every view 16-byte aligned with an even row stride (bulk-copy requirement)
+Key128 run_key(const ooc_loop* Ls, int n, const ooc_redirect* red, int nred, bool with_dead, bool* tma_ok) {
+  KeyMix m;
+  const double* ids[2 * SW_MAXD];
+  int nids = 0;
+  bool al = true;
+  auto id_of = [&](const double* p) {
+    for (int k = 0; k < nids; ++k)
+      if (ids[k] == p) return k;
+    if (nids < 2 * SW_MAXD) ids[nids++] = p;
+    return nids - 1;
+  };
+  m.put(n);
+  m.put(ring_cols());
+  for (int i = 0; i < n; ++i) {
+    const ooc_loop& L = Ls[i];
+    m.put(L.ndim);
+    for (int k = 0; k < 3; ++k) {
+      m.put(L.lo[k]);
+      m.put(L.hi[k]);
+    }
+    m.put(L.nargs);
+    for (int a = 0; a < L.nargs && a < OOC_MAX_ARGS; ++a) {
+      const ooc_view& v = L.args[a];
+      m.put(id_of(v.data));
+      for (int k = 0; k < 3; ++k) {
+        m.put(v.lo[k]);
+        m.put(v.hi[k]);
+        m.put(v.stride[k]);
+      }
+      al = al && (reinterpret_cast<std::uintptr_t>(v.data) & 15) == 0 && (v.stride[0] & 1) == 0;
+    }
+    m.put(L.ntape);
+    for (int t = 0; t < L.ntape; ++t) {
+      const ooc_ins& in = L.tape[t];
+      m.put(in.op);
+      m.put(in.op == OOC_OP_CONST ? 0 : in.arg);
+      m.put(in.offset[0]);
+      m.put(in.offset[1]);
+      m.put(in.offset[2]);
+    }
+    m.put(L.nwrites);
+    for (int w = 0; w < L.nwrites && w < OOC_MAX_WRITES; ++w) {
+      m.put(L.write_arg[w]);
+      m.put(L.write_len[w]);
+    }
+    m.put(L.reduce_op);
+    m.put(L.reduce_len);
+  }
+  if (with_dead)
+    for (int r = 0; r < nred; ++r)
+      if (!red[r].dst) m.put(1000 + id_of(red[r].src));
+  const bool tma = al && sweep_tma();
+  m.put(tma ? 1 : 0);
+  if (tma_ok) *tma_ok = tma;
+  return {m.a, m.b};
+}
+
+// One specialisation of a structure: a prefetch depth, its plan, source and kernel.
+struct SwVar {
+  int P = 0;
+  SwPlan pl;
+  SwKernel k;
+  bool built = false;
+};
+// Prefetch-depth autotuning per structure: every depth whose rings fit the budget is
+// timed on real launches (CUDA events, two rounds, the faster counts) and the fastest
+// kept — the same scheme as the tile shapes of jit.cu.
+struct SwTune {
+  std::vector<int> cands;  // indexes into SwEntry::vars
+  std::vector<float> ms;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<char> issued;
+  int best = -1;
+};
+struct SwEntry {
+  bool init = false, ok = false;
+  std::string why;
+  std::vector<std::pair<int, int>> first;  // per plan dataset: (loop, arg) of a view of it
+  std::vector<SwVar> vars;
+  int def = 0;  // the default / forced depth
+  SwTune tune;
+  int loops = 0;
+  bool tma = false;
+  std::size_t gen_hash = 0;  // hash of the kernel source at the default depth (generator version + structure)
+};
+std::unordered_map<Key128, SwEntry, Key128Hash> g_sw_entries;
+// ooc_sweep_check results per structure (no dead-store information involved)
+struct SwCheck {
+  bool ok = false;
+  std::vector<int> flags;
+};
+std::unordered_map<Key128, SwCheck, Key128Hash> g_sw_checks;
+
+void rebind(SwPlan& pl, const std::vector<std::pair<int, int>>& first, const ooc_loop* Ls) {
+  for (std::size_t d = 0; d < pl.D.size(); ++d) pl.D[d].v = &Ls[first[d].first].args[first[d].second];
+}
+
+bool init_entry(SwEntry& E, const ooc_loop* loops, int n, const ooc_redirect* red, int nred, bool tma) {
+  E.init = true;
+  E.loops = n;
+  E.tma = tma;
+  std::vector<const double*> dead;
+  for (int r = 0; r < nred; ++r)
+    if (!red[r].dst) dead.push_back(red[r].src);
+  SwPlan pl;
+  if (!analyze(loops, n, sweep_K(), sweep_P(), pl, &E.why, &dead, tma)) return E.ok = false;
+  for (const SwDs& D : pl.D) {
+    std::pair<int, int> f{-1, -1};
+    for (int i = 0; i < n && f.first < 0; ++i)
+      for (int a = 0; a < loops[i].nargs; ++a)
+        if (&loops[i].args[a] == D.v) f = {i, a};
+    if (f.first < 0) {
+      E.why = "dataset view not found";
+      return E.ok = false;
+    }
+    E.first.push_back(f);
+  }
+  E.gen_hash = std::hash<std::string>{}(generate(loops, pl, nullptr));
+  if (sweep_P_forced()) {
+    SwVar v;
+    v.P = pl.P;
+    v.pl = pl;
+    E.vars.push_back(v);
+    E.def = 0;
+    E.tune.best = 0;
+    E.tune.cands = {0};
+    E.tune.ms = {0.f};
+  } else {
+    for (int P = 1; P <= 4; ++P) {
+      SwVar v;
+      v.P = P;
+      if (P == pl.P) {
+        v.pl = pl;
+      } else if (!analyze(loops, n, sweep_K(), P, v.pl, nullptr, &dead, tma)) {
+        continue;
+      }
+      if (P == pl.P) E.def = static_cast<int>(E.vars.size());
+      E.vars.push_back(v);
+    }
+    for (int round = 0; round < 2; ++round)  // two timed launches per depth: the faster counts
+      for (std::size_t i = 0; i < E.vars.size(); ++i) E.tune.cands.push_back(static_cast<int>(i));
+    E.tune.ms.assign(E.tune.cands.size(), -1.f);
+    E.tune.ev.assign(E.tune.cands.size(), {nullptr, nullptr});
+    E.tune.issued.assign(E.tune.cands.size(), 0);
+    if (E.vars.size() <= 1) E.tune.best = 0;
+  }
+  return E.ok = true;
+}
+
+void resolve_tuning(SwTune& T) {  // timings that finished since the last launch (no blocking)
+  if (T.best >= 0) return;
+  bool all = !T.cands.empty();
+  for (std::size_t i = 0; i < T.cands.size(); ++i) {
+    if (T.ms[i] < 0 && T.issued[i] && cudaEventQuery(T.ev[i].second) == cudaSuccess)
+      cudaEventElapsedTime(&T.ms[i], T.ev[i].first, T.ev[i].second);
+    all = all && T.ms[i] >= 0;
+  }
+  if (all) {
+    T.best = 0;
+    for (std::size_t i = 1; i < T.ms.size(); ++i)
+      if (T.ms[i] < T.ms[static_cast<std::size_t>(T.best)]) T.best = static_cast<int>(i);
+  }
+}
 
 }  // namespace
 
@@ -917,36 +1265,49 @@ extern "C" int ooc_sweep_check(const ooc_loop* loops, int n, int* oop_args) {
   if (m == 0) return 0;
   if (m == 1 && static_cast<long long>(loops[0].hi[0] - loops[0].lo[0]) * (loops[0].hi[1] - loops[0].lo[1]) < min_pts)
     return 0;
-  SwPlan pl;
-  std::string why;
-  const bool ok = analyze(loops, n, sweep_K(), sweep_P(), pl, &why);
-  static const bool dbg = std::getenv("OOC_SWEEP_DEBUG") != nullptr;
-  if (dbg && !ok && n > 1) std::fprintf(stderr, "sweep: %d loops rejected: %s\n", n, why.c_str());
-  if (!ok) return 0;
-  if (oop_args)
-    for (int i = 0; i < n; ++i)
-      for (int a = 0; a < OOC_MAX_ARGS; ++a) {
-        int f = 0;
-        if (a < loops[i].nargs)
+  bool tma = false;
+  const Key128 key = run_key(loops, n, nullptr, 0, false, &tma);
+  std::lock_guard<std::mutex> lk(g_sw_mu);
+  auto it = g_sw_checks.find(key);
+  if (it == g_sw_checks.end()) {
+    SwCheck ck;
+    SwPlan pl;
+    std::string why;
+    ck.ok = analyze(loops, n, sweep_K(), sweep_P(), pl, &why, nullptr, tma);
+    static const bool dbg = std::getenv("OOC_SWEEP_DEBUG") != nullptr;
+    if (dbg && !ck.ok && n > 1) std::fprintf(stderr, "sweep: %d loops rejected: %s\n", n, why.c_str());
+    if (ck.ok) {
+      ck.flags.assign(static_cast<std::size_t>(n) * OOC_MAX_ARGS, 0);
+      for (int i = 0; i < n; ++i)
+        for (int a = 0; a < loops[i].nargs && a < OOC_MAX_ARGS; ++a)
           for (const SwDs& D : pl.D)
             if (D.v->data == loops[i].args[a].data)
-              f = (D.oop ? 1 : 0) | (D.loaded ? 2 : 0) | (D.written ? 4 : 0);
-        oop_args[i * OOC_MAX_ARGS + a] = f;
-      }
+              ck.flags[static_cast<std::size_t>(i) * OOC_MAX_ARGS + a] = (D.oop ? 1 : 0) | (D.loaded ? 2 : 0) | (D.written ? 4 : 0);
+    }
+    it = g_sw_checks.emplace(key, std::move(ck)).first;
+  }
+  if (!it->second.ok) return 0;
+  if (oop_args) std::memcpy(oop_args, it->second.flags.data(), it->second.flags.size() * sizeof(int));
   return 1;
 }
 
-extern "C" int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int len, int compile) {
-  OOC_ARG_CHECK(loops && n > 0, "ooc_sweep_describe: bad args");
+extern "C" int ooc_sweep_describe(const ooc_loop* loops, int n, const ooc_redirect* red, int nred, char* log,
+                                  int len, int compile) {
+  OOC_ARG_CHECK(loops && n > 0 && (red || nred == 0), "ooc_sweep_describe: bad args");
   SwPlan pl;
   std::string why;
-  if (!analyze(loops, n, sweep_K(), sweep_P(), pl, &why)) {
+  bool tma = false;
+  run_key(loops, n, nullptr, 0, false, &tma);
+  std::vector<const double*> dead;
+  for (int r = 0; r < nred; ++r)
+    if (!red[r].dst) dead.push_back(red[r].src);
+  if (!analyze(loops, n, sweep_K(), sweep_P(), pl, &why, &dead, tma)) {
     if (log && len > 0) std::snprintf(log, static_cast<size_t>(len), "%s", why.c_str());
     return OOC_ERR_UNSUPPORTED;
   }
   std::ostringstream o;
-  o << "{\"loops\":" << n << ",\"K\":" << pl.K << ",\"P\":" << pl.P << ",\"HC\":" << pl.HC << ",\"TC\":" << pl.TC
-    << ",\"warm\":" << pl.warm << ",\"smem\":" << pl.smem << ",\"lags\":[";
+  o << "{\"loops\":" << n << ",\"K\":" << pl.K << ",\"P\":" << pl.P << ",\"tma\":" << (pl.tma ? 1 : 0)
+    << ",\"HC\":" << pl.HC << ",\"TC\":" << pl.TC << ",\"warm\":" << pl.warm << ",\"smem\":" << pl.smem << ",\"lags\":[";
   for (int i = 0; i < n; ++i) o << (i ? "," : "") << pl.L[static_cast<std::size_t>(i)].lag;
   o << "],\"halos\":[";
   for (int i = 0; i < n; ++i) o << (i ? "," : "") << pl.L[static_cast<std::size_t>(i)].h;
@@ -956,9 +1317,36 @@ extern "C" int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int l
   for (std::size_t d = 0; d < pl.D.size(); ++d) {
     const SwDs& D = pl.D[d];
     o << (d ? "," : "") << "{\"loaded\":" << D.loaded << ",\"written\":" << D.written << ",\"oop\":" << D.oop
-      << ",\"lagL\":" << D.lagL << ",\"lagS\":" << D.lagS << ",\"W\":" << D.W << "}";
+      << ",\"store\":" << D.store << ",\"lagL\":" << D.lagL << ",\"lagS\":" << D.lagS << ",\"W\":" << D.W << "}";
   }
-  o << "]}";
+  // compulsory DRAM bytes of one launch: loaded arrays over the rows the sweep visits,
+  // live outputs over what the kernel stores (out of place: the whole launch box)
+  long long loaded = 0, stored = 0;
+  for (const SwDs& D : pl.D) {
+    const ooc_view& v = *D.v;
+    const long long cols = v.hi[1] - v.lo[1];
+    if (D.loaded) {
+      const long long r0 = std::max<long long>(v.lo[0], pl.box[0] - pl.warm), r1 = std::min<long long>(v.hi[0], pl.box[1]);
+      loaded += std::max<long long>(0, r1 - r0) * cols * 8;
+    }
+    if (D.store) {
+      long long b[4] = {pl.box[0], pl.box[1], pl.box[2], pl.box[3]};
+      if (!D.oop) {  // in place: the writers' ranges
+        b[0] = b[2] = LLONG_MAX;
+        b[1] = b[3] = LLONG_MIN;
+        for (int j : D.writers) {
+          b[0] = std::min<long long>(b[0], loops[j].lo[0]);
+          b[1] = std::max<long long>(b[1], loops[j].hi[0]);
+          b[2] = std::min<long long>(b[2], loops[j].lo[1]);
+          b[3] = std::max<long long>(b[3], loops[j].hi[1]);
+        }
+      }
+      const long long rr = std::min<long long>(b[1], v.hi[0]) - std::max<long long>(b[0], v.lo[0]);
+      const long long cc = std::min<long long>(b[3], v.hi[1]) - std::max<long long>(b[2], v.lo[1]);
+      stored += std::max<long long>(0, rr) * std::max<long long>(0, cc) * 8;
+    }
+  }
+  o << "],\"dram_bytes\":{\"loaded\":" << loaded << ",\"stored\":" << stored << "}}";
   std::string out = o.str();
   if (compile) {
     const std::string src = generate(loops, pl, nullptr);
@@ -978,42 +1366,23 @@ extern "C" int ooc_sweep_describe(const ooc_loop* loops, int n, char* log, int l
   return OOC_OK;
 }
 
-namespace {
-// Prefetch-depth autotuning per sweep structure (the run's kernel source at the default
-// depth): every depth whose rings fit the budget is tried on one real launch, timed with
-// CUDA events, and the fastest is kept — the same scheme as the tile shapes of jit.cu.
-struct SwTune {
-  std::vector<int> cands;
-  std::vector<float> ms;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-  std::vector<char> issued;
-  int best = -1;
-  int loops = 0;
-};
-std::unordered_map<std::string, SwTune> g_sw_tune;
-}  // namespace
-
 extern "C" int ooc_sweep_report(char* buf, int len) {
   std::lock_guard<std::mutex> lk(g_sw_mu);
   std::ostringstream o;
   o << "[";
   bool first = true;
-  for (auto& [key, T] : g_sw_tune) {
-    bool all = !T.cands.empty();
-    for (std::size_t i = 0; i < T.cands.size(); ++i) {  // timings that finished since the last launch
-      if (T.ms[i] < 0 && T.issued[i] && cudaEventQuery(T.ev[i].second) == cudaSuccess)
-        cudaEventElapsedTime(&T.ms[i], T.ev[i].first, T.ev[i].second);
-      all = all && T.ms[i] >= 0;
-    }
-    if (T.best < 0 && all) {
-      T.best = 0;
-      for (std::size_t i = 1; i < T.ms.size(); ++i)
-        if (T.ms[i] < T.ms[static_cast<std::size_t>(T.best)]) T.best = static_cast<int>(i);
-    }
-    o << (first ? "" : ",") << "{\"loops\":" << T.loops << ",\"key\":\"" << std::hex
-      << std::hash<std::string>{}(key) << std::dec << "\",\"P\":" << (T.best >= 0 ? T.cands[static_cast<std::size_t>(T.best)] : -1)
-      << ",\"ms\":[";
-    for (std::size_t i = 0; i < T.cands.size(); ++i) o << (i ? "," : "") << "[" << T.cands[i] << "," << T.ms[i] << "]";
+  for (auto& [key, E] : g_sw_entries) {
+    if (!E.ok) continue;
+    SwTune& T = E.tune;
+    resolve_tuning(T);
+    const int best = T.best >= 0 ? T.cands[static_cast<std::size_t>(T.best)] : -1;
+    o << (first ? "" : ",") << "{\"loops\":" << E.loops << ",\"key\":\"" << std::hex << key.a << std::dec
+      << "\",\"gen_hash\":\"" << std::hex << E.gen_hash << std::dec
+      << "\",\"tma\":" << (E.tma ? 1 : 0) << ",\"P\":" << (best >= 0 ? E.vars[static_cast<std::size_t>(best)].P : -1)
+      << ",\"smem\":" << (best >= 0 ? E.vars[static_cast<std::size_t>(best)].pl.smem : -1)
+      << ",\"occ\":" << (best >= 0 ? E.vars[static_cast<std::size_t>(best)].k.occ : -1) << ",\"ms\":[";
+    for (std::size_t i = 0; i < T.cands.size(); ++i)
+      o << (i ? "," : "") << "[" << E.vars[static_cast<std::size_t>(T.cands[i])].P << "," << T.ms[i] << "]";
     o << "]}";
     first = false;
   }
@@ -1025,143 +1394,116 @@ extern "C" int ooc_sweep_report(char* buf, int len) {
 extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n, const ooc_redirect* red,
                                 int nred) {
   OOC_ARG_CHECK(c && loops && n > 0 && q >= 0 && q < OOC_NUM_QUEUES, "ooc_launch_sweep: bad args");
-  std::vector<const double*> dead;
-  for (int r = 0; r < nred; ++r)
-    if (!red[r].dst) dead.push_back(red[r].src);
-  SwPlan pl;
-  std::string why;
-  if (!analyze(loops, n, sweep_K(), sweep_P(), pl, &why, &dead)) {
-    set_error("ooc_launch_sweep: group not sweepable: " + why);
+  const auto host0 = std::chrono::steady_clock::now();
+  bool tma = false;
+  const Key128 key = run_key(loops, n, red, nred, true, &tma);
+  std::unique_lock<std::mutex> lk(g_sw_mu);
+  SwEntry& E = g_sw_entries[key];
+  if (!E.init) init_entry(E, loops, n, red, nred, tma);
+  if (!E.ok) {
+    set_error("ooc_launch_sweep: group not sweepable: " + E.why);
     return OOC_ERR_UNSUPPORTED;
   }
   // ---- prefetch depth: forced (OOC_SWEEP_P), tuned, or being tuned on this launch
-  SwTune* tune = nullptr;
-  int pick = -1;
+  SwTune& T = E.tune;
+  int pick = -1;  // index into T.cands
   bool timing = false;
-  if (!sweep_P_forced()) {
-    std::lock_guard<std::mutex> lk(g_sw_mu);
-    tune = &g_sw_tune[generate(loops, pl, nullptr)];
-    SwTune& T = *tune;
-    if (T.cands.empty()) {
-      T.loops = n;
-      for (int round = 0; round < 2; ++round)  // two timed launches per depth: the faster counts
-        for (int P = 1; P <= 4; ++P) {
-          SwPlan tp;
-          if (analyze(loops, n, sweep_K(), P, tp, nullptr, &dead)) T.cands.push_back(P);
-        }
-      T.ms.assign(T.cands.size(), -1.f);
-      T.ev.assign(T.cands.size(), {nullptr, nullptr});
-      T.issued.assign(T.cands.size(), 0);
-      if (T.cands.size() <= 1) T.best = 0;
-    }
-    if (T.best < 0) {  // resolve finished timings without blocking
-      bool all = true;
-      for (std::size_t i = 0; i < T.cands.size(); ++i) {
-        if (T.ms[i] < 0 && T.issued[i] && cudaEventQuery(T.ev[i].second) == cudaSuccess)
-          cudaEventElapsedTime(&T.ms[i], T.ev[i].first, T.ev[i].second);
-        all = all && T.ms[i] >= 0;
-      }
-      if (all) {
-        T.best = 0;
-        for (std::size_t i = 1; i < T.ms.size(); ++i)
-          if (T.ms[i] < T.ms[static_cast<std::size_t>(T.best)]) T.best = static_cast<int>(i);
-      }
-    }
-    if (T.best >= 0) {
-      pick = T.best;
-    } else {
-      c->stats.jit_unsettled++;
-      for (std::size_t i = 0; i < T.cands.size() && pick < 0 && !g_frozen; ++i)
-        if (!T.issued[i]) pick = static_cast<int>(i);
-      timing = pick >= 0;
-      if (pick < 0)  // frozen for a graph capture, or all in flight: fastest measured so far
-        for (std::size_t i = 0; i < T.cands.size(); ++i)
-          if (T.ms[i] >= 0 && (pick < 0 || T.ms[i] < T.ms[static_cast<std::size_t>(pick)])) pick = static_cast<int>(i);
-    }
-    if (pick >= 0 && T.cands[static_cast<std::size_t>(pick)] != pl.P) {
-      if (!analyze(loops, n, sweep_K(), T.cands[static_cast<std::size_t>(pick)], pl, &why, &dead)) {
-        set_error("ooc_launch_sweep: tuned plan failed: " + why);
-        return OOC_ERR_UNSUPPORTED;
-      }
+  resolve_tuning(T);
+  if (T.best >= 0) {
+    pick = T.best;
+  } else {
+    c->stats.jit_unsettled++;
+    for (std::size_t i = 0; i < T.cands.size() && pick < 0 && !g_frozen; ++i)
+      if (!T.issued[i]) pick = static_cast<int>(i);
+    timing = pick >= 0;
+    if (pick < 0)  // frozen for a graph capture, or all in flight: fastest measured so far
+      for (std::size_t i = 0; i < T.cands.size(); ++i)
+        if (T.ms[i] >= 0 && (pick < 0 || T.ms[i] < T.ms[static_cast<std::size_t>(pick)])) pick = static_cast<int>(i);
+    if (pick < 0) {  // nothing measured yet: the default depth, untimed
+      for (std::size_t i = 0; i < T.cands.size() && pick < 0; ++i)
+        if (T.cands[i] == E.def) pick = static_cast<int>(i);
     }
   }
-  auto* sp = new SweepParams;
-  std::memset(sp, 0, sizeof *sp);
-  std::vector<double> cst;
-  const std::string src = generate(loops, pl, &cst);
-  for (std::size_t k = 0; k < cst.size(); ++k) sp->cst[k] = cst[k];
-  sp->R0 = pl.box[0];
-  sp->R1 = pl.box[1];
-  sp->C0 = pl.box[2];
-  sp->C1 = pl.box[3];
-  for (int i = 0; i < n; ++i) {
-    sp->rng[i][0] = loops[i].lo[0];
-    sp->rng[i][1] = loops[i].hi[0];
-    sp->rng[i][2] = loops[i].lo[1];
-    sp->rng[i][3] = loops[i].hi[1];
-  }
-  for (std::size_t d = 0; d < pl.D.size(); ++d) {
-    const SwDs& D = pl.D[d];
-    sp->src[d] = D.v->data;
-    sp->dst[d] = D.v->data;
-    sp->s0[d] = D.v->stride[0];
-    sp->box[d][0] = D.v->lo[0];
-    sp->box[d][1] = D.v->hi[0];
-    sp->box[d][2] = D.v->lo[1];
-    sp->box[d][3] = D.v->hi[1];
-    if (D.oop && D.store) {
-      double* to = nullptr;
-      for (int r = 0; r < nred; ++r)
-        if (red[r].src == D.v->data) to = red[r].dst;
-      if (!to) {
-        delete sp;
-        set_error("ooc_launch_sweep: no out-of-place destination for a dataset the group loads and writes");
-        return OOC_ERR_ARG;
-      }
-      sp->dst[d] = to;
-    }
-  }
+  SwVar& V = E.vars[static_cast<std::size_t>(T.cands[static_cast<std::size_t>(pick)])];
   // test hook: every sweep kernel "fails to build", exercising the engine's fallback
   static const bool fail_build = std::getenv("OOC_SWEEP_FAIL_BUILD") != nullptr;
   if (fail_build) {
-    delete sp;
     set_error("ooc_launch_sweep: build disabled (OOC_SWEEP_FAIL_BUILD)");
     return OOC_ERR_UNSUPPORTED;
   }
-  SwKernel* k = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_sw_mu);
-    SwKernel& e = g_sw_cache[src];
-    if (!e.ok && e.err.empty()) {
-      const auto t0 = std::chrono::steady_clock::now();
-      e.ok = jit_build_kernel(src, "ooc_sweep_kernel", pl.NT, pl.smem, &e.fn, &e.occ, e.err, true);
-      c->stats.jit_compiles++;
-      c->stats.jit_compile_ms += std::chrono::duration_cast<std::chrono::milliseconds>(
-                                     std::chrono::steady_clock::now() - t0).count();
-      if (!e.ok && e.err.empty()) e.err = "build failed";
-    }
-    k = &e;
+  const SwPlan& pl = V.pl;
+  if (!V.built) {
+    V.built = true;
+    rebind(V.pl, E.first, loops);
+    const std::string src = generate(loops, V.pl, nullptr);
+    const auto t0 = std::chrono::steady_clock::now();
+    V.k.ok = jit_build_kernel(src, "ooc_sweep_kernel", pl.NT, pl.smem, &V.k.fn, &V.k.occ, V.k.err, true);
+    c->stats.jit_compiles++;
+    c->stats.jit_compile_ms +=
+        std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (!V.k.ok && V.k.err.empty()) V.k.err = "build failed";
   }
-  if (!k->ok) {
-    delete sp;
-    set_error("ooc_launch_sweep: " + k->err);
+  if (!V.k.ok) {
+    set_error("ooc_launch_sweep: " + V.k.err);
     return OOC_ERR_UNSUPPORTED;
+  }
+  SweepParams sp;  // ~6 KB, filled field by field (constants in tape order)
+  int ci = 0;
+  for (int i = 0; i < n; ++i)
+    for (int t = 0; t < loops[i].ntape; ++t)
+      if (loops[i].tape[t].op == OOC_OP_CONST) sp.cst[ci++] = loops[i].tape[t].value;
+  sp.part = nullptr;
+  sp.R0 = pl.box[0];
+  sp.R1 = pl.box[1];
+  sp.C0 = pl.box[2];
+  sp.C1 = pl.box[3];
+  for (int i = 0; i < n; ++i) {
+    sp.rng[i][0] = loops[i].lo[0];
+    sp.rng[i][1] = loops[i].hi[0];
+    sp.rng[i][2] = loops[i].lo[1];
+    sp.rng[i][3] = loops[i].hi[1];
+  }
+  for (std::size_t d = 0; d < pl.D.size(); ++d) {
+    const SwDs& D = pl.D[d];
+    const ooc_view& v = loops[E.first[d].first].args[E.first[d].second];
+    sp.src[d] = v.data;
+    sp.dst[d] = v.data;
+    sp.s0[d] = v.stride[0];
+    sp.box[d][0] = v.lo[0];
+    sp.box[d][1] = v.hi[0];
+    sp.box[d][2] = v.lo[1];
+    sp.box[d][3] = v.hi[1];
+    if (D.oop && D.store) {
+      double* to = nullptr;
+      for (int r = 0; r < nred; ++r)
+        if (red[r].src == v.data) to = red[r].dst;
+      if (!to) {
+        set_error("ooc_launch_sweep: no out-of-place destination for a dataset the group loads and writes");
+        return OOC_ERR_ARG;
+      }
+      sp.dst[d] = to;
+    }
   }
   const long long rows = pl.box[1] - pl.box[0];
   const long long strips = (pl.box[3] - pl.box[2] + pl.TC - 1) / pl.TC;
   // Row segments per strip: whole waves of CTAs (the grid is strips x segments; a
   // partial last wave idles SMs), at least ~4 waves, segments >= 8 warm-up depths.
-  const long long cap = static_cast<long long>(c->prop.multiProcessorCount) * k->occ;
+  // A reducing run folds one partial per CTA in CTA order, so its partition must not
+  // depend on the tuned depth or the occupancy it allows: it is planned for a fixed
+  // 4 CTAs per SM and depth 2 (reductions are reproducible run to run, box to box).
+  const bool red_run = pl.red_op != OOC_RED_NONE;
+  const long long cap = static_cast<long long>(c->prop.multiProcessorCount) * (red_run ? 4 : V.k.occ);
+  const long long depth_rows = (red_run ? 2 : pl.P) * pl.K;
   const long long min_seg = std::max<long long>(64, 8 * (pl.warm + pl.lagS_max + pl.K));
   const long long max_nseg = std::max<long long>(1, rows / min_seg);
   long long nseg = 1;
   double best = -1.0;
   for (long long ns = 1; ns <= std::min<long long>(max_nseg, 4096); ++ns) {
     const long long seg = (rows + ns - 1) / ns, real = (rows + seg - 1) / seg, ctas = strips * real;
-    if (pl.red_op != OOC_RED_NONE && ctas > c->red_part_cap) break;  // one partial per CTA
+    if (red_run && ctas > c->red_part_cap) break;  // one partial per CTA
     const long long waves = (ctas + cap - 1) / cap;
     // wave efficiency, with a mild preference for >= 4 waves (dynamic balance)
-    const double overhead = static_cast<double>(pl.warm + pl.lagS_max + pl.P * pl.K);  // rows swept, not stored
+    const double overhead = static_cast<double>(pl.warm + pl.lagS_max + depth_rows);  // rows swept, not stored
     const double eff = static_cast<double>(ctas) / static_cast<double>(waves * cap) * static_cast<double>(seg) /
                            (static_cast<double>(seg) + overhead) -
                        (waves < 4 ? 0.05 * (4 - waves) : 0.0);
@@ -1171,33 +1513,35 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
     }
     if (waves > 16) break;
   }
-  sp->seg_rows = (rows + nseg - 1) / nseg;
-  nseg = (rows + sp->seg_rows - 1) / sp->seg_rows;
-  if (pl.red_op != OOC_RED_NONE) {
+  sp.seg_rows = (rows + nseg - 1) / nseg;
+  nseg = (rows + sp.seg_rows - 1) / sp.seg_rows;
+  if (red_run) {
     if (strips * nseg > c->red_part_cap) {
-      delete sp;
       set_error("ooc_launch_sweep: too many CTAs for the reduction partials");
       return OOC_ERR_UNSUPPORTED;
     }
-    sp->part = c->red_part[q];
+    sp.part = c->red_part[q];
   }
   c->stats.sweep_launches++;
-  void* args[] = {sp};
+  void* args[] = {&sp};
+  std::pair<cudaEvent_t, cudaEvent_t>* tev = nullptr;
   if (timing) {
-    auto& e = tune->ev[static_cast<std::size_t>(pick)];
-    if (!e.first) {
-      cudaEventCreate(&e.first);
-      cudaEventCreate(&e.second);
+    tev = &T.ev[static_cast<std::size_t>(pick)];
+    if (!tev->first) {
+      cudaEventCreate(&tev->first);
+      cudaEventCreate(&tev->second);
     }
-    cudaEventRecord(e.first, c->q[q]);
+    cudaEventRecord(tev->first, c->q[q]);
   }
-  const int rc = jit_launch_kernel(c, q, k->fn, static_cast<unsigned>(strips), static_cast<unsigned>(nseg),
+  const int rc = jit_launch_kernel(c, q, V.k.fn, static_cast<unsigned>(strips), static_cast<unsigned>(nseg),
                                    static_cast<unsigned>(pl.NT), static_cast<unsigned>(pl.smem), args);
   if (timing) {
-    cudaEventRecord(tune->ev[static_cast<std::size_t>(pick)].second, c->q[q]);
-    tune->issued[static_cast<std::size_t>(pick)] = 1;
+    cudaEventRecord(tev->second, c->q[q]);
+    T.issued[static_cast<std::size_t>(pick)] = 1;
   }
-  delete sp;
+  c->stats.sweep_host_us +=
+      std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - host0).count();
+  lk.unlock();
   if (rc != OOC_OK || pl.red_op == OOC_RED_NONE) return rc;
   return launch_fold(c, q, static_cast<int>(strips * nseg), loops[n - 1].reduce_slot, pl.red_op);
 }

@@ -461,6 +461,7 @@ const char* ooc_rt_device_json(ooc_runtime* h) {
     w.key("jit_host_us").value(st.jit_host_us);
     w.key("graph_launches").value(st.graph_launches);
     w.key("sweep_launches").value(st.sweep_launches);
+    w.key("sweep_host_us").value(st.sweep_host_us);
     w.key("mem_in_use").value(in_use);
     w.key("mem_peak").value(peak);
     w.key("build").value(std::string(ooc_dev_build_info()));
@@ -519,8 +520,8 @@ const char* ooc_rt_chain_sweep_check(ooc_runtime* h, int chain, int compile) {
       std::vector<ooc_redirect> dead;
       for (ooc::DatasetId d : run.dead) dead.push_back({views[static_cast<std::size_t>(d)].data, nullptr});
       std::vector<char> log(1 << 20);
-      int r = ooc_sweep_describe(calls.data() + a, static_cast<int>(b - a), log.data(), static_cast<int>(log.size()),
-                                 compile);
+      int r = ooc_sweep_describe(calls.data() + a, static_cast<int>(b - a), dead.data(), static_cast<int>(dead.size()),
+                                 log.data(), static_cast<int>(log.size()), compile);
       w.begin_object().key("first").value(static_cast<long long>(a)).key("loops").value(static_cast<long long>(b - a));
       w.key("ok").value(r == OOC_OK).key("plan").value(std::string(log.data()));
       w.key("dead").begin_array();
@@ -600,6 +601,10 @@ const char* ooc_rt_chain_jit_check(ooc_runtime* h, int chain, int fuse) {
     s = w.str();
   });
   return rc ? err_json() : out_str(s);
+}
+
+int ooc_rt_comm_init_ipc(ooc_runtime* h, const char* name) {
+  return guard([&] { h->rt->comm_init_ipc(name ? name : ""); });
 }
 
 int ooc_rt_comm_init(ooc_runtime* h, const void* unique_id) {

@@ -569,7 +569,8 @@ void GpuEngine::finish_chain(const LoopChain& chain, const std::map<int, int>& r
 // ---------------------------------------------------------------- streaming executor
 
 void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan& plan,
-                             const Footprints& fp, bool cyclic, ChainOut& out) {
+                             const Footprints& fp, bool cyclic, ChainOut& out,
+                             const std::vector<HaloXfer>* halos) {
   const int T = plan.tile_count;
   const int dim = plan.tiled_dim;
   if (3 * fp.slot_bytes > opts_.device.capacity_bytes)  // explicit_exec.cpp:61-62
@@ -883,7 +884,83 @@ void GpuEngine::run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan&
   // the chain ends when its last download has landed; the compute queue does not
   // wait for it, so the next chain's first tiles overlap this chain's last downloads
   DEV(ooc_queue_wait(ctx_, OOC_Q_D2H, E(ev_q0_, T - 1)));
+  if (halos && comm_ready_) {
+    // slab decomposition out of core: the neighbours' owned rows land in this rank's host
+    // ghost bands (from their host slabs, after their downloads), then the reductions
+    // are combined — the next chain uploads the refreshed rows like any others
+    exchange_host_bands(mesh, *halos);
+    for (const ParLoop& l : chain.loops)
+      if (l.has_reduction())
+        DEV(ooc_reduce_allreduce(ctx_, OOC_Q_COMPUTE, out.reduction_slot.at(l.id), lower_loop(l).reduce_op));
+  }
   finish_chain(chain, out.reduction_slot, pc, OOC_Q_D2H);
+}
+
+void GpuEngine::exchange_host_bands(Mesh& mesh, const std::vector<HaloXfer>& halos) {
+  DEV(ooc_ctx_sync(ctx_));  // the chain's downloads have landed: owned rows are current
+  struct Band {
+    DatasetId d;
+    index_t r0, r1, off;
+  };
+  std::vector<Band> send, recv;
+  std::vector<ooc_xfer> xs;
+  index_t total = 0;
+  auto band = [&](DatasetId d, const index_t* rr, std::vector<Band>& into) -> std::pair<index_t, index_t> {
+    const Extent a = mesh[d].alloc();
+    const index_t plane = a.size() / std::max<index_t>(1, a.hi[0] - a.lo[0]);
+    const index_t n = std::max<index_t>(0, rr[1] - rr[0]) * plane;
+    into.push_back({d, rr[0], rr[1], total});
+    total += n;
+    return {into.back().off, n};
+  };
+  struct Pend {
+    int peer;
+    index_t so, sn, ro, rn;
+  };
+  std::vector<Pend> pend;
+  for (const HaloXfer& h : halos) {
+    const Dataset& ds = mesh[h.dataset];
+    if (ds.host_stale) continue;  // cyclic temporaries were never downloaded (same on every rank)
+    if (rank_ > 0) {
+      auto s = band(h.dataset, h.send_left, send);
+      auto r = band(h.dataset, h.recv_left, recv);
+      pend.push_back({rank_ - 1, s.first, s.second, r.first, r.second});
+    }
+    if (rank_ + 1 < world_) {
+      auto s = band(h.dataset, h.send_right, send);
+      auto r = band(h.dataset, h.recv_right, recv);
+      pend.push_back({rank_ + 1, s.first, s.second, r.first, r.second});
+    }
+    invalidate_staged(h.dataset);  // a speculative first tile may hold the old ghost rows
+  }
+  if (pend.empty()) return;
+  if (total > band_stage_elems_) {
+    if (band_stage_) DEV(ooc_mem_free(ctx_, band_stage_));
+    void* p = nullptr;
+    DEV(ooc_mem_alloc(ctx_, static_cast<std::size_t>(total) * sizeof(double), &p));
+    band_stage_ = static_cast<double*>(p);
+    band_stage_elems_ = total;
+  }
+  auto copy = [&](const Band& b, int kind) {
+    if (b.r1 <= b.r0) return;
+    Dataset& ds = mesh[b.d];
+    Extent box = ds.alloc();
+    box.lo[0] = b.r0;
+    box.hi[0] = b.r1;
+    const BoxLayout L = padded_layout(box, 1);
+    ooc_view hv = host_view(ds);
+    ooc_view dv = view_at(band_stage_ + b.off, box, L.stride);
+    if (kind == OOC_COPY_H2D)
+      DEV(ooc_copy_box(ctx_, OOC_Q_COMPUTE, kind, &hv, &dv, dv.lo, dv.hi));
+    else
+      DEV(ooc_copy_box(ctx_, OOC_Q_COMPUTE, kind, &dv, &hv, dv.lo, dv.hi));
+  };
+  for (const Band& b : send) copy(b, OOC_COPY_H2D);
+  for (const Pend& p : pend)
+    xs.push_back({p.peer, band_stage_ + p.so, p.sn, band_stage_ + p.ro, p.rn});
+  DEV(ooc_comm_exchange(ctx_, OOC_Q_COMPUTE, xs.data(), static_cast<int>(xs.size())));
+  for (const Band& b : recv) copy(b, OOC_COPY_D2H);
+  DEV(ooc_queue_sync(ctx_, OOC_Q_COMPUTE));
 }
 
 // Real event timeline (replaces the reference's simulated one, command.cpp:35-126):
@@ -1364,6 +1441,13 @@ std::string GpuEngine::graph_key(const LoopChain& chain, const TilePlan* plan, b
 
 void GpuEngine::comm_init(int rank, int world, const void* id) {
   DEV(ooc_comm_init(ctx_, rank, world, id));
+  rank_ = rank;
+  world_ = world;
+  comm_ready_ = true;
+}
+
+void GpuEngine::comm_init_ipc(int rank, int world, const std::string& name) {
+  DEV(ooc_comm_init_ipc(ctx_, rank, world, name.c_str()));
   rank_ = rank;
   world_ = world;
   comm_ready_ = true;

@@ -19,8 +19,26 @@ Runtime::Runtime(RuntimeOptions opts) : opts_(opts) {
 Runtime::~Runtime() = default;
 
 GpuEngine& Runtime::engine() {
-  if (!gpu_) gpu_ = std::make_unique<GpuEngine>(opts_);
-  return *gpu_;
+  if (!device_.engine) {
+    device_.engine = std::make_shared<GpuEngine>(opts_);
+    device_.gpu = opts_.gpu;
+  }
+  return *device_.engine;
+}
+
+DeviceState& Runtime::device_state() {
+  engine();
+  return device_;
+}
+
+const std::vector<TimelineEntry>& Runtime::timeline_entries() {
+  const std::vector<TimelineRow>& rows = timeline();
+  for (std::size_t i = timeline_entries_.size(); i < rows.size(); ++i) {
+    const TimelineRow& r = rows[i];
+    timeline_entries_.push_back({r.command_id, static_cast<CmdKind>(r.kind), r.queue, r.bytes, r.issue, r.start,
+                                 r.end, r.dataset, r.tile, r.loop});
+  }
+  return timeline_entries_;
 }
 
 Extent Runtime::window_core(const Extent& core) const {
@@ -95,12 +113,12 @@ void Runtime::fetch_dataset_into(DatasetId d, double* dst, std::size_t n) {
   Dataset& ds = mesh_[d];
   if (ds.host_stale) throw StaleDataError(ds.name, ds.stale_chain);
   if (n != ds.host.size()) throw ValidationError("fetch buffer has the wrong length");
-  if (gpu_) {
-    if (gpu_->host_outdated(d))
-      gpu_->download_resident(mesh_, d);
+  if (device_.engine) {
+    if (device_.engine->host_outdated(d))
+      device_.engine->download_resident(mesh_, d);
     else
-      gpu_->sync();  // streamed downloads of earlier chains must have landed
-    gpu_->invalidate_staged(d);  // runtime.cpp:17
+      device_.engine->sync();  // streamed downloads of earlier chains must have landed
+    device_.engine->invalidate_staged(d);  // runtime.cpp:17
   }
   std::copy(ds.host.begin(), ds.host.end(), dst);
 }
@@ -133,15 +151,15 @@ void Runtime::finish() {
 }
 
 void Runtime::sync() {
-  if (gpu_) gpu_->sync();
+  if (device_.engine) device_.engine->sync();
 }
 
 void Runtime::sync_host() {
-  if (!gpu_) return;
+  if (!device_.engine) return;
   for (std::size_t d = 0; d < mesh_.datasets.size(); ++d)
-    if (gpu_->host_outdated(static_cast<DatasetId>(d)))
-      gpu_->download_resident(mesh_, static_cast<DatasetId>(d));
-  gpu_->sync();
+    if (device_.engine->host_outdated(static_cast<DatasetId>(d)))
+      device_.engine->download_resident(mesh_, static_cast<DatasetId>(d));
+  device_.engine->sync();
 }
 
 const PlanCache::Entry& Runtime::plan_for(const LoopChain& chain) {  // runtime.cpp:41-62
@@ -175,9 +193,22 @@ void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
     last_tiles_ = e.plan.tile_count;
     return;
   }
-  if (windowed() && opts_.executor == ExecutorKind::tiled_explicit)
-    throw ValidationError("the slab decomposition runs with the resident executor");
   GpuEngine& g = engine();
+  // slab decomposition: every chain's owned rows must be exact (ghost rows >= the chain's
+  // dependency depth) and, with neighbours, refreshed and combined after it — never run
+  // a multi-rank slab silently without its exchange
+  const bool slabbed = windowed() && opts_.dist_world > 1;
+  if (slabbed && !g.comm_ready())
+    throw ValidationError("slab decomposition over " + std::to_string(opts_.dist_world) +
+                          " ranks needs a communicator (comm_init / comm_init_ipc) before its first chain");
+  std::vector<HaloXfer> halos;
+  if (windowed()) {
+    const index_t depth = dependency_depth(chain);
+    if (depth > opts_.ghost)
+      throw ValidationError("chain " + std::to_string(chain.chain_id) + " needs " + std::to_string(depth) +
+                            " ghost rows; the slab has " + std::to_string(opts_.ghost));
+    if (g.comm_ready()) halos = halo_plan(chain);
+  }
   GpuEngine::ChainOut out;
   if (opts_.executor == ExecutorKind::tiled_explicit) {
     const PlanCache::Entry& e = plan_for(chain);
@@ -189,22 +220,19 @@ void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
       if (pd.accessed && ds.host_stale && !pd.write_first)
         throw StaleDataError(ds.name, ds.stale_chain);
     }
-    g.run_explicit(mesh_, chain, e.plan, e.footprints, cyclic_, out);
+    g.run_explicit(mesh_, chain, e.plan, e.footprints, cyclic_, out, g.comm_ready() ? &halos : nullptr);
   } else {
     const bool tiled = opts_.executor == ExecutorKind::resident &&
                        (opts_.tiles > 1 || (opts_.tiles == 0 && opts_.resident_budget > 0));
+    if (tiled && windowed())
+      throw ValidationError("resident tiling (tiles > 1 or resident_budget) cannot be combined with the "
+                            "slab decomposition; use the untiled resident or the tiled_explicit executor");
     if (tiled) {
       const PlanCache::Entry& e = plan_for(chain);
       last_tiles_ = e.plan.tile_count;
       g.run_resident(mesh_, chain, &e.plan, &e.footprints, out);
     } else if (windowed() && g.comm_ready()) {
       last_tiles_ = 1;
-      const index_t depth = dependency_depth(chain);
-      if (depth > opts_.ghost)
-        throw ValidationError("chain " + std::to_string(chain.chain_id) + " needs " +
-                              std::to_string(depth) + " ghost rows; the slab has " +
-                              std::to_string(opts_.ghost));
-      const std::vector<HaloXfer> halos = halo_plan(chain);
       g.run_resident(mesh_, chain, nullptr, nullptr, out, &halos);
     } else {
       last_tiles_ = 1;
@@ -281,17 +309,21 @@ void Runtime::comm_init(const void* unique_id) {
   engine().comm_init(opts_.dist_rank, opts_.dist_world, unique_id);
 }
 
+void Runtime::comm_init_ipc(const std::string& name) {
+  engine().comm_init_ipc(opts_.dist_rank, opts_.dist_world, name);
+}
+
 const std::vector<ChainTiming>& Runtime::chain_timings() {
-  if (gpu_)
-    for (ChainTiming& t : gpu_->take_timings()) timings_.push_back(t);
+  if (device_.engine)
+    for (ChainTiming& t : device_.engine->take_timings()) timings_.push_back(t);
   return timings_;
 }
 
 const std::vector<LoopMetric>& Runtime::loop_metrics() {
-  if (gpu_ && opts_.timeline) {
+  if (device_.engine && opts_.timeline) {
     timeline();
-  } else if (gpu_) {
-    for (const auto& [id, s] : gpu_->take_loop_times()) {
+  } else if (device_.engine) {
+    for (const auto& [id, s] : device_.engine->take_loop_times()) {
       auto it = metric_index_.find(id);
       if (it == metric_index_.end()) continue;
       LoopMetric& m = loop_metrics_[it->second];
@@ -305,8 +337,8 @@ const std::vector<LoopMetric>& Runtime::loop_metrics() {
 // Real-timeline loop attribution (restates proj/src/metrics.cpp:14-32 over measured
 // rows): kernel rows sorted by (start, command_id); each gets max(0, end - prev_end).
 const std::vector<TimelineRow>& Runtime::timeline() {
-  if (!gpu_) return timeline_;
-  std::vector<TimelineRow> rows = gpu_->take_timeline();
+  if (!device_.engine) return timeline_;
+  std::vector<TimelineRow> rows = device_.engine->take_timeline();
   std::vector<const TimelineRow*> k;
   for (const TimelineRow& r : rows)
     if (r.kind == 3) k.push_back(&r);

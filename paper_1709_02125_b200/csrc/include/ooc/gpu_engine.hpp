@@ -77,12 +77,16 @@ class GpuEngine {
   };
 
   void run_explicit(Mesh& mesh, const LoopChain& chain, const TilePlan& plan,
-                    const Footprints& fp, bool cyclic, ChainOut& out);
+                    const Footprints& fp, bool cyclic, ChainOut& out,
+                    const std::vector<HaloXfer>* halos = nullptr);
   void run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan* plan,
                     const Footprints* fp, ChainOut& out,
                     const std::vector<HaloXfer>* halos = nullptr);
   /// Join the NCCL communicator of the slab decomposition.
   void comm_init(int rank, int world, const void* unique_id);
+  /// Join the CUDA-IPC transport of the slab decomposition (ranks of one node; `name`
+  /// identifies the job's shared-memory rendezvous).
+  void comm_init_ipc(int rank, int world, const std::string& name);
   int rank() const { return rank_; }
   int world() const { return world_; }
   bool comm_ready() const { return comm_ready_; }
@@ -113,6 +117,15 @@ class GpuEngine {
   /// Resolve the real event timeline recorded so far (RuntimeOptions::timeline).
   std::vector<TimelineRow> take_timeline();
   ooc_ctx* ctx() { return ctx_; }
+  /// ExecOptions::prefetch per call (run_chain_explicit seam).
+  void set_prefetch(bool on) { opts_.prefetch = on; }
+  int slot_cursor() const { return slot_cursor_; }
+  /// Datasets whose next-chain first tile is staged in HBM, with the staged region.
+  std::map<DatasetId, Extent> staged_regions() const {
+    std::map<DatasetId, Extent> m;
+    for (const auto& [d, s] : staged_) m[d] = s.region;
+    return m;
+  }
   const ooc_dev_props& props() const { return props_; }
 
  private:
@@ -188,6 +201,12 @@ class GpuEngine {
   double* staging_ = nullptr;
   index_t staging_elems_ = 0;
   void ensure_staging(index_t elems);
+  /// Out-of-core slabs: refresh the host ghost bands of `halos` from the neighbours'
+  /// owned rows (after this chain's downloads): H2D of the send bands into a device
+  /// scratch, exchange, D2H of the received bands.
+  void exchange_host_bands(Mesh& mesh, const std::vector<HaloXfer>& halos);
+  double* band_stage_ = nullptr;
+  index_t band_stage_elems_ = 0;
   struct TLPending {
     int kind, queue;
     index_t bytes;

@@ -26,7 +26,12 @@
 #include <string>
 #include <vector>
 
+#include "ooc/command.hpp"
 #include "ooc/core.hpp"
+#include "ooc/device_config.hpp"
+#include "ooc/explicit_exec.hpp"
+#include "ooc/kernel_exec.hpp"
+#include "ooc/metrics.hpp"
 #include "ooc/tiler.hpp"
 
 namespace ooc {
@@ -49,32 +54,6 @@ inline const char* executor_name(ExecutorKind k) {
       return "plan_only";
   }
 }
-
-/// Device description. `capacity_bytes` is the (artificial) HBM budget the
-/// planner sizes the three slots against (proj/include/ooc/device_config.hpp:14-36);
-/// the bandwidth fields are kept for source compatibility only — this build
-/// measures instead of modelling.
-struct DeviceConfig {
-  index_t capacity_bytes = 16000000000;
-  double h2d_bandwidth = 16e9;
-  double d2h_bandwidth = 16e9;
-  double d2d_bandwidth = 510e9;
-  double device_kernel_bandwidth = 510e9;
-  double transfer_latency = 1e-6;
-  index_t cache_page_bytes = 65536;
-  double fault_latency = 50e-6;
-  double prefetch_bandwidth = 16e9;
-  double prefetch_degradation = 1.0;
-  static DeviceConfig pcie() { return DeviceConfig{}; }
-  static DeviceConfig nvlink() {
-    DeviceConfig c;
-    c.h2d_bandwidth = c.d2h_bandwidth = c.prefetch_bandwidth = 40e9;
-    return c;
-  }
-};
-
-enum class ExecPolicy { serial, openmp };  // source compatibility; kernels run on the GPU
-inline ExecPolicy default_exec_policy() { return ExecPolicy::openmp; }
 
 struct RuntimeOptions {
   ExecutorKind executor = ExecutorKind::reference;
@@ -113,21 +92,6 @@ struct FlushRecord {
   int loop_count;
 };
 
-/// Per-(dataset, tile) byte audit (proj/include/ooc/explicit_exec.hpp:20-24).
-struct AuditRow {
-  DatasetId dataset = -1;
-  int tile = -1;
-  index_t uploaded = 0, downloaded = 0, d2d = 0;
-};
-
-struct LoopMetric {
-  int loop_id = -1;
-  index_t points = 0;
-  index_t bytes = 0;
-  double time_s = 0.0;
-  double bandwidth = 0.0;
-};
-
 /// One command of the real event timeline (schema of the reference's simulated
 /// Timeline, proj/include/ooc/command.hpp:93-108). kind: 0 h2d, 1 d2h, 2 d2d, 3 kernel.
 struct TimelineRow {
@@ -149,23 +113,6 @@ struct ChainTiming {
   index_t metric_bytes = 0;
   index_t uploaded = 0, downloaded = 0, d2d = 0;
   double seconds = 0.0;  // first device op of the chain -> last (H2D..D2H)
-};
-
-struct RunReport {
-  std::string mode;
-  int tiles = 1;
-  double average_bandwidth = 0.0;  // metric bytes / device time
-  index_t total_bytes = 0;
-  double total_time = 0.0;
-  double makespan = 0.0;
-  index_t uploaded = 0, downloaded = 0, d2d = 0;
-  double efficiency = 0.0;
-  double hit_rate = -1.0;
-  index_t faults = -1;
-  std::string app, size;
-  int iters = 0;
-  index_t capacity = 0;
-  std::string error;
 };
 
 class GpuEngine;  // device-side state: context, slots, resident buffers, events
@@ -201,6 +148,8 @@ class Runtime {
   std::vector<HaloXfer> halo_plan(const LoopChain& chain);
   /// Join the NCCL communicator of the slab decomposition (128-byte unique id).
   void comm_init(const void* unique_id);
+  /// Join the CUDA-IPC transport instead (ranks of one node; same `name` on every rank).
+  void comm_init_ipc(const std::string& name);
 
   void enqueue_loop(ParLoop loop);
   std::vector<double> fetch_dataset(DatasetId d);
@@ -236,6 +185,10 @@ class Runtime {
   GpuEngine& engine();
   /// Real event timeline rows resolved so far (RuntimeOptions::timeline).
   const std::vector<TimelineRow>& timeline();
+  /// The same rows in the reference's TimelineEntry schema (proj/include/ooc/runtime.hpp:93).
+  const std::vector<TimelineEntry>& timeline_entries();
+  /// Device-side state shared with run_chain_explicit callers (the GPU engine).
+  DeviceState& device_state();
   // CSVs in the reference's schemas (proj/src/metrics.cpp:46-79, command.cpp:160-168)
   std::string report_csv(const std::string& app = "", const std::string& size = "", int iters = 0);
   std::string loops_csv();
@@ -266,8 +219,9 @@ class Runtime {
   std::map<int, index_t> owned_bytes_;   // windowed runs: metric bytes of the owned rows
   std::vector<ChainTiming> timings_;
   std::vector<TimelineRow> timeline_;
+  std::vector<TimelineEntry> timeline_entries_;
   double last_kernel_end_ = 0.0;
-  std::unique_ptr<GpuEngine> gpu_;
+  DeviceState device_;  // device_.engine: the GPU engine (created at first use)
 };
 
 }  // namespace ooc

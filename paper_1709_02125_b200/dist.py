@@ -7,6 +7,8 @@ torch.distributed is only the bootstrap that carries NCCL's unique id.
 from __future__ import annotations
 
 import ctypes
+import os
+import uuid
 
 from . import Runtime, _native
 
@@ -29,9 +31,31 @@ def unique_id() -> bytes:
     return buf.raw
 
 
-def init_comm(rt: Runtime, rank: int, group=None):
-    """Rank 0 creates the NCCL id, torch.distributed broadcasts it, every rank joins."""
+def transport() -> str:
+    """Ghost-exchange transport of the slab decomposition: "nccl" (default) or "ipc"
+    (CUDA IPC peer copies + a shared-memory rendezvous; OOC_COMM=ipc)."""
+    t = os.environ.get("OOC_COMM", "nccl").lower()
+    if t not in ("nccl", "ipc"):
+        raise ValueError(f"OOC_COMM={t}: expected nccl or ipc")
+    return t
+
+
+def ipc_name() -> str:
+    """A job-unique rendezvous name for the IPC transport."""
+    return f"{os.getpid()}_{uuid.uuid4().hex[:12]}"
+
+
+def init_comm(rt: Runtime, rank: int, group=None, kind: str | None = None):
+    """Join the slab decomposition's communicator. NCCL: rank 0 creates the id and
+    torch.distributed broadcasts it. IPC: rank 0 picks the rendezvous name and
+    torch.distributed broadcasts that. torch is only the bootstrap either way."""
     import torch.distributed as dist
+    kind = kind or transport()
+    if kind == "ipc":
+        obj = [ipc_name() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        rt.comm_init_ipc(obj[0])
+        return
     obj = [unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     rt.comm_init(obj[0])

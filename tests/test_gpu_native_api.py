@@ -47,3 +47,69 @@ def test_example_runs_on_gpu_bitwise(tmp_path):
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
     usum = float(r.stderr.decode().split()[1])
     assert abs(usum - want[(want.size and 0):].reshape(n + 2, n + 2)[1:-1, 1:-1].sum()) <= 1e-9 * usum
+
+
+# ---------------------------------------------------------------- the reference's own apps.cpp
+REF_APPS_SRC = "/root/reference/proj/src/apps.cpp"
+REF_APPS_BIN = os.path.join(ROOT, "tests", "_bin", "ref_apps_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_APPS_SRC), reason="reference sources not present")
+def test_reference_apps_cpp_compiles_unchanged():
+    """proj/src/apps.cpp (the reference's apps, app_baseline_bandwidth, scaling_sweep —
+    Runtime, metrics.hpp report CSVs, timeline_entries, CmdKind) compiles unchanged
+    against this repo's headers and links with libooc.so (tests/native/Makefile)."""
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "native"), "syntax", "all"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert os.path.exists(REF_APPS_BIN)
+
+
+def _ref_app_record(name, kw, want):
+    args = [REF_APPS_BIN, name, str(kw["nx"]), str(kw["ny"]), str(kw["iters"]), str(kw.get("span", 0)),
+            "explicit" if want["executor"] == "explicit" else "reference", str(want["tiles"]),
+            str(want["capacity"]), str(int(want["cyclic"])), str(int(want.get("prefetch", False)))]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    import json
+    return json.loads(r.stdout)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_APPS_BIN), reason="tests/_bin/ref_apps_b200 not built")
+def test_reference_apps_cpp_on_b200_vs_golden(golden_apps):
+    """The reference's own run_app (its apps.cpp, unchanged) drives this runtime on the GPU:
+    fields bit for bit, stale flags, audit rows and transfer totals exactly, reductions
+    within 1e-12 — against the golden records the reference library produced."""
+    from tests.helpers import close, sha
+    bad, ran = [], 0
+    for case in golden_apps:
+        name, kw = case["case"]
+        if name not in ("heat2d", "miniflow2d", "rk3chain"):
+            continue  # the 3-D analogues are this repo's apps, not the reference's
+        for want in case["runs"]:
+            got = _ref_app_record(name, kw, want)
+            ran += 1
+            tag = (name, want["executor"], want["tiles"], want["cyclic"], want.get("prefetch", False))
+            if "error" in want or "error" in got:
+                if want.get("error") != got.get("error"):
+                    bad.append((tag, want.get("error"), got.get("error")))
+                continue
+            if got["buffers"] != want["buffers"]:
+                bad.append((tag, "buffers"))
+            if got["stale"] != want["stale"]:
+                bad.append((tag, "stale"))
+            for rn, v in want["reductions"].items():
+                if rn not in got["reductions"] or not close(v, got["reductions"][rn]):
+                    bad.append((tag, rn))
+            if want["executor"] == "explicit":
+                if sha(got["audit"]) != want["audit_sha"]:
+                    bad.append((tag, "audit"))
+                if got["totals"][:3] != want["totals"][:3]:
+                    bad.append((tag, "totals", got["totals"], want["totals"]))
+            if got["totals"][3] != want["totals"][3]:
+                bad.append((tag, "metric bytes"))
+            if [list(x) for x in got["flush_log"]] != [list(x) for x in want["flush_log"]]:
+                bad.append((tag, "flush log"))
+    assert ran >= 20
+    assert not bad, bad
