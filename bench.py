@@ -276,8 +276,9 @@ def run_incore(B, n, steps, warmup, profile, gpu, resident_budget=0, rank=0, wor
     # label (the sweep planner's own accounting: inputs read once, live outputs written once)
     out["sweep_dram"] = {}
     try:
+        sizes = [f[2] for f in rt.flush_log()]
         for c in range(rt.num_chains()):
-            if rt.chain_plan(c, tiles=1)["loops"] == 141:
+            if sizes[c] == 141:
                 for g in rt.chain_sweep_check(c, compile=False):
                     if not g["ok"]:
                         continue

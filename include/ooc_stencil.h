@@ -154,6 +154,9 @@ const char* ooc_rt_chain_plan_text(ooc_runtime* rt, int chain, int tiles);
 /* Slab decomposition: join the NCCL communicator (id from ooc_comm_unique_id in
  * ooc_device.h); export a recorded chain's (window-clipped) loops; its ghost depth
  * and the ghost-band exchange it triggers. */
+/* Chain-description JSON (proj/include/ooc/chain_file.hpp:22-23 load_chain_json): declares
+ * the datasets and enqueues the loops; "ops" lists may interleave flush / finish / cyclic. */
+int ooc_rt_load_chain_json(ooc_runtime* rt, const char* json_text, int* loops_enqueued);
 int ooc_rt_comm_init(ooc_runtime* rt, const void* unique_id128);
 /* Join the CUDA-IPC transport instead of NCCL: the ranks of one node rendezvous in a
  * shared-memory segment named `name` (same on every rank), ghost bands move by

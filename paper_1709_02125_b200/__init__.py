@@ -368,47 +368,12 @@ class Runtime:
 
 # ---------------------------------------------------------------------- chain files
 def load_program(rt: Runtime, prog):
-    """Chain-file loader (proj/src/chain_file.cpp:58-162): declare the datasets, then
-    enqueue the loops; an optional "ops" list interleaves flush / cyclic / finish."""
-    if isinstance(prog, str):
-        prog = json.loads(prog)
-    for jd in prog.get("datasets", []):
-        lo, hi = jd["core"]["lo"], jd["core"]["hi"]
-        h = jd.get("halo", 0)
-        halo = [h] * len(lo) if isinstance(h, int) else list(h)
-        rt.declare(jd["name"], lo, hi, halo, jd.get("fill", 0.0), jd.get("elem_bytes", 8))
-    stencils = {"point": POINT}
-    for js in prog.get("stencils", []):
-        stencils[js["name"]] = [tuple(list(o) + [0] * (3 - len(o))) for o in js["offsets"]]
-    ops = prog.get("ops")
-    if ops is None:
-        ops = [dict(l, op="loop") for l in prog.get("loops", [])]
-    for op in ops:
-        kind = op["op"]
-        if kind == "loop":
-            args = []
-            for ja in op["args"]:
-                d = rt.find(ja["dataset"])
-                if d < 0:
-                    raise ValidationError(f"loop argument names unknown dataset '{ja['dataset']}'")
-                if ja["stencil"] not in stencils:
-                    raise ValidationError(f"loop argument names unknown stencil '{ja['stencil']}'")
-                args.append((d, stencils[ja["stencil"]], ja["mode"]))
-            k = op.get("kernel", {})
-            writes = {int(a): e for a, e in sorted(k.get("writes", {}).items())}
-            red = None
-            if "reduction" in k:
-                r = k["reduction"]
-                red = (r["op"], r["expr"], r["name"])
-            rt.enqueue_loop(op["range"]["lo"], op["range"]["hi"], args, writes, red)
-        elif kind == "flush":
-            rt.flush()
-        elif kind == "finish":
-            rt.finish()
-        elif kind == "cyclic":
-            rt.set_cyclic_flag(op.get("on", True))
-        else:
-            raise ValidationError(f"unknown program op '{kind}'")
+    """Chain-file loader (proj/src/chain_file.cpp:58-162, load_chain_json): declare the
+    datasets, then enqueue the loops; an optional "ops" list interleaves flush / cyclic /
+    finish. Parsed and executed natively (csrc/host/chain_file.cpp)."""
+    text = prog if isinstance(prog, str) else json.dumps(prog)
+    n = ctypes.c_int()
+    _check(_native.lib().ooc_rt_load_chain_json(rt._h, text.encode(), ctypes.byref(n)))
     return rt
 
 

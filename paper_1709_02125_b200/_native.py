@@ -99,6 +99,7 @@ def lib():
         "ooc_rt_chain_sweep_check": (cp, [vp, i, i]),
         "ooc_rt_comm_init": (i, [vp, ctypes.c_char_p]),
         "ooc_rt_comm_init_ipc": (i, [vp, ctypes.c_char_p]),
+        "ooc_rt_load_chain_json": (i, [vp, ctypes.c_char_p, ctypes.POINTER(i)]),
         "ooc_rt_chain_export_json": (cp, [vp, i]),
         "ooc_rt_dist_plan_json": (cp, [vp, i]),
         "ooc_rt_chain_oracle_json": (cp, [vp, i, i]),

@@ -10,6 +10,7 @@
 #include "json_writer.hpp"
 #include "ooc/apps.hpp"
 #include "ooc/gpu_engine.hpp"
+#include "ooc/chain_file.hpp"
 #include "ooc/runtime.hpp"
 
 struct ooc_runtime {
@@ -601,6 +602,13 @@ const char* ooc_rt_chain_jit_check(ooc_runtime* h, int chain, int fuse) {
     s = w.str();
   });
   return rc ? err_json() : out_str(s);
+}
+
+int ooc_rt_load_chain_json(ooc_runtime* h, const char* text, int* loops_enqueued) {
+  return guard([&] {
+    const ooc::ChainFileResult r = ooc::load_chain_json(*h->rt, text ? text : "");
+    if (loops_enqueued) *loops_enqueued = r.loops_enqueued;
+  });
 }
 
 int ooc_rt_comm_init_ipc(ooc_runtime* h, const char* name) {

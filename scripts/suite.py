@@ -17,6 +17,9 @@ WORK = {
     "miniflow2d": ("miniflow2d", 15360, 15360, 0, 10, 0),
     "miniflow3d": ("miniflow3d", 600, 600, 600, 10, 0),
     "rk3chain3d": ("rk3chain3d", 700, 700, 700, 3, 3),
+    # high-reuse chains: ten RK3 timesteps per chain
+    "rk3chain3d_s10": ("rk3chain3d", 640, 640, 640, 10, 10),
+    "rk3chain_s10": ("rk3chain", 15360, 15360, 0, 10, 10),
 }
 
 
@@ -44,7 +47,9 @@ def run(app_key, executor, steps=3, warmup=5, **kw):
            "GBps_device": nbytes / dev_s / 1e9, "GBps_wall": nbytes / wall / 1e9,
            "tiles": r1["tiles"], "uploaded": r1["uploaded"] - r0["uploaded"],
            "downloaded": r1["downloaded"] - r0["downloaded"], "d2d": r1["d2d"] - r0["d2d"],
-           "declare_s": t_decl, "launches": rt.device()["kernel_launches"]}
+           "declare_s": t_decl, "launches": rt.device()["kernel_launches"],
+           # per-chain reuse of the link bytes: metric bytes per byte moved over PCIe
+           "reuse": nbytes / max(1, (r1["uploaded"] - r0["uploaded"]) + (r1["downloaded"] - r0["downloaded"]))}
     rt.close()
     return out
 
@@ -66,20 +71,22 @@ def main():
                           **run("miniflow2d", "resident", resident_budget=96 << 20, steps=1, warmup=1)))
         B.set_sweep(True)
     for cfg, app, cyc in (("3", "miniflow2d", False), ("3", "miniflow2d", True),
-                          ("4", "miniflow3d", True), ("5", "rk3chain3d", False)):
+                          ("4", "miniflow3d", True), ("5", "rk3chain3d", False),
+                          ("5s10", "rk3chain3d_s10", False), ("5s10", "rk3chain3d_s10", True),
+                          ("2s10", "rk3chain_s10", False), ("2s10", "rk3chain_s10", True)):
         if cfg not in which:
             continue
         CYCLIC[0] = cyc
         pb = B.problem_bytes(*[WORK[app][i] for i in (0, 1, 2, 3)], WORK[app][5])
         base = run(app, "resident")
-        lines.append(dict(config=int(cfg), mode="in-core baseline", cyclic=cyc, **base))
+        lines.append(dict(config=cfg, mode="in-core baseline", cyclic=cyc, **base))
         for ratio in ((1.5, 3.0) if cfg == "3" else (3.0,)):
             try:
                 r = run(app, "explicit", capacity=int(pb / ratio))
-                r.update(config=int(cfg), mode=f"out-of-core {ratio}x (capacity = problem/{ratio})",
+                r.update(config=cfg, mode=f"out-of-core {ratio}x (capacity = problem/{ratio})",
                          cyclic=cyc, ooc_over_incore=r["GBps_wall"] / base["GBps_device"])
             except Exception as e:  # noqa: BLE001
-                r = {"config": int(cfg), "app": app, "ratio": ratio, "error": str(e)}
+                r = {"config": cfg, "app": app, "ratio": ratio, "error": str(e)}
             lines.append(r)
         CYCLIC[0] = False
     for l in lines:

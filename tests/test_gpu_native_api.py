@@ -113,3 +113,49 @@ def test_reference_apps_cpp_on_b200_vs_golden(golden_apps):
                 bad.append((tag, "flush log"))
     assert ran >= 20
     assert not bad, bad
+
+
+# ---------------------------------------------------------------- the executor seam
+def build_seam_example(tmp_path):
+    exe = str(tmp_path / "executor_seam")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O2", "-ffp-contract=off",
+                    "-I", os.path.join(PKG, "csrc", "include"), "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "executor_seam.cpp"), "-o", exe,
+                    "-L", os.path.join(PKG, "lib"), "-looc", "-Wl,-rpath," + os.path.join(PKG, "lib")],
+                   check=True)
+    return exe
+
+
+def test_executor_seam_example_compiles(tmp_path):
+    """run_chain_explicit with the reference's signature
+    (Mesh&, LoopChain, TilePlan, Footprints, DeviceConfig, ExecOptions, DeviceState&)."""
+    assert os.path.exists(build_seam_example(tmp_path))
+
+
+@pytest.mark.gpu
+def test_executor_seam_runs_bitwise(tmp_path):
+    """Three planned chains through run_chain_explicit with one DeviceState (prefetch on,
+    capacity = problem/3): the field equals the oracle's bit for bit, the reduction the
+    reference's sequential sum within 1e-12."""
+    exe = build_seam_example(tmp_path)
+    n, iters, chains = 96, 4, 3
+    r = subprocess.run([exe, str(n), str(iters), str(chains)], capture_output=True, check=True)
+    got = np.frombuffer(r.stdout, dtype=np.float64)
+    rt = O.Runtime("reference")
+    u = rt.declare("u", O.Ext.make(2, (0, 0), (n, n)), (1, 1), 8, "(+ 1.0 (* 0.125 (+ i j)))")
+    t = rt.declare("tmp", O.Ext.make(2, (0, 0), (n, n)), (1, 1), 8, 0.0)
+    s5 = [(0, 0, 0), (-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0)]
+    avg = O.parse_prefix("(* 0.25 (+ (+ (r 0 -1 0) (r 0 1 0)) (+ (r 0 0 -1) (r 0 0 1))))")
+    for _ in range(iters * chains):
+        rt.enqueue_loop(O.Loop(O.Ext.make(2, (1, 1), (n - 1, n - 1)),
+                               [O.Arg(u, s5, O.READ), O.Arg(t, [(0, 0, 0)], O.WRITE)], [(1, avg)]))
+        rt.enqueue_loop(O.Loop(O.Ext.make(2, (1, 1), (n - 1, n - 1)),
+                               [O.Arg(t, [(0, 0, 0)], O.READ), O.Arg(u, [(0, 0, 0)], O.WRITE)],
+                               [(1, ("read", 0, (0, 0, 0)))]))
+    want = rt.fetch_dataset(u).ravel()
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    log = r.stderr.decode()
+    assert "staged=" in log and "T=" in log
+    usum = float(log.split("usum")[1].split()[0])
+    ref = want.reshape(n + 2, n + 2)[1:-1, 1:-1].sum()
+    assert abs(usum - ref) <= 1e-12 * abs(ref)
