@@ -129,27 +129,39 @@ __device__ __forceinline__ void sw_bulk(unsigned dst, const double* src, unsigne
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+__device__ __forceinline__ int sw_slot(int x, int w) {  // x mod w, for rings of any length
+  const int r = x % w;
+  return r < 0 ? r + w : r;
+}
 struct SwLd {  // one loaded dataset's row copies: source column, rows, ring placement
   const double* src;
   long long s0, vrb, nrows;  // view row of ring row u = vrb + u + lagL; rows in [0, nrows)
   unsigned dst, tn;          // ring byte offset of the copy (row 0), bytes per row copy
-  int wmask, lagL;
+  int w, lagL;               // ring length (rows)
 };
-__device__ __noinline__ void sw_issue(const SwLd* t, int nl, int sn, int K, unsigned bar, unsigned sbase, int pitch8) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+// Producer work of one step: the ring rows of step `sn` (bulk copies completing on
+// barrier `bar`; sn < 0: none) and an L2 prefetch of the rows of step `pf` (pf < 0: none)
+// — DRAM latency is covered from L2 without holding shared memory for it.
+__device__ __noinline__ void sw_issue(const SwLd* t, int nl, int sn, int pf, int nsteps, int K, unsigned bar,
+                                      unsigned sbase, int pitch8) {
+  if (sn >= 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll 1
   for (int i = 0; i < nl; ++i) {
     const SwLd L = t[i];
+    if (!L.tn) continue;
     for (int r = 0; r < K; ++r) {
       const long long vr = L.vrb + static_cast<long long>(sn) * K + r;
-      if (L.tn && vr >= 0 && vr < L.nrows) {
+      if (sn >= 0 && vr >= 0 && vr < L.nrows) {
         const int u = sn * K + r - L.lagL;
         asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(L.tn) : "memory");
-        sw_bulk(sbase + L.dst + static_cast<unsigned>((u & L.wmask) * pitch8), L.src + vr * L.s0, L.tn, bar);
+        sw_bulk(sbase + L.dst + static_cast<unsigned>(sw_slot(u, L.w) * pitch8), L.src + vr * L.s0, L.tn, bar);
       }
+      const long long vp = L.vrb + static_cast<long long>(pf) * K + r;
+      if (pf >= 0 && pf < nsteps && vp >= 0 && vp < L.nrows)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(L.src + vp * L.s0), "r"(L.tn) : "memory");
     }
   }
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+  if (sn >= 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
 }
 __device__ __forceinline__ void sw_cp8(double* dst, const double* src, bool ok) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -179,6 +191,8 @@ struct SwDs {
 struct SwPlan {
   int n = 0, K = 2, P = 2, NT = 256, RC = 128;
   bool tma = false;  // loads: bulk async copies (one thread, mbarrier ring) instead of per-thread cp.async
+  long long U = 8;   // ring period: every ring length divides it (0: none small enough, no unrolling)
+  int NB = 8;        // load barriers (a multiple of U's steps: constant indices in unrolled steps)
   int RCp = 128;     // ring row pitch in doubles (RC, or RC + 2 with TMA: even-column row copies)
   long long HC = 0, TC = 0, warm = 0, lagS_max = 0, smem = 0;
   int red_op = OOC_RED_NONE;  // the run's last loop reduces (no writes): folded per CTA
@@ -375,11 +389,47 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
         B = std::max(B, K - 1 - S.lag);
       }
     }
-    D.W = 1;
     D.need = std::max<long long>(A + B + 1, K);
-    while (D.W < D.need) D.W *= 2;  // power of two: slot = row & (W-1)
-    D.off = off;
-    off += D.W * pl.RCp;
+  }
+  // ring lengths: the smallest divisor of a common period U >= each ring's live rows,
+  // U chosen among 8, 12, 16, 24 for the fewest rows in total (a period lets the
+  // interior steps unroll U times with constant slots; lengths need not be powers of
+  // two — 3- and 6-row rings save shared memory, i.e. CTAs per SM). OOC_SWEEP_RING=pow2
+  // keeps power-of-two lengths.
+  {
+    static const bool pow2_only = std::getenv("OOC_SWEEP_RING") && std::string(std::getenv("OOC_SWEEP_RING")) == "pow2";
+    long long bestU = 0, bestRows = LLONG_MAX;
+    for (long long Uc : {8LL, 12LL, 16LL, 24LL}) {
+      if (pow2_only && (Uc & (Uc - 1))) continue;
+      long long rows = 0;
+      bool okU = true;
+      for (const SwDs& D : pl.D) {
+        long long w = D.need;
+        while (w <= Uc && Uc % w) ++w;
+        if (w > Uc) {
+          okU = false;
+          break;
+        }
+        rows += w;
+      }
+      if (okU && rows < bestRows) {
+        bestRows = rows;
+        bestU = Uc;
+      }
+    }
+    pl.U = bestU;
+    pl.NB = bestU > 0 ? static_cast<int>(bestU) : 8;
+    for (SwDs& D : pl.D) {
+      if (bestU > 0) {
+        D.W = D.need;
+        while (bestU % D.W) ++D.W;
+      } else {  // rings longer than 24 rows: powers of two, no unrolled steps
+        D.W = 1;
+        while (D.W < D.need) D.W *= 2;
+      }
+      D.off = off;
+      off += D.W * pl.RCp;
+    }
   }
   pl.smem = (off + 2 * kPad) * 8;
   if (pl.smem > smem_budget()) return fail(why, "shared memory");
@@ -484,7 +534,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   else if (smem_occ > 1) o << ", " << smem_occ;
   o << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p) {\n";
   o << "  extern __shared__ __align__(16) double sw_sm[];\n";
-  if (pl.tma) o << "  __shared__ __align__(8) unsigned long long sw_bar[8];\n";
+  if (pl.tma) o << "  __shared__ __align__(8) unsigned long long sw_bar[" << pl.NB << "];\n";
   o << "  const int lc = threadIdx.x;\n";
   o << "  double* const B = sw_sm + " << kPad << " + lc;\n";
   o << "  const long long c0 = p.C0 + static_cast<long long>(blockIdx.x) * " << pl.TC << ";\n";
@@ -563,7 +613,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   }
   if (pl.tma) {
     o << "  if (threadIdx.x == " << pl.RC << ") {\n";
-    o << "    for (int b = 0; b < 8; ++b)\n";
+    o << "    for (int b = 0; b < " << pl.NB << "; ++b)\n";
     o << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(sw_saddr(&sw_bar[b])) : \"memory\");\n";
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
     o << "  }\n  __syncthreads();\n";
@@ -571,10 +621,23 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
   // element (dataset d, row u + q) of this thread's column; u, q relative to rbase
+  // In an unrolled step (unroll_u >= 0: u = unroll_u modulo the ring period) the slot is a
+  // constant; otherwise (u + q) mod W at run time (a mask for power-of-two lengths).
+  long long unroll_u = -1;
   auto at = [&](int d, const std::string& u, long long q, long long oc) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     std::ostringstream e;
-    e << "R" << d << "[(((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RCp;
+    long long extra = -1;
+    if (unroll_u >= 0 && u == "u") extra = 0;
+    if (unroll_u >= 0 && u == "u + " + std::to_string(K)) extra = K;
+    if (extra >= 0) {
+      const long long slot = (((unroll_u + extra + q) % D.W) + D.W) % D.W;
+      e << "R" << d << "[" << slot * pl.RCp;
+    } else if ((D.W & (D.W - 1)) == 0) {
+      e << "R" << d << "[(((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RCp;
+    } else {
+      e << "R" << d << "[sw_slot((" << u << ") + (" << q << "), " << D.W << ") * " << pl.RCp;
+    }
     if (oc) e << " + (" << oc << ")";
     e << "]";
     return e.str();
@@ -627,9 +690,14 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // stale ring contents only reach values that are never stored.
   int nload = 0;
   for (const SwDs& D : pl.D) nload += D.loaded ? 1 : 0;
-  auto tma_issue = [&](const std::string& step, const char* ind) {
-    o << ind << "if (threadIdx.x == " << pl.RC << " && (" << step << ") < nsteps) sw_issue(sw_ld, " << nload << ", " << step << ", " << K
-      << ", sw_saddr(sw_bar) + static_cast<unsigned>(((" << step << ") & 7) * 8), sw_saddr(sw_sm), " << pl.RCp * 8 << ");\n";
+  static const int l2_ahead = [] {  // steps between the L2 prefetch and the ring load of a row
+    const char* e = std::getenv("OOC_SWEEP_L2AHEAD");
+    return e ? std::atoi(e) : 4;
+  }();
+  auto tma_issue = [&](const std::string& step, const char* ind, const std::string& pf) {
+    o << ind << "if (threadIdx.x == " << pl.RC << ") sw_issue(sw_ld, " << nload << ", (" << step << ") < nsteps ? (" << step
+      << ") : -1, " << pf << ", nsteps, " << K << ", sw_saddr(sw_bar) + static_cast<unsigned>(((" << step << ") % " << pl.NB
+      << ") * 8), sw_saddr(sw_sm), " << pl.RCp * 8 << ");\n";
   };
   if (pl.tma) {  // the CTA's load descriptors (computed once by the issuing thread)
     o << "  __shared__ SwLd sw_ld[" << std::max(nload, 1) << "];\n";
@@ -649,7 +717,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       o << "      L.nrows = p.box[" << ds << "][1] - p.box[" << ds << "][0];\n";
       o << "      L.dst = static_cast<unsigned>((" << kPad + D.off << " + a0 - (cs - (cs & 1))) * 8);\n";
       o << "      L.tn = a1 > a0 ? static_cast<unsigned>(a1 - a0) * 8u : 0u;\n";
-      o << "      L.wmask = " << D.W - 1 << ";\n      L.lagL = " << D.lagL << ";\n";
+      o << "      L.w = " << D.W << ";\n      L.lagL = " << D.lagL << ";\n";
       o << "    }\n";
       ++i;
     }
@@ -659,10 +727,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     // the producer warp: loads of steps 0..P-1, then per step (after the consumers'
     // step barrier, which frees the ring rows the next loads overwrite) those of step s+P;
     // the consumers' other barriers are named barrier 1 over the ring threads only
-    for (int t = 0; t < pl.P; ++t) tma_issue(std::to_string(t), "  ");
+    for (int t = 0; t < pl.P; ++t) tma_issue(std::to_string(t), "  ", l2_ahead > 0 ? std::to_string(pl.P + t) : "-1");
+    for (int t = pl.P; t < l2_ahead; ++t) tma_issue("-1", "  ", std::to_string(pl.P + t));
     o << "  if (threadIdx.x >= " << pl.RC << ") {\n";
     o << "    for (int s = 0; s < nsteps; ++s) {\n      __syncthreads();\n";
-    tma_issue("s + " + std::to_string(pl.P), "      ");
+    tma_issue("s + " + std::to_string(pl.P), "      ", l2_ahead > 0 ? "s + " + std::to_string(pl.P + l2_ahead) : "-1");
     o << "    }\n    return;\n  }\n";
   } else
     for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false, false);
@@ -979,9 +1048,13 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         << ";\n" << ind << "  }\n" << ind << "}\n";
     }
   };
-  auto step_top = [&](const std::string& ind) {
-    if (pl.tma) {
-      o << ind << "sw_wait(sw_saddr(sw_bar) + static_cast<unsigned>((s & 7) * 8), static_cast<unsigned>((s >> 3) & 1));\n";
+  auto step_top = [&](const std::string& ind, long long j = -1) {
+    if (pl.tma && j >= 0) {  // unrolled step j of a period block (U == NB): constant barrier
+      o << ind << "sw_wait(sw_saddr(sw_bar) + " << (j % pl.NB) * 8 << "u, static_cast<unsigned>(sbl & 1));\n";
+      o << ind << "__syncthreads();\n";
+    } else if (pl.tma) {
+      o << ind << "sw_wait(sw_saddr(sw_bar) + static_cast<unsigned>((s % " << pl.NB << ") * 8), static_cast<unsigned>((s / "
+        << pl.NB << ") & 1));\n";
       o << ind << "__syncthreads();\n";
     } else {
       o << ind << "asm volatile(\"cp.async.wait_group " << pl.P - 1 << ";\" ::: \"memory\");\n";
@@ -1004,21 +1077,20 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     const char* e = std::getenv("OOC_SWEEP_UNROLL");
     return e ? std::atoi(e) : 1;
   }();
-  long long U = pl.tma ? 8 : 1;
-  for (const SwDs& D : pl.D) U = std::max(U, D.W);
-  if (unroll_env == 0 || U > 16) U = 0;
-  int logU = 0;
-  while (U > 0 && (1LL << logU) < U) ++logU;
+  long long U = pl.U;  // ring period (every ring length divides it; == NB with TMA)
+  if (unroll_env == 0 || U > 24 || (pl.tma && U != pl.NB)) U = 0;
   o << "  for (int s = 0; s < nsteps;) {\n";
   if (U > 1) {
-    o << "    if (strip_in && (s & " << U - 1 << ") == 0 && s >= s_lo && s + " << U << " <= s_hi) {\n";
-    o << "      const int sbl = s >> " << logU << ";\n";
+    o << "    if (strip_in && s % " << U << " == 0 && s >= s_lo && s + " << U << " <= s_hi) {\n";
+    o << "      const int sbl = s / " << U << ";\n";
     for (long long j = 0; j < U; ++j) {
       o << "      {  // unrolled fast step " << j << "\n";
-      o << "        const int s = (sbl << " << logU << ") + " << j << ";\n";
-      step_top("        ");
+      o << "        const int s = sbl * " << U << " + " << j << ";\n";
+      step_top("        ", j);
       o << "        {\n";
-      fast_body(nullptr, "((sbl << " + std::to_string(logU) + ") + " + std::to_string(j) + ") * " + std::to_string(K));
+      unroll_u = j * K;
+      fast_body(nullptr, "(sbl * " + std::to_string(U) + " + " + std::to_string(j) + ") * " + std::to_string(K));
+      unroll_u = -1;
       o << "        }\n";
       advance("        ");
       o << "      }\n";

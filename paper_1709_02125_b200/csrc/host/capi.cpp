@@ -463,6 +463,7 @@ const char* ooc_rt_device_json(ooc_runtime* h) {
     w.key("graph_launches").value(st.graph_launches);
     w.key("sweep_launches").value(st.sweep_launches);
     w.key("sweep_host_us").value(st.sweep_host_us);
+    w.key("comm_bytes").value(st.comm_bytes);
     w.key("mem_in_use").value(in_use);
     w.key("mem_peak").value(peak);
     w.key("build").value(std::string(ooc_dev_build_info()));

@@ -27,11 +27,8 @@ pad = 3 * (span or 1) - 1 if app.startswith("rk3") else 0
 own = D.slab(rank, world, nx + 2 * pad, -pad)
 kw = dict(dist=(rank, world), own=own, ghost=ghost, gpu=0)
 if executor == "explicit":
-    rt0 = B.Runtime("plan_only", dist=(rank, world), own=own, ghost=ghost)
-    rt0.declare_app(app, nx, ny, nz, span)
-    slab_bytes = sum(rt0.dataset_info(d)["len"] * 8 for d in range(rt0.num_datasets))
-    rt0.close()
-    rt = B.Runtime("explicit", capacity=slab_bytes // 3, prefetch=True, **kw)
+    # each rank streams its own slab through 3 HBM slots in 3 skewed tiles
+    rt = B.Runtime("explicit", tiles=3, prefetch=True, **kw)
 else:
     rt = B.Runtime("resident", **kw)
 rt.comm_init_ipc(name)
