@@ -133,36 +133,6 @@ __device__ __forceinline__ int sw_slot(int x, int w) {  // x mod w, for rings of
   const int r = x % w;
   return r < 0 ? r + w : r;
 }
-struct SwLd {  // one loaded dataset's row copies: source column, rows, ring placement
-  const double* src;
-  long long s0, vrb, nrows;  // view row of ring row u = vrb + u + lagL; rows in [0, nrows)
-  unsigned dst, tn;          // ring byte offset of the copy (row 0), bytes per row copy
-  int w, lagL;               // ring length (rows)
-};
-// Producer work of one step: the ring rows of step `sn` (bulk copies completing on
-// barrier `bar`; sn < 0: none) and an L2 prefetch of the rows of step `pf` (pf < 0: none)
-// — DRAM latency is covered from L2 without holding shared memory for it.
-__device__ __noinline__ void sw_issue(const SwLd* t, int nl, int sn, int pf, int nsteps, int K, unsigned bar,
-                                      unsigned sbase, int pitch8) {
-  if (sn >= 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#pragma unroll 1
-  for (int i = 0; i < nl; ++i) {
-    const SwLd L = t[i];
-    if (!L.tn) continue;
-    for (int r = 0; r < K; ++r) {
-      const long long vr = L.vrb + static_cast<long long>(sn) * K + r;
-      if (sn >= 0 && vr >= 0 && vr < L.nrows) {
-        const int u = sn * K + r - L.lagL;
-        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(L.tn) : "memory");
-        sw_bulk(sbase + L.dst + static_cast<unsigned>(sw_slot(u, L.w) * pitch8), L.src + vr * L.s0, L.tn, bar);
-      }
-      const long long vp = L.vrb + static_cast<long long>(pf) * K + r;
-      if (pf >= 0 && pf < nsteps && vp >= 0 && vp < L.nrows)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(L.src + vp * L.s0), "r"(L.tn) : "memory");
-    }
-  }
-  if (sn >= 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
-}
 __device__ __forceinline__ void sw_cp8(double* dst, const double* src, bool ok) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(s), "l"(src), "r"(ok ? 8 : 0) : "memory");
@@ -683,55 +653,74 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // aligned), completing on mbarrier step & 7. Rows outside the view are not copied:
   // nothing in range reads them (validate_loop), so stale ring contents only reach
   // values that are never stored.
-  // TMA issue of the rows of step `step` (thread 0, sw_issue): per loaded dataset and row,
-  // one bulk copy of the ring's columns clipped to the view (even start and length:
-  // 16-byte aligned) from the CTA's descriptor table, completing on mbarrier step & 7.
-  // Rows outside the view are not copied: nothing in range reads them (validate_loop), so
-  // stale ring contents only reach values that are never stored.
+  // The producer warp (TMA): lane i streams the i-th loaded dataset. Per step, after the
+  // consumers' step barrier (which frees the ring rows the next loads overwrite), each
+  // lane issues one bulk copy per row of step s+P — the ring's columns clipped to the view
+  // (even start and length: 16-byte aligned) — arming barrier (s+P) mod NB with its bytes;
+  // lane 0 then arrives. Rows outside the view are not copied: nothing in range reads them
+  // (validate_loop), so stale ring contents only reach values that are never stored. An
+  // L2 bulk prefetch runs `l2_ahead` steps further, so the ring loads hit L2.
   int nload = 0;
   for (const SwDs& D : pl.D) nload += D.loaded ? 1 : 0;
   static const int l2_ahead = [] {  // steps between the L2 prefetch and the ring load of a row
     const char* e = std::getenv("OOC_SWEEP_L2AHEAD");
     return e ? std::atoi(e) : 4;
   }();
-  auto tma_issue = [&](const std::string& step, const char* ind, const std::string& pf) {
-    o << ind << "if (threadIdx.x == " << pl.RC << ") sw_issue(sw_ld, " << nload << ", (" << step << ") < nsteps ? (" << step
-      << ") : -1, " << pf << ", nsteps, " << K << ", sw_saddr(sw_bar) + static_cast<unsigned>(((" << step << ") % " << pl.NB
-      << ") * 8), sw_saddr(sw_sm), " << pl.RCp * 8 << ");\n";
+  auto tma_issue = [&](const std::string& step, const std::string& pf, const char* ind) {
+    o << ind << "{\n" << ind << "  const int sn = " << step << ", pf = " << pf << ";\n";
+    o << ind << "  if (sn >= 0 && sn < nsteps) {\n";
+    o << ind << "    const unsigned bar = bar0 + static_cast<unsigned>((sn % " << pl.NB << ") * 8);\n";
+    o << ind << "    if (tn) {\n";
+    o << ind << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+    for (int r = 0; r < K; ++r) {
+      o << ind << "      {\n" << ind << "        const long long v = vr0 + static_cast<long long>(sn) * " << K << " + " << r << ";\n";
+      o << ind << "        if (v >= 0 && v < nrows) {\n";
+      o << ind << "          asm volatile(\"mbarrier.expect_tx.shared::cta.b64 [%0], %1;\" :: \"r\"(bar), \"r\"(tn) : \"memory\");\n";
+      o << ind << "          sw_bulk(dst + static_cast<unsigned>(sw_slot(sn * " << K << " + " << r << " - lagL, wlen) * " << pl.RCp * 8
+        << "), src + v * s0, tn, bar);\n";
+      o << ind << "        }\n" << ind << "      }\n";
+    }
+    o << ind << "    }\n" << ind << "    __syncwarp();\n";
+    o << ind << "    if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(bar) : \"memory\");\n";
+    o << ind << "  }\n";
+    o << ind << "  if (tn && pf >= 0 && pf < nsteps) {\n";
+    for (int r = 0; r < K; ++r) {
+      o << ind << "    {\n" << ind << "      const long long v = vr0 + static_cast<long long>(pf) * " << K << " + " << r << ";\n";
+      o << ind << "      if (v >= 0 && v < nrows)\n";
+      o << ind << "        asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(src + v * s0), \"r\"(tn) : \"memory\");\n";
+      o << ind << "    }\n";
+    }
+    o << ind << "  }\n" << ind << "}\n";
   };
-  if (pl.tma) {  // the CTA's load descriptors (computed once by the issuing thread)
-    o << "  __shared__ SwLd sw_ld[" << std::max(nload, 1) << "];\n";
-    o << "  if (threadIdx.x == " << pl.RC << ") {\n";
+  if (pl.tma) {
+    o << "  if (threadIdx.x >= " << pl.RC << ") {  // ---- producer warp\n";
+    o << "    const int lane = threadIdx.x - " << pl.RC << ";\n";
+    o << "    int dd = -1, lagL = 0, wlen = 1, roff = 0;\n";
     int i = 0;
     for (int d = 0; d < nd; ++d) {
       const SwDs& D = pl.D[static_cast<std::size_t>(d)];
       if (!D.loaded) continue;
-      const std::string ds = std::to_string(d);
-      o << "    {\n";
-      o << "      const long long cs = c0 - " << pl.HC << " - p.box[" << ds << "][2];\n";
-      o << "      const long long a0 = cs > 0 ? (cs & ~1LL) : 0LL;\n";
-      o << "      const long long a1 = (min(cs + " << pl.RC << "LL, p.box[" << ds << "][3] - p.box[" << ds << "][2]) + 1) & ~1LL;\n";
-      o << "      SwLd& L = sw_ld[" << i << "];\n";
-      o << "      L.src = p.src[" << ds << "] + a0;\n      L.s0 = p.s0[" << ds << "];\n";
-      o << "      L.vrb = rbase - p.box[" << ds << "][0] - " << D.lagL << ";\n";
-      o << "      L.nrows = p.box[" << ds << "][1] - p.box[" << ds << "][0];\n";
-      o << "      L.dst = static_cast<unsigned>((" << kPad + D.off << " + a0 - (cs - (cs & 1))) * 8);\n";
-      o << "      L.tn = a1 > a0 ? static_cast<unsigned>(a1 - a0) * 8u : 0u;\n";
-      o << "      L.w = " << D.W << ";\n      L.lagL = " << D.lagL << ";\n";
-      o << "    }\n";
+      o << "    " << (i ? "else if" : "if") << " (lane == " << i << ") { dd = " << d << "; lagL = " << D.lagL << "; wlen = " << D.W
+        << "; roff = " << kPad + D.off << "; }\n";
       ++i;
     }
-    o << "  }\n";
-  }
-  if (pl.tma) {
-    // the producer warp: loads of steps 0..P-1, then per step (after the consumers'
-    // step barrier, which frees the ring rows the next loads overwrite) those of step s+P;
-    // the consumers' other barriers are named barrier 1 over the ring threads only
-    for (int t = 0; t < pl.P; ++t) tma_issue(std::to_string(t), "  ", l2_ahead > 0 ? std::to_string(pl.P + t) : "-1");
-    for (int t = pl.P; t < l2_ahead; ++t) tma_issue("-1", "  ", std::to_string(pl.P + t));
-    o << "  if (threadIdx.x >= " << pl.RC << ") {\n";
+    o << "    const double* src = nullptr;\n    long long s0 = 0, vr0 = 0, nrows = 0;\n    unsigned dst = 0, tn = 0;\n";
+    o << "    if (dd >= 0) {\n";
+    o << "      const long long cs = c0 - " << pl.HC << " - p.box[dd][2];\n";
+    o << "      const long long a0 = cs > 0 ? (cs & ~1LL) : 0LL;\n";
+    o << "      const long long a1 = (min(cs + " << pl.RC << "LL, p.box[dd][3] - p.box[dd][2]) + 1) & ~1LL;\n";
+    o << "      tn = a1 > a0 ? static_cast<unsigned>(a1 - a0) * 8u : 0u;\n";
+    o << "      src = p.src[dd] + a0;\n      s0 = p.s0[dd];\n";
+    o << "      vr0 = rbase - p.box[dd][0] - lagL;  // view row of step sn, row r: vr0 + sn*K + r\n";
+    o << "      nrows = p.box[dd][1] - p.box[dd][0];\n";
+    o << "      dst = sw_saddr(sw_sm) + static_cast<unsigned>((roff + a0 - (cs - (cs & 1))) * 8);\n";
+    o << "    }\n";
+    o << "    const unsigned bar0 = sw_saddr(sw_bar);\n";
+    o << "    for (int t = 0; t < " << pl.P + std::max(l2_ahead, 0) << "; ++t)\n";
+    tma_issue("t < " + std::to_string(pl.P) + " ? t : -1",
+              l2_ahead > 0 ? "t >= " + std::to_string(pl.P) + " ? t : -1" : "-1", "      ");
     o << "    for (int s = 0; s < nsteps; ++s) {\n      __syncthreads();\n";
-    tma_issue("s + " + std::to_string(pl.P), "      ", l2_ahead > 0 ? "s + " + std::to_string(pl.P + l2_ahead) : "-1");
+    tma_issue("s + " + std::to_string(pl.P), l2_ahead > 0 ? "s + " + std::to_string(pl.P + l2_ahead) : "-1", "      ");
     o << "    }\n    return;\n  }\n";
   } else
     for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false, false);

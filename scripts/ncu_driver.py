@@ -30,6 +30,8 @@ os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 seq_name = "ncu_seq.json" if not os.environ.get("OOC_JIT_TUNE") else "ncu_seq_replay.json"
 with open(os.path.join(ROOT, "gpurun_out", seq_name), "w") as f:
     json.dump({"app": app, "n": n, "fuse": fuse, "chains": chains, "last_chain": seq}, f)
+with open(os.path.join(ROOT, "gpurun_out", "ncu_sweep_report.json"), "w") as f:
+    json.dump(B.sweep_report(), f)  # generator hashes of the sweep kernels this run built
 with open(os.path.join(ROOT, "gpurun_out", "ncu_tune.txt"), "w") as f:
     for k in B.jit_report():  # replay these shapes under ncu: OOC_JIT_TUNE=gpurun_out/ncu_tune.txt
         if k["shape"]:

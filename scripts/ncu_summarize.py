@@ -1,6 +1,6 @@
 """Label ncu's launch list with the engine's launch groups and summarise per group.
 
-    python scripts/ncu_summarize.py gpurun_out/launches.csv gpurun_out/ncu_seq.json OUT.json
+    python scripts/ncu_summarize.py gpurun_out/launches.csv gpurun_out/ncu_seq.json OUT.json [sweep_report.json]
 
 The launch list comes from `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --clock-control none --csv python scripts/ncu_driver.py ...`; the
@@ -13,7 +13,7 @@ import json
 import sys
 
 
-def main(csv_path, seq_path, out_path):
+def main(csv_path, seq_path, out_path, sweep_report=None):
     rows = {}
     with open(csv_path) as f:
         lines = [l for l in f if l.startswith('"')]
@@ -51,6 +51,8 @@ def main(csv_path, seq_path, out_path):
     out = {"source": f"ncu launch list {csv_path}; last chain of scripts/ncu_driver.py "
                      f"({seq['app']} {seq['n']}, fuse={seq['fuse']}); cold-cache serialised replay",
            "kernels": []}
+    if sweep_report:  # bench.py pairs these bytes with its timings only for the same kernel sources
+        out["gen_hashes"] = sorted({e["gen_hash"] for e in json.load(open(sweep_report)) if "gen_hash" in e})
     for k, g in sorted(groups.items(), key=lambda kv: -kv[1]["s"]):
         us = 1e6 * g["s"] / g["launches"]
         db = g["dram"] / g["launches"]
@@ -69,4 +71,4 @@ def main(csv_path, seq_path, out_path):
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:5])
