@@ -361,13 +361,14 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
     }
     D.need = std::max<long long>(A + B + 1, K);
   }
-  // ring lengths: the smallest divisor of a common period U >= each ring's live rows,
-  // U chosen among 8, 12, 16, 24 for the fewest rows in total (a period lets the
-  // interior steps unroll U times with constant slots; lengths need not be powers of
-  // two — 3- and 6-row rings save shared memory, i.e. CTAs per SM). OOC_SWEEP_RING=pow2
-  // keeps power-of-two lengths.
+  // ring lengths: powers of two (default), or with OOC_SWEEP_RING=period the smallest
+  // divisor of a common period U >= each ring's live rows, U among 8, 12, 16, 24 for the
+  // fewest rows in total. Either way every ring length divides U, so the interior steps
+  // unroll U times with constant slots. Period rings save shared memory (3 CTAs per SM
+  // instead of 2 on miniflow2d) but measured slower: 3.3-3.6 ms per timestep against
+  // 2.64-2.68 ms with power-of-two rings (round-2 record in profiles/).
   {
-    static const bool pow2_only = std::getenv("OOC_SWEEP_RING") && std::string(std::getenv("OOC_SWEEP_RING")) == "pow2";
+    static const bool pow2_only = !(std::getenv("OOC_SWEEP_RING") && std::string(std::getenv("OOC_SWEEP_RING")) == "period");
     long long bestU = 0, bestRows = LLONG_MAX;
     for (long long Uc : {8LL, 12LL, 16LL, 24LL}) {
       if (pow2_only && (Uc & (Uc - 1))) continue;
@@ -662,9 +663,9 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // L2 bulk prefetch runs `l2_ahead` steps further, so the ring loads hit L2.
   int nload = 0;
   for (const SwDs& D : pl.D) nload += D.loaded ? 1 : 0;
-  static const int l2_ahead = [] {  // steps between the L2 prefetch and the ring load of a row
-    const char* e = std::getenv("OOC_SWEEP_L2AHEAD");
-    return e ? std::atoi(e) : 4;
+  static const int l2_ahead = [] {  // steps between an L2 prefetch and the ring load of a row
+    const char* e = std::getenv("OOC_SWEEP_L2AHEAD");  // measured neutral to slightly slower: off
+    return e ? std::atoi(e) : 0;
   }();
   auto tma_issue = [&](const std::string& step, const std::string& pf, const char* ind) {
     o << ind << "{\n" << ind << "  const int sn = " << step << ", pf = " << pf << ";\n";
@@ -1277,7 +1278,13 @@ bool init_entry(SwEntry& E, const ooc_loop* loops, int n, const ooc_redirect* re
     }
     E.first.push_back(f);
   }
-  E.gen_hash = std::hash<std::string>{}(generate(loops, pl, nullptr));
+  {  // generator identity at a canonical depth (independent of tuning and OOC_SWEEP_P)
+    SwPlan canon;
+    if (analyze(loops, n, sweep_K(), 3, canon, nullptr, &dead, tma))
+      E.gen_hash = std::hash<std::string>{}(generate(loops, canon, nullptr));
+    else
+      E.gen_hash = std::hash<std::string>{}(generate(loops, pl, nullptr));
+  }
   if (sweep_P_forced()) {
     SwVar v;
     v.P = pl.P;

@@ -42,3 +42,23 @@ def test_slab_bench_under_torchrun_single_rank():
     line = json.loads(lines[0])
     assert line["value"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["parallelism"].startswith("dp1 dim-0 slabs")
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu_decompose_one_mesh():
+    """bench.py --gpus 2 under torchrun with both ranks on one GPU (gloo for the bench's
+    own collectives, the engine's CUDA-IPC transport for the ghost bands): the in-core run
+    and the out-of-core e2e run both decompose ONE (2n) x n mesh into dim-0 slabs with
+    real neighbour exchanges; one JSON line with dp2 slabs and an e2e value."""
+    env = dict(os.environ, OOC_BENCH_BACKEND="gloo", OOC_COMM="ipc")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29543", "bench.py", "--gpus", "2",
+           "--size", "1536", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-parity"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = r.stdout.splitlines()
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["parallelism"].startswith("dp2 dim-0 slabs")
+    assert "one 3072x1536 mesh in 2 dim-0 slabs" in line["e2e"]["mode"]
