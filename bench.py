@@ -662,7 +662,8 @@ def main():
         line["parity"] = par
     if not args.no_cpu:
         try:
-            line["cpu_baseline"] = cpu_reference(1, n_sample=1920, warmup=0)
+            # the same bounded sample as the --impl reference arm's default (5 chains)
+            line["cpu_baseline"] = cpu_reference(5, n_sample=1920, warmup=0)
             line["cpu_baseline"].pop("metric_bytes", None)
             line["cpu_baseline"].pop("loop_time_s", None)
             line["cpu_baseline"]["config1_tiled_explicit"] = cpu_config1()
