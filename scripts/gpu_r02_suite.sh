@@ -1,8 +1,13 @@
 #!/bin/bash
-# BASELINE configs 2-5 + high-reuse span-10 chains; labelled ncu launch lists of the 3-D apps.
+# L2-prefetch variants of the sweep, BASELINE configs 2-5 + high-reuse span-10 chains, and
+# labelled ncu launch lists of the 3-D apps.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 export PYTHONFAULTHANDLER=1
+for v in "OOC_SWEEP_L2AHEAD=4" "OOC_SWEEP_L2AHEAD=12"; do
+  tag=$(echo $v | tr ' =' '_-')
+  env $v timeout 600 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu --no-parity > gpurun_out/r02f_bench_$tag.json 2> gpurun_out/r02f_bench_$tag.err
+done
 timeout 3600 python scripts/suite.py 2 3 4 5 5s10 2s10 > gpurun_out/r02_suite.jsonl 2> gpurun_out/r02_suite.err; echo "suite rc=$?" >> gpurun_out/r02_suite.err
 for spec in "600 miniflow3d" "512 rk3chain3d"; do
   set -- $spec
