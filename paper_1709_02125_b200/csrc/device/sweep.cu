@@ -74,18 +74,37 @@ int ring_cols() {
   }();
   return rc;
 }
-constexpr int kPad = 32;  // doubles of shared memory before/after the rings (edge lanes' neighbour reads)
+// 3-D plane tiles: RB rows (dim 1) x RC columns; measured choices, OOC_SWEEP_RB / OOC_SWEEP_RC3
+int ring_rows3() {
+  static int rb = [] {
+    const char* e = std::getenv("OOC_SWEEP_RB");
+    const int v = e ? std::atoi(e) : 16;
+    return v == 8 || v == 16 || v == 32 ? v : 16;
+  }();
+  return rb;
+}
+int ring_cols3() {
+  static int rc = [] {
+    const char* e = std::getenv("OOC_SWEEP_RC3");
+    const int v = e ? std::atoi(e) : 32;
+    return v == 32 || v == 64 ? v : 32;
+  }();
+  return rc;
+}
 
 // Parameter block; the kernel source declares an identical struct.
 struct SweepParams {
   double* part;              // reduction: one partial per CTA
-  long long R0, R1, C0, C1;  // launch box: rows [R0,R1) x columns [C0,C1), absolute
+  long long R0, R1, C0, C1;  // launch box: rows (dim 0) [R0,R1) x columns (last dim) [C0,C1), absolute
+  long long B0, B1;          // 3-D: launch box along dim 1 (2-D: [0,1))
+  long long ntc;             // CTA tiles along the columns (blockIdx.x = tile_b * ntc + tile_c)
   long long seg_rows;        // rows owned per CTA row-segment
-  long long rng[SW_MAXL][4];  // per loop: rows [0,1), columns [2,3), absolute
+  long long rng[SW_MAXL][6];  // per loop: rows [0,1), columns [2,3), dim 1 [4,5), absolute
   const double* src[SW_MAXD];
   double* dst[SW_MAXD];
-  long long s0[SW_MAXD];      // row stride (elements)
-  long long box[SW_MAXD][4];  // view box: rows [0,1), columns [2,3)
+  long long s0[SW_MAXD];      // dim-0 stride (elements)
+  long long s1[SW_MAXD];      // 3-D: dim-1 stride
+  long long box[SW_MAXD][6];  // view box: rows [0,1), columns [2,3), dim 1 [4,5)
   double cst[SW_MAXC];
 };
 
@@ -93,12 +112,15 @@ const char* kSweepDecl = R"CUDA(
 struct SweepParams {
   double* part;
   long long R0, R1, C0, C1;
+  long long B0, B1;
+  long long ntc;
   long long seg_rows;
-  long long rng[SW_MAXL][4];
+  long long rng[SW_MAXL][6];
   const double* src[SW_MAXD];
   double* dst[SW_MAXD];
   long long s0[SW_MAXD];
-  long long box[SW_MAXD][4];
+  long long s1[SW_MAXD];
+  long long box[SW_MAXD][6];
   double cst[SW_MAXC];
 };
 __device__ __forceinline__ double ooc_min(double a, double b) { return b < a ? b : a; }
@@ -141,10 +163,11 @@ __device__ __forceinline__ void sw_cp8(double* dst, const double* src, bool ok) 
 
 struct Rd {
   long long omin = LLONG_MAX, omax = LLONG_MIN, oc = 0;  // row offsets range, max |column offset|
+  long long ob = 0;                                      // 3-D: max |dim-1 offset|
 };
 
 struct SwLoop {
-  long long lag = 0, h = 0;
+  long long lag = 0, h = 0, hb = 0;  // hb: 3-D halo along dim 1
   std::vector<int> wds;        // dataset of each write
   std::map<int, Rd> rd;        // dataset -> read offsets
   bool barrier = false;        // barrier before this loop (within a step)
@@ -160,6 +183,10 @@ struct SwDs {
 
 struct SwPlan {
   int n = 0, K = 2, P = 2, NT = 256, RC = 128;
+  int nd = 2;                      // 2: thread per ring column; 3: thread per (dim-1, column) of a plane tile
+  int RB = 1;                      // 3-D: tile rows along dim 1 (ring "row" = RB x RCp plane tile)
+  long long HB = 0, TB = 1;        // 3-D: dim-1 halo and owned tile rows
+  long long pad = 32;              // doubles before/after the rings (edge neighbour reads)
   bool tma = false;  // loads: bulk async copies (one thread, mbarrier ring) instead of per-thread cp.async
   long long U = 8;   // ring period: every ring length divides it (0: none small enough, no unrolling)
   int NB = 8;        // load barriers (a multiple of U's steps: constant indices in unrolled steps)
@@ -167,11 +194,18 @@ struct SwPlan {
   long long HC = 0, TC = 0, warm = 0, lagS_max = 0, smem = 0;
   int red_op = OOC_RED_NONE;  // the run's last loop reduces (no writes): folded per CTA
   long long red_lag = 0;
-  long long box[4] = {0, 0, 0, 0};  // launch box rows/cols
+  long long box[6] = {0, 0, 0, 0, 0, 1};  // launch box rows [0,1) / cols [2,3) / dim 1 [4,5)
   std::vector<SwLoop> L;
   std::vector<SwDs> D;
 };
 
+long long smem_budget3() {  // 3-D rings of plane tiles: one CTA per SM
+  static long long b = [] {
+    const char* e = std::getenv("OOC_SWEEP_SMEM3");
+    return e ? std::atoll(e) : 200LL * 1024;
+  }();
+  return b;
+}
 long long smem_budget() {
   static long long b = [] {
     const char* e = std::getenv("OOC_SWEEP_SMEM");
@@ -194,11 +228,16 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   pl.n = n;
   pl.K = K;
   pl.P = P;
-  pl.NT = pl.RC = ring_cols();
+  if (n < 1 || n > SW_MAXL) return fail(why, "group size");
+  pl.nd = Ls[0].ndim;
+  if (pl.nd != 2 && pl.nd != 3) return fail(why, "not 2-D / 3-D");
+  if (pl.nd == 3 && !tma) return fail(why, "3-D sweeps load with TMA only");
+  pl.RC = pl.nd == 2 ? ring_cols() : ring_cols3();
+  pl.RB = pl.nd == 2 ? 1 : ring_rows3();
+  pl.NT = pl.RB * pl.RC;
   pl.tma = tma;
   pl.RCp = tma ? pl.RC + 2 : pl.RC;
-  if (tma) pl.NT = pl.RC + 32;  // + one producer warp issuing the bulk-copy loads
-  if (n < 1 || n > SW_MAXL) return fail(why, "group size");
+  if (tma) pl.NT += 32;  // + one producer warp issuing the bulk-copy loads
   pl.L.resize(static_cast<std::size_t>(n));
   int ncst = 0;
   auto ds_of = [&](const ooc_view& v) -> int {
@@ -209,7 +248,8 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
         if (w.lo[k] != v.lo[k] || w.hi[k] != v.hi[k] || w.stride[k] != v.stride[k]) return -2;
       return static_cast<int>(d);
     }
-    if (v.stride[1] != 1 || v.lo[2] != 0 || v.hi[2] != 1) return -2;
+    if (pl.nd == 2 && (v.stride[1] != 1 || v.lo[2] != 0 || v.hi[2] != 1)) return -2;
+    if (pl.nd == 3 && v.stride[2] != 1) return -2;
     if (pl.D.size() >= SW_MAXD) return -3;
     SwDs D;
     D.v = &v;
@@ -220,10 +260,11 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   for (int i = 0; i < n; ++i) {
     const ooc_loop& L = Ls[i];
     SwLoop& S = pl.L[static_cast<std::size_t>(i)];
-    if (L.ndim != 2) return fail(why, "not 2-D");
+    if (L.ndim != pl.nd) return fail(why, "mixed ranks");
     if (L.reduce_op != OOC_RED_NONE && (i != n - 1 || L.nwrites != 0 || n < 2))
       return fail(why, "reduction (only as the last, write-free loop of a run)");
-    if (L.lo[2] != 0 || L.hi[2] != 1 || L.hi[0] <= L.lo[0] || L.hi[1] <= L.lo[1]) return fail(why, "range");
+    if (L.hi[0] <= L.lo[0] || L.hi[1] <= L.lo[1]) return fail(why, "range");
+    if (pl.nd == 2 ? (L.lo[2] != 0 || L.hi[2] != 1) : L.hi[2] <= L.lo[2]) return fail(why, "range");
     tape_total += L.ntape;
     for (int t = 0; t < L.ntape; ++t) {
       const ooc_ins& in = L.tape[t];
@@ -233,12 +274,14 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
         if (in.arg < 0 || in.arg >= L.nargs) return fail(why, "bad arg");
         const int d = ds_of(L.args[in.arg]);
         if (d < 0) return fail(why, "dataset views differ / too many datasets");
-        if (in.offset[2] != 0 || std::llabs(in.offset[0]) > 8 || std::llabs(in.offset[1]) > 8)
+        if ((pl.nd == 2 && in.offset[2] != 0) || std::llabs(in.offset[0]) > 8 || std::llabs(in.offset[1]) > 8 ||
+            std::llabs(in.offset[2]) > 8)
           return fail(why, "offset");
         Rd& r = S.rd[d];
         r.omin = std::min<long long>(r.omin, in.offset[0]);
         r.omax = std::max<long long>(r.omax, in.offset[0]);
-        r.oc = std::max<long long>(r.oc, std::llabs(in.offset[1]));
+        r.oc = std::max<long long>(r.oc, std::llabs(in.offset[pl.nd - 1]));
+        if (pl.nd == 3) r.ob = std::max<long long>(r.ob, std::llabs(in.offset[1]));
       } else if (in.op < OOC_OP_ADD || in.op > OOC_OP_MAX) {
         return fail(why, "opcode");
       }
@@ -248,7 +291,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
       if (d < 0) return fail(why, "dataset views differ / too many datasets");
       S.wds.push_back(d);
       auto it = S.rd.find(d);
-      if (it != S.rd.end() && (it->second.omin != 0 || it->second.omax != 0 || it->second.oc != 0))
+      if (it != S.rd.end() && (it->second.omin != 0 || it->second.omax != 0 || it->second.oc != 0 || it->second.ob != 0))
         return fail(why, "loop reads its own output at an offset");
     }
   }
@@ -264,20 +307,33 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   for (int d = 0; d < nd; ++d)
     for (int j = 0; j < n; ++j)
       if (writes(j, d)) pl.D[static_cast<std::size_t>(d)].writers.push_back(j);
-  // ---- column halos (backward)
+  // ---- column halos (backward), and along dim 1 for 3-D plane tiles
   for (int k = n - 1; k >= 0; --k)
     for (const auto& [d, r] : pl.L[static_cast<std::size_t>(k)].rd)
       for (int j = 0; j < k; ++j)
-        if (writes(j, d)) pl.L[static_cast<std::size_t>(j)].h = std::max(pl.L[static_cast<std::size_t>(j)].h,
-                                                                        pl.L[static_cast<std::size_t>(k)].h + r.oc);
-  long long HC = 0;
+        if (writes(j, d)) {
+          SwLoop& J = pl.L[static_cast<std::size_t>(j)];
+          const SwLoop& Kl = pl.L[static_cast<std::size_t>(k)];
+          J.h = std::max(J.h, Kl.h + r.oc);
+          J.hb = std::max(J.hb, Kl.hb + r.ob);
+        }
+  long long HC = 0, HB = 0;
   for (const SwLoop& S : pl.L) {
     HC = std::max(HC, S.h);
-    for (const auto& [d, r] : S.rd) HC = std::max(HC, S.h + r.oc);
+    HB = std::max(HB, S.hb);
+    for (const auto& [d, r] : S.rd) {
+      HC = std::max(HC, S.h + r.oc);
+      HB = std::max(HB, S.hb + r.ob);
+    }
   }
   if (HC > 16 || 2 * HC >= pl.RC / 2) return fail(why, "column halo");
+  if (pl.nd == 3 && 2 * HB > pl.RB / 2) return fail(why, "dim-1 halo");
   pl.HC = HC;
   pl.TC = pl.RC - 2 * HC;
+  pl.HB = pl.nd == 3 ? HB : 0;
+  pl.TB = pl.RB - 2 * pl.HB;
+  // shared memory around the rings: the farthest neighbour read of an edge lane
+  pl.pad = std::max<long long>(32, (pl.HB * pl.RCp + pl.HC + 4 + 1) / 2 * 2);
   // ---- loaded / written / out-of-place
   for (int d = 0; d < nd; ++d) {
     SwDs& D = pl.D[static_cast<std::size_t>(d)];
@@ -286,11 +342,14 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
       if (!reads(k, d)) continue;
       const ooc_loop& L = Ls[k];
       const Rd& r = pl.L[static_cast<std::size_t>(k)].rd.at(d);
-      const long long b0 = L.lo[0] + r.omin, b1 = L.hi[0] + r.omax, c0 = L.lo[1] - r.oc, c1 = L.hi[1] + r.oc;
+      const int dc = pl.nd - 1;  // column dimension
+      const long long b0 = L.lo[0] + r.omin, b1 = L.hi[0] + r.omax, c0 = L.lo[dc] - r.oc, c1 = L.hi[dc] + r.oc;
+      const long long y0 = pl.nd == 3 ? L.lo[1] - r.ob : 0, y1 = pl.nd == 3 ? L.hi[1] + r.ob : 1;
       bool covered = false;
       for (int j = 0; j < k && !covered; ++j)
         if (writes(j, d))
-          covered = Ls[j].lo[0] <= b0 && Ls[j].hi[0] >= b1 && Ls[j].lo[1] <= c0 && Ls[j].hi[1] >= c1;
+          covered = Ls[j].lo[0] <= b0 && Ls[j].hi[0] >= b1 && Ls[j].lo[dc] <= c0 && Ls[j].hi[dc] >= c1 &&
+                    (pl.nd == 2 || (Ls[j].lo[1] <= y0 && Ls[j].hi[1] >= y1));
       if (!covered) D.loaded = true;
     }
     D.oop = D.loaded && D.written;
@@ -399,11 +458,11 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
         while (D.W < D.need) D.W *= 2;
       }
       D.off = off;
-      off += D.W * pl.RCp;
+      off += D.W * pl.RCp * pl.RB;
     }
   }
-  pl.smem = (off + 2 * kPad) * 8;
-  if (pl.smem > smem_budget()) return fail(why, "shared memory");
+  pl.smem = (off + 2 * pl.pad) * 8;
+  if (pl.smem > (pl.nd == 2 ? smem_budget() : smem_budget3())) return fail(why, "shared memory");
   // ---- warm-up depth: first correct row of every version (relative to the sweep start)
   const long long NONE = LLONG_MIN / 4;
   std::vector<long long> F(static_cast<std::size_t>(nd), NONE);
@@ -443,7 +502,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   for (int i = 0; i < n && !skew; ++i) {
     SwLoop& S = pl.L[static_cast<std::size_t>(i)];
     bool conflict = false;
-    for (const auto& [d, r] : S.rd) conflict = conflict || (r.oc != 0 && ww[static_cast<std::size_t>(d)]);
+    for (const auto& [d, r] : S.rd) conflict = conflict || ((r.oc != 0 || r.ob != 0) && ww[static_cast<std::size_t>(d)]);
     for (int d : S.wds) conflict = conflict || rc[static_cast<std::size_t>(d)];
     if (conflict && i > 0) {
       S.barrier = true;
@@ -451,27 +510,40 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
       std::fill(ww.begin(), ww.end(), 0);
     }
     for (const auto& [d, r] : S.rd)
-      if (r.oc != 0) rc[static_cast<std::size_t>(d)] = 1;
+      if (r.oc != 0 || r.ob != 0) rc[static_cast<std::size_t>(d)] = 1;
     for (int d : S.wds) ww[static_cast<std::size_t>(d)] = 1;
   }
   // ---- launch box: loop ranges plus the allocations of out-of-place outputs (their
   // shadow must receive every element, written or not)
-  long long bx[4] = {LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN};
-  auto grow = [&](long long r0, long long r1, long long c0, long long c1) {
-    bx[0] = std::min(bx[0], r0);
-    bx[1] = std::max(bx[1], r1);
-    bx[2] = std::min(bx[2], c0);
-    bx[3] = std::max(bx[3], c1);
+  const int dc = pl.nd - 1;  // column (contiguous) dimension
+  long long bx[6] = {LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN, 0, 1};
+  if (pl.nd == 3) {
+    bx[4] = LLONG_MAX;
+    bx[5] = LLONG_MIN;
+  }
+  auto grow = [&](const int64_t* lo, const int64_t* hi) {
+    bx[0] = std::min<long long>(bx[0], lo[0]);
+    bx[1] = std::max<long long>(bx[1], hi[0]);
+    bx[2] = std::min<long long>(bx[2], lo[dc]);
+    bx[3] = std::max<long long>(bx[3], hi[dc]);
+    if (pl.nd == 3) {
+      bx[4] = std::min<long long>(bx[4], lo[1]);
+      bx[5] = std::max<long long>(bx[5], hi[1]);
+    }
   };
-  for (int i = 0; i < n; ++i) grow(Ls[i].lo[0], Ls[i].hi[0], Ls[i].lo[1], Ls[i].hi[1]);
-  const double pts_loops = static_cast<double>(bx[1] - bx[0]) * static_cast<double>(bx[3] - bx[2]);
+  auto npts = [&] {
+    return static_cast<double>(bx[1] - bx[0]) * static_cast<double>(bx[3] - bx[2]) * static_cast<double>(bx[5] - bx[4]);
+  };
+  for (int i = 0; i < n; ++i) grow(Ls[i].lo, Ls[i].hi);
+  const double pts_loops = npts();
   for (const SwDs& D : pl.D)
-    if (D.oop) grow(D.v->lo[0], D.v->hi[0], D.v->lo[1], D.v->hi[1]);
-  const double pts = static_cast<double>(bx[1] - bx[0]) * static_cast<double>(bx[3] - bx[2]);
+    if (D.oop) grow(D.v->lo, D.v->hi);
+  const double pts = npts();
   if (pts > 1.25 * pts_loops + 4096) return fail(why, "out-of-place allocation much larger than the loops");
-  for (int k = 0; k < 4; ++k) pl.box[k] = bx[k];
+  for (int k = 0; k < 6; ++k) pl.box[k] = bx[k];
   // a reducing run writes one partial per CTA into the queue's partial buffer (8192)
-  if (pl.red_op != OOC_RED_NONE && (bx[3] - bx[2] + pl.TC - 1) / pl.TC > 4096)
+  if (pl.red_op != OOC_RED_NONE &&
+      (bx[3] - bx[2] + pl.TC - 1) / pl.TC * ((bx[5] - bx[4] + pl.TB - 1) / pl.TB) > 4096)
     return fail(why, "reduction over too many strips");
   return true;
 }
@@ -489,7 +561,9 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   const int nd = static_cast<int>(pl.D.size());
   const int K = pl.K;
   // barrier among the ring threads (the TMA producer warp only joins the step barriers)
-  const std::string cbar = pl.tma ? "asm volatile(\"bar.sync 1, " + std::to_string(pl.RC) + ";\" ::: \"memory\");"
+  const int NTc = pl.RB * pl.RC;  // consumer (ring) threads
+  const bool d3 = pl.nd == 3;
+  const std::string cbar = pl.tma ? "asm volatile(\"bar.sync 1, " + std::to_string(NTc) + ";\" ::: \"memory\");"
                                   : std::string("__syncthreads();");
   o << "#define SW_MAXL " << SW_MAXL << "\n#define SW_MAXD " << SW_MAXD << "\n#define SW_MAXC " << SW_MAXC << "\n";
   o << kSweepDecl;
@@ -506,9 +580,14 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   o << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p) {\n";
   o << "  extern __shared__ __align__(16) double sw_sm[];\n";
   if (pl.tma) o << "  __shared__ __align__(8) unsigned long long sw_bar[" << pl.NB << "];\n";
-  o << "  const int lc = threadIdx.x;\n";
-  o << "  double* const B = sw_sm + " << kPad << " + lc;\n";
-  o << "  const long long c0 = p.C0 + static_cast<long long>(blockIdx.x) * " << pl.TC << ";\n";
+  // thread -> ring column lc (and, 3-D, tile row lb); CTA tile origin (c0, b0)
+  o << "  const int lc = threadIdx.x % " << pl.RC << ", lb = threadIdx.x / " << pl.RC << ";\n";
+  o << "  double* const B = sw_sm + " << pl.pad << " + lb * " << pl.RCp << " + lc;\n";
+  o << "  const long long c0 = p.C0 + (static_cast<long long>(blockIdx.x) % p.ntc) * " << pl.TC << ";\n";
+  if (d3) {
+    o << "  const long long b0 = p.B0 + (static_cast<long long>(blockIdx.x) / p.ntc) * " << pl.TB << ";\n";
+    o << "  const long long b = b0 - " << pl.HB << " + lb;\n";
+  }
   // one restrict-qualified base per ring: rings never overlap, so the compiler may move
   // a ring's loads across another ring's stores (instruction-level parallelism)
   static const bool restrict_rings = !(std::getenv("OOC_SWEEP_RESTRICT") && std::atoi(std::getenv("OOC_SWEEP_RESTRICT")) == 0);
@@ -558,9 +637,15 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   for (int i = 0; i < pl.n; ++i) {
     const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
     o << "  if (lc >= " << pl.HC - S.h << " && lc < " << pl.HC + pl.TC + S.h << " && c >= p.rng[" << i
-      << "][2] && c < p.rng[" << i << "][3]) colmask |= 1ull << " << i << ";\n";
+      << "][2] && c < p.rng[" << i << "][3]";
+    if (d3)
+      o << " && lb >= " << pl.HB - S.hb << " && lb < " << pl.HB + pl.TB + S.hb << " && b >= p.rng[" << i << "][4] && b < p.rng["
+        << i << "][5]";
+    o << ") colmask |= 1ull << " << i << ";\n";
   }
-  o << "  const bool own_col = lc >= " << pl.HC << " && lc < " << pl.HC + pl.TC << " && c < p.C1;\n";
+  o << "  const bool own_col = lc >= " << pl.HC << " && lc < " << pl.HC + pl.TC << " && c < p.C1";
+  if (d3) o << " && lb >= " << pl.HB << " && lb < " << pl.HB + pl.TB << " && b < p.B1";
+  o << ";\n";
   // interior strip: all 128 ring columns inside every loop range and load box, every
   // owned column inside the launch box — the fast steps then evaluate every loop on
   // every lane without predicates (lanes outside a loop's halo produce values nobody
@@ -574,18 +659,31 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     if (D.loaded || D.store)
       o << "  strip_in = strip_in && p.box[" << d << "][2] <= cl && p.box[" << d << "][3] >= ch;\n";
   }
+  if (d3) {  // the whole plane tile inside every range and box along dim 1 too
+    o << "  const long long bl = b0 - " << pl.HB << ", bh = bl + " << pl.RB << ";\n";
+    o << "  strip_in = strip_in && b0 + " << pl.TB << " <= p.B1;\n";
+    for (int i = 0; i < pl.n; ++i)
+      o << "  strip_in = strip_in && p.rng[" << i << "][4] <= bl && p.rng[" << i << "][5] >= bh;\n";
+    for (int d = 0; d < nd; ++d) {
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (D.loaded || D.store)
+        o << "  strip_in = strip_in && p.box[" << d << "][4] <= bl && p.box[" << d << "][5] >= bh;\n";
+    }
+  }
   for (int d = 0; d < nd; ++d) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     if (D.loaded && !pl.tma)
       o << "  const bool colok" << d << " = c >= p.box[" << d << "][2] && c < p.box[" << d << "][3];\n";
     if (D.store) {
-      o << "  if (own_col && c >= p.box[" << d << "][2] && c < p.box[" << d << "][3]) stmask |= 1u << " << d << ";\n";
+      o << "  if (own_col && c >= p.box[" << d << "][2] && c < p.box[" << d << "][3]";
+      if (d3) o << " && b >= p.box[" << d << "][4] && b < p.box[" << d << "][5]";
+      o << ") stmask |= 1u << " << d << ";\n";
     }
   }
   if (pl.tma) {
-    o << "  if (threadIdx.x == " << pl.RC << ") {\n";
-    o << "    for (int b = 0; b < " << pl.NB << "; ++b)\n";
-    o << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(sw_saddr(&sw_bar[b])) : \"memory\");\n";
+    o << "  if (threadIdx.x == " << NTc << ") {\n";
+    o << "    for (int k = 0; k < " << pl.NB << "; ++k)\n";
+    o << "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(sw_saddr(&sw_bar[k])) : \"memory\");\n";
     o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
     o << "  }\n  __syncthreads();\n";
   }
@@ -595,6 +693,12 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // In an unrolled step (unroll_u >= 0: u = unroll_u modulo the ring period) the slot is a
   // constant; otherwise (u + q) mod W at run time (a mask for power-of-two lengths).
   long long unroll_u = -1;
+  const long long PL = static_cast<long long>(pl.RB) * pl.RCp;  // ring "row": a plane tile in 3-D
+  // a read's cross-thread offset in ring elements: dim-1 offset x pitch + column offset
+  // (0: the thread's own element, so it can be forwarded / carried in registers)
+  auto xoff = [&](const ooc_ins& in) -> long long {
+    return (pl.nd == 3 ? in.offset[1] * pl.RCp : 0) + in.offset[pl.nd - 1];
+  };
   auto at = [&](int d, const std::string& u, long long q, long long oc) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     std::ostringstream e;
@@ -603,11 +707,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     if (unroll_u >= 0 && u == "u + " + std::to_string(K)) extra = K;
     if (extra >= 0) {
       const long long slot = (((unroll_u + extra + q) % D.W) + D.W) % D.W;
-      e << "R" << d << "[" << slot * pl.RCp;
+      e << "R" << d << "[" << slot * PL;
     } else if ((D.W & (D.W - 1)) == 0) {
-      e << "R" << d << "[(((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << pl.RCp;
+      e << "R" << d << "[(((" << u << ") + (" << q << ")) & " << D.W - 1 << ") * " << PL;
     } else {
-      e << "R" << d << "[sw_slot((" << u << ") + (" << q << "), " << D.W << ") * " << pl.RCp;
+      e << "R" << d << "[sw_slot((" << u << ") + (" << q << "), " << D.W << ") * " << PL;
     }
     if (oc) e << " + (" << oc << ")";
     e << "]";
@@ -622,7 +726,8 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         << "][0]) * p.s0[" << d << "] + (c - p.box[" << d << "][2]);\n";
     if (D.store)
       o << "  double* gs" << d << " = p.dst[" << d << "] + (rbase - " << D.lagS << " - p.box[" << d << "][0]) * p.s0[" << d
-        << "] + (c - p.box[" << d << "][2]);\n";
+        << "] + (c - p.box[" << d << "][2])" << (d3 ? " + (b - p.box[" + std::to_string(d) + "][4]) * p.s1[" + std::to_string(d) + "]" : "")
+        << ";\n";
   }
   auto loads = [&](const std::string& step, const char* ind, bool fast, bool running) {
     if (pl.tma) return;  // issued once per step by one thread (tma_issue)
@@ -667,55 +772,78 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     const char* e = std::getenv("OOC_SWEEP_L2AHEAD");  // measured neutral to slightly slower: off
     return e ? std::atoi(e) : 0;
   }();
+  // copies per step: one per loaded dataset and plane-tile row (RB rows in 3-D); lane l
+  // of the producer owns copies l, l + 32, ... (descriptors computed once, in registers)
+  const int ncopy = nload * pl.RB, J = (ncopy + 31) / 32;
   auto tma_issue = [&](const std::string& step, const std::string& pf, const char* ind) {
     o << ind << "{\n" << ind << "  const int sn = " << step << ", pf = " << pf << ";\n";
     o << ind << "  if (sn >= 0 && sn < nsteps) {\n";
     o << ind << "    const unsigned bar = bar0 + static_cast<unsigned>((sn % " << pl.NB << ") * 8);\n";
-    o << ind << "    if (tn) {\n";
-    o << ind << "      asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
-    for (int r = 0; r < K; ++r) {
-      o << ind << "      {\n" << ind << "        const long long v = vr0 + static_cast<long long>(sn) * " << K << " + " << r << ";\n";
-      o << ind << "        if (v >= 0 && v < nrows) {\n";
-      o << ind << "          asm volatile(\"mbarrier.expect_tx.shared::cta.b64 [%0], %1;\" :: \"r\"(bar), \"r\"(tn) : \"memory\");\n";
-      o << ind << "          sw_bulk(dst + static_cast<unsigned>(sw_slot(sn * " << K << " + " << r << " - lagL, wlen) * " << pl.RCp * 8
-        << "), src + v * s0, tn, bar);\n";
-      o << ind << "        }\n" << ind << "      }\n";
-    }
-    o << ind << "    }\n" << ind << "    __syncwarp();\n";
+    o << ind << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+    for (int j = 0; j < J; ++j)
+      for (int r = 0; r < K; ++r) {
+        const std::string js = std::to_string(j);
+        o << ind << "    {\n" << ind << "      const long long v = vr0_" << js << " + static_cast<long long>(sn) * " << K << " + " << r
+          << ";\n";
+        o << ind << "      if (tn_" << js << " && v >= 0 && v < nrows_" << js << ") {\n";
+        o << ind << "        asm volatile(\"mbarrier.expect_tx.shared::cta.b64 [%0], %1;\" :: \"r\"(bar), \"r\"(tn_" << js
+          << ") : \"memory\");\n";
+        o << ind << "        sw_bulk(dst_" << js << " + static_cast<unsigned>(sw_slot(sn * " << K << " + " << r << " - lagL_" << js
+          << ", wlen_" << js << ") * " << PL * 8 << "), src_" << js << " + v * s0_" << js << ", tn_" << js << ", bar);\n";
+        o << ind << "      }\n" << ind << "    }\n";
+      }
+    o << ind << "    __syncwarp();\n";
     o << ind << "    if (lane == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" :: \"r\"(bar) : \"memory\");\n";
     o << ind << "  }\n";
-    o << ind << "  if (tn && pf >= 0 && pf < nsteps) {\n";
-    for (int r = 0; r < K; ++r) {
-      o << ind << "    {\n" << ind << "      const long long v = vr0 + static_cast<long long>(pf) * " << K << " + " << r << ";\n";
-      o << ind << "      if (v >= 0 && v < nrows)\n";
-      o << ind << "        asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(src + v * s0), \"r\"(tn) : \"memory\");\n";
-      o << ind << "    }\n";
-    }
+    o << ind << "  if (pf >= 0 && pf < nsteps) {\n";
+    for (int j = 0; j < J; ++j)
+      for (int r = 0; r < K; ++r) {
+        const std::string js = std::to_string(j);
+        o << ind << "    {\n" << ind << "      const long long v = vr0_" << js << " + static_cast<long long>(pf) * " << K << " + " << r
+          << ";\n";
+        o << ind << "      if (tn_" << js << " && v >= 0 && v < nrows_" << js << ")\n";
+        o << ind << "        asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(src_" << js << " + v * s0_" << js
+          << "), \"r\"(tn_" << js << ") : \"memory\");\n";
+        o << ind << "    }\n";
+      }
     o << ind << "  }\n" << ind << "}\n";
   };
   if (pl.tma) {
-    o << "  if (threadIdx.x >= " << pl.RC << ") {  // ---- producer warp\n";
-    o << "    const int lane = threadIdx.x - " << pl.RC << ";\n";
-    o << "    int dd = -1, lagL = 0, wlen = 1, roff = 0;\n";
-    int i = 0;
-    for (int d = 0; d < nd; ++d) {
-      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
-      if (!D.loaded) continue;
-      o << "    " << (i ? "else if" : "if") << " (lane == " << i << ") { dd = " << d << "; lagL = " << D.lagL << "; wlen = " << D.W
-        << "; roff = " << kPad + D.off << "; }\n";
-      ++i;
+    o << "  if (threadIdx.x >= " << NTc << ") {  // ---- producer warp\n";
+    o << "    const int lane = threadIdx.x - " << NTc << ";\n";
+    for (int j = 0; j < J; ++j) {
+      const std::string js = std::to_string(j);
+      o << "    const double* src_" << js << " = nullptr;\n    long long s0_" << js << " = 0, vr0_" << js << " = 0, nrows_" << js
+        << " = 0;\n    unsigned dst_" << js << " = 0, tn_" << js << " = 0;\n    int lagL_" << js << " = 0, wlen_" << js << " = 1;\n";
+      o << "    {\n      const int idx = lane + " << 32 * j << ", li = idx / " << pl.RB << ", rb = idx % " << pl.RB << ";\n";
+      o << "      int dd = -1;\n      long long roff = 0;\n";
+      int i = 0;
+      for (int d = 0; d < nd; ++d) {
+        const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+        if (!D.loaded) continue;
+        o << "      " << (i ? "else if" : "if") << " (idx < " << ncopy << " && li == " << i << ") { dd = " << d << "; lagL_" << js
+          << " = " << D.lagL << "; wlen_" << js << " = " << D.W << "; roff = " << pl.pad + D.off << "; }\n";
+        ++i;
+      }
+      o << "      if (dd >= 0) {\n";
+      o << "        const long long cs = c0 - " << pl.HC << " - p.box[dd][2];\n";
+      o << "        const long long a0 = cs > 0 ? (cs & ~1LL) : 0LL;\n";
+      o << "        const long long a1 = (min(cs + " << pl.RC << "LL, p.box[dd][3] - p.box[dd][2]) + 1) & ~1LL;\n";
+      if (d3) {
+        o << "        const long long yb = b0 - " << pl.HB << " + rb - p.box[dd][4];  // this copy's dim-1 row in the view\n";
+        o << "        const bool yok = yb >= 0 && yb < p.box[dd][5] - p.box[dd][4];\n";
+      } else {
+        o << "        const bool yok = true;\n        const long long yb = 0;\n";
+      }
+      o << "        tn_" << js << " = yok && a1 > a0 ? static_cast<unsigned>(a1 - a0) * 8u : 0u;\n";
+      o << "        src_" << js << " = p.src[dd] + a0" << (d3 ? " + yb * p.s1[dd]" : "") << ";\n";
+      o << "        s0_" << js << " = p.s0[dd];\n";
+      o << "        vr0_" << js << " = rbase - p.box[dd][0] - lagL_" << js << ";  // view row of step sn, row r: vr0 + sn*K + r\n";
+      o << "        nrows_" << js << " = p.box[dd][1] - p.box[dd][0];\n";
+      o << "        dst_" << js << " = sw_saddr(sw_sm) + static_cast<unsigned>((roff + rb * " << pl.RCp
+        << " + a0 - (cs - (cs & 1))) * 8);\n";
+      o << "        (void)yb;\n      }\n    }\n";
     }
-    o << "    const double* src = nullptr;\n    long long s0 = 0, vr0 = 0, nrows = 0;\n    unsigned dst = 0, tn = 0;\n";
-    o << "    if (dd >= 0) {\n";
-    o << "      const long long cs = c0 - " << pl.HC << " - p.box[dd][2];\n";
-    o << "      const long long a0 = cs > 0 ? (cs & ~1LL) : 0LL;\n";
-    o << "      const long long a1 = (min(cs + " << pl.RC << "LL, p.box[dd][3] - p.box[dd][2]) + 1) & ~1LL;\n";
-    o << "      tn = a1 > a0 ? static_cast<unsigned>(a1 - a0) * 8u : 0u;\n";
-    o << "      src = p.src[dd] + a0;\n      s0 = p.s0[dd];\n";
-    o << "      vr0 = rbase - p.box[dd][0] - lagL;  // view row of step sn, row r: vr0 + sn*K + r\n";
-    o << "      nrows = p.box[dd][1] - p.box[dd][0];\n";
-    o << "      dst = sw_saddr(sw_sm) + static_cast<unsigned>((roff + a0 - (cs - (cs & 1))) * 8);\n";
-    o << "    }\n";
     o << "    const unsigned bar0 = sw_saddr(sw_bar);\n";
     o << "    for (int t = 0; t < " << pl.P + std::max(l2_ahead, 0) << "; ++t)\n";
     tma_issue("t < " + std::to_string(pl.P) + " ? t : -1",
@@ -744,7 +872,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       if (L.tape[t].op == OOC_OP_READ)
         for (int d = 0; d < nd; ++d)
           if (pl.D[static_cast<std::size_t>(d)].v->data == L.args[L.tape[t].arg].data)
-            out.emplace_back(d, L.tape[t].offset[0], L.tape[t].offset[1]);
+            out.emplace_back(d, L.tape[t].offset[0], xoff(L.tape[t]));
   };
   std::vector<std::vector<char>> need_sts(static_cast<std::size_t>(pl.n), std::vector<char>(static_cast<std::size_t>(nd), 0));
   std::vector<int> last_writer(static_cast<std::size_t>(nd), -1);
@@ -832,12 +960,12 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
               st.push_back("p.cst[" + std::to_string(ci++) + "]");
             } else if (in.op == OOC_OP_READ) {
               const int d = dsof_arg[in.arg];
-              const auto key = std::make_tuple(d, q0 + in.offset[0], static_cast<long long>(in.offset[1]));
-              if (info && touched.insert(key).second && in.offset[1] == 0) info->first_read.push_back(key);
+              const auto key = std::make_tuple(d, q0 + in.offset[0], xoff(in));
+              if (info && touched.insert(key).second && xoff(in) == 0) info->first_read.push_back(key);
               auto it = forward ? cache.find(key) : cache.end();
               if (it == cache.end()) {
                 const std::string name = pre + std::to_string(tmp++);
-                o << ind << "const double " << name << " = " << at(d, "u", q0 + in.offset[0], in.offset[1]) << ";\n";
+                o << ind << "const double " << name << " = " << at(d, "u", q0 + in.offset[0], xoff(in)) << ";\n";
                 it = cache.emplace(key, name).first;
                 if (info) info->miss[static_cast<std::size_t>(d)] = 1;
               }
@@ -982,7 +1110,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
             st.push_back("p.cst[" + std::to_string(ci++) + "]");
           } else if (in.op == OOC_OP_READ) {
             const std::string name = "v" + is + "_" + std::to_string(tmp++);
-            o << ind << "      const double " << name << " = " << at(dsof_arg[in.arg], ur, in.offset[0], in.offset[1])
+            o << ind << "      const double " << name << " = " << at(dsof_arg[in.arg], ur, in.offset[0], xoff(in))
               << ";\n";
             st.push_back(name);
           } else {
@@ -1029,7 +1157,8 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
           o << " && (false";
           for (int j : D.writers)
             o << " || (row >= p.rng[" << j << "][0] && row < p.rng[" << j << "][1] && c >= p.rng[" << j
-              << "][2] && c < p.rng[" << j << "][3])";
+              << "][2] && c < p.rng[" << j << "][3]"
+              << (d3 ? " && b >= p.rng[" + std::to_string(j) + "][4] && b < p.rng[" + std::to_string(j) + "][5]" : "") << ")";
           o << ")";
         }
         o << ")\n";
@@ -1099,11 +1228,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   if (pl.red_op != OOC_RED_NONE) {  // warp tree, then the CTA's warps in order: one partial per CTA
     o << "#pragma unroll\n  for (int w = 16; w > 0; w >>= 1) racc = ooc_red(" << pl.red_op
       << ", racc, __shfl_down_sync(0xffffffffu, racc, w));\n";
-    o << "  __shared__ double red_warp[" << pl.RC / 32 << "];\n";
+    o << "  __shared__ double red_warp[" << NTc / 32 << "];\n";
     o << "  if ((threadIdx.x & 31) == 0) red_warp[threadIdx.x >> 5] = racc;\n  " << cbar << "\n";
-    o << "  if (threadIdx.x == 0) {\n    double b = red_warp[0];\n";
-    o << "    for (int w = 1; w < " << pl.RC / 32 << "; ++w) b = ooc_red(" << pl.red_op << ", b, red_warp[w]);\n";
-    o << "    p.part[static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x] = b;\n  }\n";
+    o << "  if (threadIdx.x == 0) {\n    double bsum = red_warp[0];\n";
+    o << "    for (int w = 1; w < " << NTc / 32 << "; ++w) bsum = ooc_red(" << pl.red_op << ", bsum, red_warp[w]);\n";
+    o << "    p.part[static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x] = bsum;\n  }\n";
   }
   o << "}\n";
   return o.str();
@@ -1402,26 +1531,38 @@ extern "C" int ooc_sweep_describe(const ooc_loop* loops, int n, const ooc_redire
   long long loaded = 0, stored = 0;
   for (const SwDs& D : pl.D) {
     const ooc_view& v = *D.v;
-    const long long cols = v.hi[1] - v.lo[1];
+    // extent of the view across the non-row dimensions (2-D: columns; 3-D: dim 1 x dim 2)
+    long long plane = 1;
+    for (int k = 1; k < pl.nd; ++k) plane *= v.hi[k] - v.lo[k];
     if (D.loaded) {
       const long long r0 = std::max<long long>(v.lo[0], pl.box[0] - pl.warm), r1 = std::min<long long>(v.hi[0], pl.box[1]);
-      loaded += std::max<long long>(0, r1 - r0) * cols * 8;
+      loaded += std::max<long long>(0, r1 - r0) * plane * 8;
     }
     if (D.store) {
-      long long b[4] = {pl.box[0], pl.box[1], pl.box[2], pl.box[3]};
-      if (!D.oop) {  // in place: the writers' ranges
-        b[0] = b[2] = LLONG_MAX;
-        b[1] = b[3] = LLONG_MIN;
-        for (int j : D.writers) {
-          b[0] = std::min<long long>(b[0], loops[j].lo[0]);
-          b[1] = std::max<long long>(b[1], loops[j].hi[0]);
-          b[2] = std::min<long long>(b[2], loops[j].lo[1]);
-          b[3] = std::max<long long>(b[3], loops[j].hi[1]);
-        }
+      long long lo[3] = {pl.box[0], 0, 0}, hi[3] = {pl.box[1], 1, 1};
+      if (pl.nd == 2) {
+        lo[1] = pl.box[2];
+        hi[1] = pl.box[3];
+      } else {
+        lo[1] = pl.box[4];
+        hi[1] = pl.box[5];
+        lo[2] = pl.box[2];
+        hi[2] = pl.box[3];
       }
-      const long long rr = std::min<long long>(b[1], v.hi[0]) - std::max<long long>(b[0], v.lo[0]);
-      const long long cc = std::min<long long>(b[3], v.hi[1]) - std::max<long long>(b[2], v.lo[1]);
-      stored += std::max<long long>(0, rr) * std::max<long long>(0, cc) * 8;
+      if (!D.oop) {  // in place: the writers' ranges
+        for (int k = 0; k < 3; ++k) {
+          lo[k] = LLONG_MAX;
+          hi[k] = LLONG_MIN;
+        }
+        for (int j : D.writers)
+          for (int k = 0; k < 3; ++k) {
+            lo[k] = std::min<long long>(lo[k], loops[j].lo[k]);
+            hi[k] = std::max<long long>(hi[k], loops[j].hi[k]);
+          }
+      }
+      long long pts = 1;
+      for (int k = 0; k < pl.nd; ++k) pts *= std::max<long long>(0, std::min<long long>(hi[k], v.hi[k]) - std::max<long long>(lo[k], v.lo[k]));
+      stored += pts * 8;
     }
   }
   o << "],\"dram_bytes\":{\"loaded\":" << loaded << ",\"stored\":" << stored << "}}";
@@ -1541,11 +1682,16 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   sp.R1 = pl.box[1];
   sp.C0 = pl.box[2];
   sp.C1 = pl.box[3];
+  sp.B0 = pl.box[4];
+  sp.B1 = pl.box[5];
+  const int dc = pl.nd - 1;  // column dimension of the loops and views
   for (int i = 0; i < n; ++i) {
     sp.rng[i][0] = loops[i].lo[0];
     sp.rng[i][1] = loops[i].hi[0];
-    sp.rng[i][2] = loops[i].lo[1];
-    sp.rng[i][3] = loops[i].hi[1];
+    sp.rng[i][2] = loops[i].lo[dc];
+    sp.rng[i][3] = loops[i].hi[dc];
+    sp.rng[i][4] = pl.nd == 3 ? loops[i].lo[1] : 0;
+    sp.rng[i][5] = pl.nd == 3 ? loops[i].hi[1] : 1;
   }
   for (std::size_t d = 0; d < pl.D.size(); ++d) {
     const SwDs& D = pl.D[d];
@@ -1553,10 +1699,13 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
     sp.src[d] = v.data;
     sp.dst[d] = v.data;
     sp.s0[d] = v.stride[0];
+    sp.s1[d] = pl.nd == 3 ? v.stride[1] : 0;
     sp.box[d][0] = v.lo[0];
     sp.box[d][1] = v.hi[0];
-    sp.box[d][2] = v.lo[1];
-    sp.box[d][3] = v.hi[1];
+    sp.box[d][2] = v.lo[dc];
+    sp.box[d][3] = v.hi[dc];
+    sp.box[d][4] = pl.nd == 3 ? v.lo[1] : 0;
+    sp.box[d][5] = pl.nd == 3 ? v.hi[1] : 1;
     if (D.oop && D.store) {
       double* to = nullptr;
       for (int r = 0; r < nred; ++r)
@@ -1569,7 +1718,10 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
     }
   }
   const long long rows = pl.box[1] - pl.box[0];
-  const long long strips = (pl.box[3] - pl.box[2] + pl.TC - 1) / pl.TC;
+  // CTA tiles: strips of TC columns (x ntb tiles of TB rows along dim 1 in 3-D)
+  const long long ntc = (pl.box[3] - pl.box[2] + pl.TC - 1) / pl.TC;
+  const long long strips = ntc * ((pl.box[5] - pl.box[4] + pl.TB - 1) / pl.TB);
+  sp.ntc = ntc;
   // Row segments per strip: whole waves of CTAs (the grid is strips x segments; a
   // partial last wave idles SMs), at least ~4 waves, segments >= 8 warm-up depths.
   // A reducing run folds one partial per CTA in CTA order, so its partition must not

@@ -47,6 +47,21 @@ def test_sweep_apps_vs_oracle(app, nx, ny, iters, span, jit_always):
     assert rt.device()["sweep_launches"] > 0
 
 
+@pytest.mark.parametrize("app,nx,ny,nz,iters,span", [
+    ("miniflow3d", 40, 36, 30, 12, 0),
+    ("miniflow3d", 70, 45, 66, 10, 0),
+    ("rk3chain3d", 32, 30, 28, 3, 3),
+    ("rk3chain3d", 60, 41, 37, 2, 1),
+])
+def test_sweep_3d_apps_vs_oracle(app, nx, ny, nz, iters, span, jit_always):
+    """3-D chains as plane-tile sweeps (threads over a dim-1 x column tile, rings of plane
+    tiles, dim-1 and column halos recomputed): bit-identical to the oracle."""
+    prog = P.app_program(app, nx, ny, nz, iters=iters, span=span)
+    diff, rt = _resident_vs_oracle(prog)
+    assert not diff, diff
+    assert rt.device()["sweep_launches"] > 0
+
+
 def test_sweep_random_programs_vs_golden(golden_random, jit_always):
     """Random 2-D chains (mixed stencils, ranges, read-write loops, flushes, reductions)
     through the resident executor: the reference's golden buffers and reductions."""

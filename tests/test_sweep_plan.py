@@ -43,10 +43,16 @@ def test_miniflow2d_timesteps_fuse_into_sweeps(jit_always):
     assert sum(d["oop"] for d in first) == 3
 
 
-def test_3d_chains_are_not_swept(jit_always):
-    rt, chains = _chains(P.app_program("miniflow3d", 12, 10, 8, iters=3))
-    for c in chains:
-        assert rt.chain_sweep_check(c, compile=False) == []
+def test_3d_chains_sweep_as_plane_tiles(jit_always):
+    """3-D chains become plane-tile sweeps (TMA row copies per tile row) whose kernels
+    compile for sm_100a; a whole miniflow3d timestep fits one run."""
+    for app, kw in (("miniflow3d", dict(iters=3)), ("rk3chain3d", dict(iters=3, span=3))):
+        rt, chains = _chains(P.app_program(app, 24, 20, 18, **kw))
+        runs = [g for c in chains for g in rt.chain_sweep_check(c, compile=True)]
+        assert runs and all(g["ok"] for g in runs), runs
+        if app == "miniflow3d":
+            assert any(g["loops"] >= 14 for g in runs)
+            assert all(g["plan"]["tma"] == 1 for g in runs)
 
 
 def test_random_2d_chains_compile(jit_always):
