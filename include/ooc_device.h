@@ -197,6 +197,10 @@ typedef struct {
   double* dst;       /* buffer receiving its new values (same box and strides); NULL: dead */
 } ooc_redirect;
 int ooc_sweep_check(const ooc_loop* loops, int n, int* flags);
+/* 3-D chains as plane-tile sweeps (threads over a dim-1 x column tile of each plane,
+ * rings of plane tiles): 1 enables, 0 disables (default: OOC_SWEEP_3D, else off). */
+void ooc_sweep_set_3d(int on);
+int ooc_sweep_3d_enabled(void);
 int ooc_launch_sweep(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n, const ooc_redirect* redirects,
                      int nredirects);
 /* JSON description of the sweep plan (lags, halos, rings, load mode) and its compulsory

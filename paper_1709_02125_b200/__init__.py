@@ -398,6 +398,13 @@ def set_sweep(on: bool) -> None:
     _native.lib().ooc_rt_set_sweep(int(bool(on)))
 
 
+def set_sweep_3d(on: bool) -> None:
+    """Process-wide: 3-D chains as plane-tile row sweeps (ooc_sweep_set_3d)."""
+    _native.lib()
+    dev = ctypes.CDLL(_native.device_lib_path())
+    dev.ooc_sweep_set_3d(int(bool(on)))
+
+
 def set_row_recompute(on: bool) -> None:
     """Process-wide fusion policy (ooc_rt_set_row_recompute)."""
     _native.lib().ooc_rt_set_row_recompute(int(bool(on)))

@@ -199,6 +199,13 @@ struct SwPlan {
   std::vector<SwDs> D;
 };
 
+// 3-D plane-tile sweeps: off by default (measured slower than the fused 3-D launches so
+// far, profiles/r02_summary.md); ooc_sweep_set_3d(1) / OOC_SWEEP_3D=1 enables them
+int g_sweep3d = -1;
+bool sweep_3d_enabled() {
+  if (g_sweep3d < 0) g_sweep3d = std::getenv("OOC_SWEEP_3D") && std::atoi(std::getenv("OOC_SWEEP_3D")) == 1 ? 1 : 0;
+  return g_sweep3d == 1;
+}
 long long smem_budget3() {  // 3-D rings of plane tiles: one CTA per SM
   static long long b = [] {
     const char* e = std::getenv("OOC_SWEEP_SMEM3");
@@ -231,6 +238,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   if (n < 1 || n > SW_MAXL) return fail(why, "group size");
   pl.nd = Ls[0].ndim;
   if (pl.nd != 2 && pl.nd != 3) return fail(why, "not 2-D / 3-D");
+  if (pl.nd == 3 && !sweep_3d_enabled()) return fail(why, "3-D sweeps disabled (ooc_sweep_set_3d)");
   if (pl.nd == 3 && !tma) return fail(why, "3-D sweeps load with TMA only");
   pl.RC = pl.nd == 2 ? ring_cols() : ring_cols3();
   pl.RB = pl.nd == 2 ? 1 : ring_rows3();
@@ -1461,6 +1469,14 @@ void resolve_tuning(SwTune& T) {  // timings that finished since the last launch
 }
 
 }  // namespace
+
+extern "C" int ooc_sweep_3d_enabled(void) { return sweep_3d_enabled() ? 1 : 0; }
+
+extern "C" void ooc_sweep_set_3d(int on) {
+  std::lock_guard<std::mutex> lk(g_sw_mu);
+  g_sweep3d = on ? 1 : 0;
+  g_sw_checks.clear();  // cached verdicts depend on it
+}
 
 extern "C" int ooc_sweep_check(const ooc_loop* loops, int n, int* oop_args) {
   OOC_ARG_CHECK(loops && n > 0, "ooc_sweep_check: bad args");

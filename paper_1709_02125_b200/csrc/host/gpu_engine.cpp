@@ -1223,7 +1223,8 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
     int jm = 1;
     long long jmin = 0;
     ooc_jit_policy(&jm, &jmin);
-    const std::string key = sweep_key(mesh, chain) + "|" + std::to_string(jm) + "|" + std::to_string(jmin);
+    const std::string key = sweep_key(mesh, chain) + "|" + std::to_string(jm) + "|" + std::to_string(jmin) + "|" +
+                            std::to_string(ooc_sweep_3d_enabled());
     auto it = sweep_cache.find(key);
     if (it == sweep_cache.end()) {
       std::vector<ooc_loop> calls;

@@ -56,10 +56,14 @@ def test_sweep_apps_vs_oracle(app, nx, ny, iters, span, jit_always):
 def test_sweep_3d_apps_vs_oracle(app, nx, ny, nz, iters, span, jit_always):
     """3-D chains as plane-tile sweeps (threads over a dim-1 x column tile, rings of plane
     tiles, dim-1 and column halos recomputed): bit-identical to the oracle."""
-    prog = P.app_program(app, nx, ny, nz, iters=iters, span=span)
-    diff, rt = _resident_vs_oracle(prog)
-    assert not diff, diff
-    assert rt.device()["sweep_launches"] > 0
+    B.set_sweep_3d(True)
+    try:
+        prog = P.app_program(app, nx, ny, nz, iters=iters, span=span)
+        diff, rt = _resident_vs_oracle(prog)
+        assert not diff, diff
+        assert rt.device()["sweep_launches"] > 0
+    finally:
+        B.set_sweep_3d(False)
 
 
 def test_sweep_random_programs_vs_golden(golden_random, jit_always):

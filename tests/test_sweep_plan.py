@@ -46,6 +46,10 @@ def test_miniflow2d_timesteps_fuse_into_sweeps(jit_always):
 def test_3d_chains_sweep_as_plane_tiles(jit_always):
     """3-D chains become plane-tile sweeps (TMA row copies per tile row) whose kernels
     compile for sm_100a; a whole miniflow3d timestep fits one run."""
+    B.set_sweep_3d(False)
+    rt, chains = _chains(P.app_program("miniflow3d", 24, 20, 18, iters=3))
+    assert all(rt.chain_sweep_check(c, compile=False) == [] for c in chains)  # off by default
+    B.set_sweep_3d(True)
     for app, kw in (("miniflow3d", dict(iters=3)), ("rk3chain3d", dict(iters=3, span=3))):
         rt, chains = _chains(P.app_program(app, 24, 20, 18, **kw))
         runs = [g for c in chains for g in rt.chain_sweep_check(c, compile=True)]
@@ -53,6 +57,7 @@ def test_3d_chains_sweep_as_plane_tiles(jit_always):
         if app == "miniflow3d":
             assert any(g["loops"] >= 14 for g in runs)
             assert all(g["plan"]["tma"] == 1 for g in runs)
+    B.set_sweep_3d(False)
 
 
 def test_random_2d_chains_compile(jit_always):
