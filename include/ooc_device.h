@@ -198,7 +198,7 @@ typedef struct {
 } ooc_redirect;
 int ooc_sweep_check(const ooc_loop* loops, int n, int* flags);
 /* 3-D chains as plane-tile sweeps (threads over a dim-1 x column tile of each plane,
- * rings of plane tiles): 1 enables, 0 disables (default: OOC_SWEEP_3D, else off). */
+ * rings of plane tiles): 1 enables, 0 disables (default on; OOC_SWEEP_3D=0 turns them off). */
 void ooc_sweep_set_3d(int on);
 int ooc_sweep_3d_enabled(void);
 int ooc_launch_sweep(ooc_ctx* ctx, int queue, const ooc_loop* loops, int n, const ooc_redirect* redirects,

@@ -1682,6 +1682,24 @@ bool jit_available(bool load, std::string& why) {
   return load ? a.ok : a.nvrtc_ok;
 }
 
+// Tiled tensor map of an f64 view (driver cuTensorMapEncodeTiled, no swizzle, zero fill
+// out of bounds). gdim / box innermost first; gstride_bytes: rank - 1 strides.
+bool jit_tensor_map(void* out128, int rank, const double* base, const unsigned long long* gdim,
+                    const unsigned long long* gstride_bytes, const unsigned* box) {
+  Api& a = api();
+  if (!a.ok || !a.encode_tiled) return false;
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bx[5], es[5] = {1, 1, 1, 1, 1};
+  for (int k = 0; k < rank; ++k) {
+    gd[k] = gdim[k];
+    bx[k] = box[k];
+    if (k + 1 < rank) gs[k] = gstride_bytes[k];
+  }
+  return a.encode_tiled(static_cast<CUtensorMap*>(out128), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(rank),
+                        const_cast<double*>(base), gd, gs, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool jit_build_kernel(const std::string& src, const char* kname, int block, long long smem, void** fn,
                       int* occ, std::string& err, bool load) {
   if (!jit_available(load, err)) return false;

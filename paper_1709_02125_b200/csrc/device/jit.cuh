@@ -43,6 +43,10 @@ int launch_fold(ooc_ctx* c, int q, int blocks, int slot, int op);
 extern bool g_frozen;  // graph capture in progress: no tuning launches (ooc_jit_freeze)
 bool jit_build_kernel(const std::string& src, const char* kname, int block, long long smem, void** fn,
                       int* occ, std::string& err, bool load);
+// Tiled f64 tensor map for TMA tensor copies (zero fill out of bounds); false if the driver
+// entry point is unavailable or rejects the layout.
+bool jit_tensor_map(void* out128, int rank, const double* base, const unsigned long long* gdim,
+                    const unsigned long long* gstride_bytes, const unsigned* box);
 int jit_launch_kernel(ooc_ctx* c, int q, void* fn, unsigned gx, unsigned gy, unsigned block, unsigned smem,
                       void** args);
 }

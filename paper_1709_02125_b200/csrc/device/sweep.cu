@@ -151,6 +151,13 @@ __device__ __forceinline__ void sw_bulk(unsigned dst, const double* src, unsigne
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+// 3-D: one tiled tensor copy per dataset and step — the whole RB x RCp plane tile, out-of-
+// bounds elements zero-filled (innermost coordinate even: 16-byte aligned; negative is fine)
+struct __align__(64) SwMaps { unsigned long long t[SW_MAXD][16]; };
+__device__ __forceinline__ void sw_tensor3(unsigned dst, const void* map, int x, int y, int z, unsigned bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               :: "r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar) : "memory");
+}
 __device__ __forceinline__ int sw_slot(int x, int w) {  // x mod w, for rings of any length
   const int r = x % w;
   return r < 0 ? r + w : r;
@@ -199,11 +206,12 @@ struct SwPlan {
   std::vector<SwDs> D;
 };
 
-// 3-D plane-tile sweeps: off by default (measured slower than the fused 3-D launches so
-// far, profiles/r02_summary.md); ooc_sweep_set_3d(1) / OOC_SWEEP_3D=1 enables them
+// 3-D plane-tile sweeps: on by default (measured 1.9x / 1.5x over the fused 3-D launches
+// on miniflow3d / rk3chain3d, profiles/r02_summary.md); ooc_sweep_set_3d(0) / OOC_SWEEP_3D=0
+// turns them off
 int g_sweep3d = -1;
 bool sweep_3d_enabled() {
-  if (g_sweep3d < 0) g_sweep3d = std::getenv("OOC_SWEEP_3D") && std::atoi(std::getenv("OOC_SWEEP_3D")) == 1 ? 1 : 0;
+  if (g_sweep3d < 0) g_sweep3d = std::getenv("OOC_SWEEP_3D") && std::atoi(std::getenv("OOC_SWEEP_3D")) == 0 ? 0 : 1;
   return g_sweep3d == 1;
 }
 long long smem_budget3() {  // 3-D rings of plane tiles: one CTA per SM
@@ -341,7 +349,9 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   pl.HB = pl.nd == 3 ? HB : 0;
   pl.TB = pl.RB - 2 * pl.HB;
   // shared memory around the rings: the farthest neighbour read of an edge lane
-  pl.pad = std::max<long long>(32, (pl.HB * pl.RCp + pl.HC + 4 + 1) / 2 * 2);
+  // (a multiple of 16 doubles: 3-D tensor copies land on 128-byte aligned plane slots)
+  pl.pad = (std::max<long long>(32, pl.HB * pl.RCp + pl.HC + 4) + 15) / 16 * 16;
+  if (pl.nd == 3 && (static_cast<long long>(pl.RB) * pl.RCp) % 16 != 0) return fail(why, "plane tile not 128-byte aligned");
   // ---- loaded / written / out-of-place
   for (int d = 0; d < nd; ++d) {
     SwDs& D = pl.D[static_cast<std::size_t>(d)];
@@ -585,8 +595,9 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   o << "extern \"C\" __global__ void __launch_bounds__(" << pl.NT;
   if (min_blocks > 0) o << ", " << min_blocks;
   else if (smem_occ > 1) o << ", " << smem_occ;
-  o << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p) {\n";
-  o << "  extern __shared__ __align__(16) double sw_sm[];\n";
+  o << ") ooc_sweep_kernel(const __grid_constant__ SweepParams p" << (d3 ? ", const __grid_constant__ SwMaps m" : "")
+    << ") {\n";
+  o << "  extern __shared__ __align__(128) double sw_sm[];\n";
   if (pl.tma) o << "  __shared__ __align__(8) unsigned long long sw_bar[" << pl.NB << "];\n";
   // thread -> ring column lc (and, 3-D, tile row lb); CTA tile origin (c0, b0)
   o << "  const int lc = threadIdx.x % " << pl.RC << ", lb = threadIdx.x / " << pl.RC << ";\n";
@@ -782,7 +793,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   }();
   // copies per step: one per loaded dataset and plane-tile row (RB rows in 3-D); lane l
   // of the producer owns copies l, l + 32, ... (descriptors computed once, in registers)
-  const int ncopy = nload * pl.RB, J = (ncopy + 31) / 32;
+  const int ncopy = d3 ? nload : nload * pl.RB, J = (ncopy + 31) / 32;
   auto tma_issue = [&](const std::string& step, const std::string& pf, const char* ind) {
     o << ind << "{\n" << ind << "  const int sn = " << step << ", pf = " << pf << ";\n";
     o << ind << "  if (sn >= 0 && sn < nsteps) {\n";
@@ -796,8 +807,13 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         o << ind << "      if (tn_" << js << " && v >= 0 && v < nrows_" << js << ") {\n";
         o << ind << "        asm volatile(\"mbarrier.expect_tx.shared::cta.b64 [%0], %1;\" :: \"r\"(bar), \"r\"(tn_" << js
           << ") : \"memory\");\n";
-        o << ind << "        sw_bulk(dst_" << js << " + static_cast<unsigned>(sw_slot(sn * " << K << " + " << r << " - lagL_" << js
-          << ", wlen_" << js << ") * " << PL * 8 << "), src_" << js << " + v * s0_" << js << ", tn_" << js << ", bar);\n";
+        if (d3)
+          o << ind << "        sw_tensor3(dst_" << js << " + static_cast<unsigned>(sw_slot(sn * " << K << " + " << r << " - lagL_"
+            << js << ", wlen_" << js << ") * " << PL * 8 << "), &m.t[dd_" << js << "][0], tx_" << js << ", ty_" << js
+            << ", static_cast<int>(v), bar);\n";
+        else
+          o << ind << "        sw_bulk(dst_" << js << " + static_cast<unsigned>(sw_slot(sn * " << K << " + " << r << " - lagL_" << js
+            << ", wlen_" << js << ") * " << PL * 8 << "), src_" << js << " + v * s0_" << js << ", tn_" << js << ", bar);\n";
         o << ind << "      }\n" << ind << "    }\n";
       }
     o << ind << "    __syncwarp();\n";
@@ -823,7 +839,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       const std::string js = std::to_string(j);
       o << "    const double* src_" << js << " = nullptr;\n    long long s0_" << js << " = 0, vr0_" << js << " = 0, nrows_" << js
         << " = 0;\n    unsigned dst_" << js << " = 0, tn_" << js << " = 0;\n    int lagL_" << js << " = 0, wlen_" << js << " = 1;\n";
-      o << "    {\n      const int idx = lane + " << 32 * j << ", li = idx / " << pl.RB << ", rb = idx % " << pl.RB << ";\n";
+      if (d3) o << "    int dd_" << js << " = 0, tx_" << js << " = 0, ty_" << js << " = 0;\n";
+      if (d3)  // one tensor copy per dataset
+        o << "    {\n      const int idx = lane + " << 32 * j << ", li = idx, rb = 0;\n";
+      else  // one row copy per dataset and tile row
+        o << "    {\n      const int idx = lane + " << 32 * j << ", li = idx / " << pl.RB << ", rb = idx % " << pl.RB << ";\n";
       o << "      int dd = -1;\n      long long roff = 0;\n";
       int i = 0;
       for (int d = 0; d < nd; ++d) {
@@ -833,7 +853,18 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
           << " = " << D.lagL << "; wlen_" << js << " = " << D.W << "; roff = " << pl.pad + D.off << "; }\n";
         ++i;
       }
-      o << "      if (dd >= 0) {\n";
+      o << "      if (dd >= 0 && " << (d3 ? "true" : "false") << ") {  // 3-D: the plane tile's tensor-copy origin\n";
+      o << "        const long long cs = c0 - " << pl.HC << " - p.box[dd][2];\n";
+      if (d3) {
+        o << "        dd_" << js << " = dd;\n";
+        o << "        tx_" << js << " = static_cast<int>(cs - (cs & 1));  // even (16-byte aligned) column at or below the tile\n";
+        o << "        ty_" << js << " = static_cast<int>(b0 - " << pl.HB << " - p.box[dd][4]);\n";
+        o << "        tn_" << js << " = " << PL * 8 << "u;  // the whole box, zero-filled out of bounds\n";
+        o << "        vr0_" << js << " = rbase - p.box[dd][0] - lagL_" << js << ";\n";
+        o << "        nrows_" << js << " = p.box[dd][1] - p.box[dd][0];\n";
+        o << "        dst_" << js << " = sw_saddr(sw_sm) + static_cast<unsigned>(roff * 8);\n";
+      }
+      o << "      } else if (dd >= 0) {\n";
       o << "        const long long cs = c0 - " << pl.HC << " - p.box[dd][2];\n";
       o << "        const long long a0 = cs > 0 ? (cs & ~1LL) : 0LL;\n";
       o << "        const long long a1 = (min(cs + " << pl.RC << "LL, p.box[dd][3] - p.box[dd][2]) + 1) & ~1LL;\n";
@@ -1485,7 +1516,9 @@ extern "C" int ooc_sweep_check(const ooc_loop* loops, int n, int* oop_args) {
   long long min_pts = 0;
   const int m = jit_policy(&min_pts);
   if (m == 0) return 0;
-  if (m == 1 && static_cast<long long>(loops[0].hi[0] - loops[0].lo[0]) * (loops[0].hi[1] - loops[0].lo[1]) < min_pts)
+  if (m == 1 && static_cast<long long>(loops[0].hi[0] - loops[0].lo[0]) * (loops[0].hi[1] - loops[0].lo[1]) *
+                        std::max<long long>(1, loops[0].hi[2] - loops[0].lo[2]) <
+                    min_pts)
     return 0;
   bool tma = false;
   const Key128 key = run_key(loops, n, nullptr, 0, false, &tma);
@@ -1775,7 +1808,29 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
     sp.part = c->red_part[q];
   }
   c->stats.sweep_launches++;
-  void* args[] = {&sp};
+  // 3-D: one tiled tensor map per loaded dataset view (box = the RB x RCp plane tile)
+  struct alignas(64) HostMaps {
+    unsigned long long t[SW_MAXD][16];
+  };
+  HostMaps maps;
+  std::memset(&maps, 0, sizeof maps);
+  if (pl.nd == 3) {
+    for (std::size_t d = 0; d < pl.D.size(); ++d) {
+      if (!pl.D[d].loaded) continue;
+      const ooc_view& v = loops[E.first[d].first].args[E.first[d].second];
+      const unsigned long long gdim[3] = {static_cast<unsigned long long>(v.hi[2] - v.lo[2]),
+                                          static_cast<unsigned long long>(v.hi[1] - v.lo[1]),
+                                          static_cast<unsigned long long>(v.hi[0] - v.lo[0])};
+      const unsigned long long gstr[2] = {static_cast<unsigned long long>(v.stride[1]) * 8,
+                                          static_cast<unsigned long long>(v.stride[0]) * 8};
+      const unsigned box[3] = {static_cast<unsigned>(pl.RCp), static_cast<unsigned>(pl.RB), 1u};
+      if (!jit_tensor_map(&maps.t[d][0], 3, v.data, gdim, gstr, box)) {
+        set_error("ooc_launch_sweep: cuTensorMapEncodeTiled rejected a 3-D view");
+        return OOC_ERR_UNSUPPORTED;
+      }
+    }
+  }
+  void* args[] = {&sp, &maps};
   std::pair<cudaEvent_t, cudaEvent_t>* tev = nullptr;
   if (timing) {
     tev = &T.ev[static_cast<std::size_t>(pick)];

@@ -63,7 +63,7 @@ def test_sweep_3d_apps_vs_oracle(app, nx, ny, nz, iters, span, jit_always):
         assert not diff, diff
         assert rt.device()["sweep_launches"] > 0
     finally:
-        B.set_sweep_3d(False)
+        B.set_sweep_3d(True)
 
 
 def test_sweep_random_programs_vs_golden(golden_random, jit_always):

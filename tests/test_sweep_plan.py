@@ -48,7 +48,7 @@ def test_3d_chains_sweep_as_plane_tiles(jit_always):
     compile for sm_100a; a whole miniflow3d timestep fits one run."""
     B.set_sweep_3d(False)
     rt, chains = _chains(P.app_program("miniflow3d", 24, 20, 18, iters=3))
-    assert all(rt.chain_sweep_check(c, compile=False) == [] for c in chains)  # off by default
+    assert all(rt.chain_sweep_check(c, compile=False) == [] for c in chains)  # the switch works
     B.set_sweep_3d(True)
     for app, kw in (("miniflow3d", dict(iters=3)), ("rk3chain3d", dict(iters=3, span=3))):
         rt, chains = _chains(P.app_program(app, 24, 20, 18, **kw))
@@ -57,7 +57,6 @@ def test_3d_chains_sweep_as_plane_tiles(jit_always):
         if app == "miniflow3d":
             assert any(g["loops"] >= 14 for g in runs)
             assert all(g["plan"]["tma"] == 1 for g in runs)
-    B.set_sweep_3d(False)
 
 
 def test_random_2d_chains_compile(jit_always):
