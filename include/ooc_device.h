@@ -53,6 +53,9 @@ const char* ooc_dev_build_info(void);
 /* ------------------------------------------------------------ host memory */
 int ooc_host_alloc(size_t bytes, void** out); /* page-locked, portable */
 int ooc_host_free(void* p);
+/* Preferred GPU for the page-locked allocations of the calling thread (-1: none): the
+ * pages are placed on the CPUs local to that GPU (its NUMA node). */
+int ooc_host_numa_device(int device);
 
 /* ------------------------------------------------------------ context */
 typedef struct ooc_ctx ooc_ctx;

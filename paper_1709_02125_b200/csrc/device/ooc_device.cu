@@ -1,9 +1,14 @@
 // Device layer: contexts, pinned host memory, HBM memory manager, queues/events,
 // strided box copies. Implements include/ooc_device.h (except loop launch /
 // reductions, in loop_kernels.cu).
+#include <sched.h>
+
+#include <cctype>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <mutex>
+#include <string>
 #include <unordered_set>
 
 #include "internal.cuh"
@@ -67,6 +72,43 @@ int ooc_dev_count(int* n) {
   return OOC_OK;
 }
 
+// NUMA placement of page-locked memory: with a preferred device set for the calling
+// thread, cudaHostAlloc runs with the thread bound to the CPUs local to that GPU
+// (/sys/bus/pci/devices/<bus id>/local_cpulist), so the pinned pages — each rank's slab,
+// streamed over its own link — live on the GPU's socket. A no-op on single-node hosts.
+static thread_local int g_numa_dev = -1;
+
+int ooc_host_numa_device(int device) {
+  g_numa_dev = device;
+  return OOC_OK;
+}
+
+static bool local_cpus(int device, cpu_set_t* set) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  std::string id(bus);
+  for (char& ch : id) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+  std::ifstream in("/sys/bus/pci/devices/" + id + "/local_cpulist");
+  std::string list;
+  if (!in || !std::getline(in, list) || list.empty()) return false;
+  CPU_ZERO(set);
+  std::size_t i = 0;
+  int n = 0;
+  while (i < list.size()) {
+    std::size_t j = list.find(',', i);
+    if (j == std::string::npos) j = list.size();
+    const std::string part = list.substr(i, j - i);
+    const std::size_t dash = part.find('-');
+    const int a = std::atoi(part.c_str()), b = dash == std::string::npos ? a : std::atoi(part.c_str() + dash + 1);
+    for (int c = a; c <= b && c < CPU_SETSIZE; ++c, ++n) CPU_SET(c, set);
+    i = j + 1;
+  }
+  return n > 0;
+}
+
 int ooc_host_alloc(size_t bytes, void** out) {
   static int has_dev = -1;
   if (has_dev < 0) {
@@ -78,7 +120,11 @@ int ooc_host_alloc(size_t bytes, void** out) {
     return OOC_ERR_NODEV;
   }
   void* p = nullptr;
+  cpu_set_t old_set, want;
+  const bool bind = g_numa_dev >= 0 && sched_getaffinity(0, sizeof old_set, &old_set) == 0 && local_cpus(g_numa_dev, &want) &&
+                    sched_setaffinity(0, sizeof want, &want) == 0;
   cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+  if (bind) sched_setaffinity(0, sizeof old_set, &old_set);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error(std::string("cudaHostAlloc: ") + cudaGetErrorString(e));

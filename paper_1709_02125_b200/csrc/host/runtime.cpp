@@ -6,10 +6,13 @@
 #include <sstream>
 
 #include "ooc/gpu_engine.hpp"
+#include "ooc_device.h"
 
 namespace ooc {
 
 Runtime::Runtime(RuntimeOptions opts) : opts_(opts) {
+  // this runtime's datasets (declared on this thread) are pinned next to its GPU
+  ooc_host_numa_device(opts_.gpu);
   if (opts_.executor == ExecutorKind::tiled_cache || opts_.executor == ExecutorKind::unified)
     throw ValidationError(std::string("executor '") + executor_name(opts_.executor) +
                           "' (a KNL cache / unified-memory cost model of the reference) is not "
