@@ -30,11 +30,12 @@ def test_reference_arm_prints_one_json_line():
 @pytest.mark.gpu
 def test_slab_bench_under_torchrun_single_rank():
     """The multi-GPU bench path (torchrun, NCCL, dim-0 slabs, ghost exchange after every
-    chain) on one GPU (OOC_BENCH_FORCE_DIST=1), small grid: one JSON line, dp1 slabs."""
+    chain, in core and out of core) on one GPU (OOC_BENCH_FORCE_DIST=1), small grid: one
+    JSON line, dp1 slabs."""
     env = dict(os.environ, OOC_BENCH_FORCE_DIST="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
            "--master-addr", "127.0.0.1", "--master-port", "29541", "bench.py", "--gpus", "1",
-           "--size", "2048", "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu"]
+           "--size", "2048", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-parity"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = r.stdout.splitlines()
@@ -42,6 +43,8 @@ def test_slab_bench_under_torchrun_single_rank():
     line = json.loads(lines[0])
     assert line["value"] > 0 and line["gpu_launches"] > 0
     assert line["config"]["parallelism"].startswith("dp1 dim-0 slabs")
+    # the out-of-core slab path (windowed tiled_explicit runtime on an NCCL communicator)
+    assert line["e2e"]["value"] > 0 and "dim-0 slabs" in line["e2e"]["mode"]
 
 
 @pytest.mark.gpu
