@@ -70,7 +70,7 @@ int ring_cols() {
   static int rc = [] {
     const char* e = std::getenv("OOC_SWEEP_RC");
     const int v = e ? std::atoi(e) : 256;  // measured: 256 > 128 (+3 %) > 64
-    return v == 64 || v == 128 || v == 256 ? v : 256;
+    return v == 64 || v == 128 || v == 256 || v == 512 ? v : 256;
   }();
   return rc;
 }
@@ -225,7 +225,7 @@ long long smem_budget() {
   static long long b = [] {
     const char* e = std::getenv("OOC_SWEEP_SMEM");
     // measured: occupancy beats fewer DRAM passes (56 KB per 128 ring columns)
-    return e ? std::atoll(e) : 56LL * 1024 * ring_cols() / 128;
+    return e ? std::atoll(e) : std::min<long long>(56LL * 1024 * ring_cols() / 128, 220LL * 1024);
   }();
   return b;
 }
