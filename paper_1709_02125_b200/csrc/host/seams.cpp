@@ -83,9 +83,14 @@ void apply_loop(const ParLoop& loop, const Extent& range, const std::vector<ArgV
   LoopCtx& c = loop_ctx(gpu);
   const LoweredLoop lw = lower_loop(loop);
   std::vector<ooc_view> v;
-  for (const ArgView& a : views) {
-    if (!a.box.contains(range.ndim == a.box.ndim ? a.box : a.box))
-      throw ValidationError("apply_loop: bad view");
+  for (std::size_t i = 0; i < views.size(); ++i) {
+    const ArgView& a = views[i];
+    // every point the loop touches through this argument must lie in its view
+    // (proj/src/kernel_exec.cpp:97-101 check_containment)
+    auto [slo, shi] = stencil_extents(loop.args[i].stencil);
+    if (!a.data || a.box.ndim != range.ndim || !a.box.contains(range.expand(slo, shi)))
+      throw ValidationError("apply_loop: argument " + std::to_string(i) + " view " + a.box.str() +
+                            " does not contain the range " + range.str() + " and its stencil");
     v.push_back(view_at(a.data, a.box, padded_layout(a.box, 1).stride));
   }
   const int slot = 0;

@@ -159,3 +159,27 @@ def test_executor_seam_runs_bitwise(tmp_path):
     usum = float(log.split("usum")[1].split()[0])
     ref = want.reshape(n + 2, n + 2)[1:-1, 1:-1].sum()
     assert abs(usum - ref) <= 1e-12 * abs(ref)
+
+
+# ---------------------------------------------------------------- the kernel seam
+def build_kernel_seam(tmp_path):
+    exe = str(tmp_path / "kernel_seam")
+    subprocess.run(["/usr/bin/g++", "-std=c++20", "-O2", "-ffp-contract=off",
+                    "-I", os.path.join(PKG, "csrc", "include"), "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "kernel_seam.cpp"), "-o", exe,
+                    "-L", os.path.join(PKG, "lib"), "-looc", "-Wl,-rpath," + os.path.join(PKG, "lib")],
+                   check=True)
+    return exe
+
+
+def test_kernel_seam_example_compiles(tmp_path):
+    """apply_loop with the reference's signature (proj/include/ooc/kernel_exec.hpp:29-30)."""
+    assert os.path.exists(build_kernel_seam(tmp_path))
+
+
+@pytest.mark.gpu
+def test_kernel_seam_runs_bitwise(tmp_path):
+    """apply_loop on the page-locked host buffers of a Mesh: one sm_100a launch; the
+    field equals a host evaluation bit for bit, the reduction within 1e-12."""
+    r = subprocess.run([build_kernel_seam(tmp_path), "200"], capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
