@@ -46,7 +46,7 @@ int main(int argc, char** argv) {
         std::printf("mismatch at (%lld,%lld): %.17g vs %.17g\n", static_cast<long long>(i), static_cast<long long>(j), got, want);
         return 1;
       }
-      want_sum += U(i, j) - U(i, j + 1);
+      want_sum += U(i, j) - U(i + 1, j);  // r(0, 1, 0): one row down (dim 0)
     }
   if (std::fabs(acc - want_sum) > 1e-12 * std::fabs(want_sum)) {
     std::printf("reduction %.17g vs %.17g\n", acc, want_sum);
