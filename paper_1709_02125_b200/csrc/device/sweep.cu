@@ -195,6 +195,7 @@ struct SwPlan {
   long long HB = 0, TB = 1;        // 3-D: dim-1 halo and owned tile rows
   long long pad = 32;              // doubles before/after the rings (edge neighbour reads)
   bool tma = false;  // loads: bulk async copies (one thread, mbarrier ring) instead of per-thread cp.async
+  bool bulk_st = false;  // 2-D TMA: interior rows stored by the producer with bulk copies (smem -> global)
   long long U = 8;   // ring period: every ring length divides it (0: none small enough, no unrolling)
   int NB = 8;        // load barriers (a multiple of U's steps: constant indices in unrolled steps)
   int RCp = 128;     // ring row pitch in doubles (RC, or RC + 2 with TMA: even-column row copies)
@@ -252,6 +253,11 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   pl.RB = pl.nd == 2 ? 1 : ring_rows3();
   pl.NT = pl.RB * pl.RC;
   pl.tma = tma;
+  // bulk-copy stores of the interior rows by the producer (OOC_SWEEP_BULKST=1): parity-
+  // tested, measured no faster on the timestep runs (2.70 ms either way) and slower on the
+  // chain's last run, which stores nine datasets (6.1 vs 5.1 ms): off by default
+  static const bool bulk_env = std::getenv("OOC_SWEEP_BULKST") && std::atoi(std::getenv("OOC_SWEEP_BULKST")) == 1;
+  pl.bulk_st = tma && pl.nd == 2 && bulk_env;
   pl.RCp = tma ? pl.RC + 2 : pl.RC;
   if (tma) pl.NT += 32;  // + one producer warp issuing the bulk-copy loads
   pl.L.resize(static_cast<std::size_t>(n));
@@ -425,6 +431,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
       B = std::max(B, (P + 1) * K - 1 - D.lagL);
     }
     if (D.written) A = std::max(A, D.lagS);
+    if (pl.bulk_st && D.store) A = std::max(A, D.lagS + K);  // read by the producer's bulk store one step later
     for (int k = 0; k < n; ++k) {
       const SwLoop& S = pl.L[static_cast<std::size_t>(k)];
       if (reads(k, d)) {
@@ -616,7 +623,8 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   for (int d = 0; d < nd; ++d) {
     const SwDs& D = pl.D[static_cast<std::size_t>(d)];
     o << "  double* " << (restrict_rings ? "__restrict__ " : "") << "const R" << d << " = B + " << D.off;
-    if (pl.tma && D.loaded) o << " + static_cast<int>((c0 - " << pl.HC << " - p.box[" << d << "][2]) & 1)";
+    if (pl.tma && (D.loaded || (pl.bulk_st && D.store)))
+      o << " + static_cast<int>((c0 - " << pl.HC << " - p.box[" << d << "][2]) & 1)";
     o << ";\n";
   }
   o << "  const long long r_own0 = p.R0 + static_cast<long long>(blockIdx.y) * p.seg_rows;\n";
@@ -665,6 +673,18 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   o << "  const bool own_col = lc >= " << pl.HC << " && lc < " << pl.HC + pl.TC << " && c < p.C1";
   if (d3) o << " && lb >= " << pl.HB << " && lb < " << pl.HB + pl.TB << " && b < p.B1";
   o << ";\n";
+  // bulk stores cover the owned columns from the first 16-byte aligned one to the last; the
+  // (at most two) edge columns outside are stored by their threads (stedge)
+  if (pl.bulk_st) {
+    o << "  unsigned stedge = 0u;\n";
+    for (int d = 0; d < nd; ++d) {
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (!D.store) continue;
+      const std::string ds = std::to_string(d);
+      o << "  if (own_col && (c < c0 + ((c0 - p.box[" << ds << "][2]) & 1) || c >= c0 + " << pl.TC << " - ((c0 + " << pl.TC
+        << " - p.box[" << ds << "][2]) & 1))) stedge |= 1u << " << d << ";\n";
+    }
+  }
   // interior strip: all 128 ring columns inside every loop range and load box, every
   // owned column inside the launch box — the fast steps then evaluate every loop on
   // every lane without predicates (lanes outside a loop's halo produce values nobody
@@ -887,9 +907,55 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     o << "    for (int t = 0; t < " << pl.P + std::max(l2_ahead, 0) << "; ++t)\n";
     tma_issue("t < " + std::to_string(pl.P) + " ? t : -1",
               l2_ahead > 0 ? "t >= " + std::to_string(pl.P) + " ? t : -1" : "-1", "      ");
-    o << "    for (int s = 0; s < nsteps; ++s) {\n      __syncthreads();\n";
+    // bulk stores (2-D): lane i copies the aligned owned columns of the i-th stored
+    // dataset's row(s) of the PREVIOUS fast step out of its ring slot (kept one step longer
+    // for this); the copy has read its rows before the producer joins the next barrier
+    int nstore = 0;
+    for (const SwDs& D : pl.D) nstore += D.store ? 1 : 0;
+    const bool bst = pl.bulk_st && nstore > 0;
+    auto bulk_store = [&](const std::string& step, const char* ind) {
+      o << ind << "if (sdd >= 0 && snb && strip_in && (" << step << ") >= s_lo && (" << step << ") < s_hi) {\n";
+      for (int r = 0; r < K; ++r) {
+        o << ind << "  {\n" << ind << "    const int v = (" << step << ") * " << K << " + " << r << ";\n";
+        o << ind << "    asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\" :: \"l\"(sg + static_cast<long long>(v) * ss0), "
+          << "\"r\"(ssrc + static_cast<unsigned>(sw_slot(v - slagS, swl) * " << pl.RCp * 8 << ")), \"r\"(snb) : \"memory\");\n";
+        o << ind << "  }\n";
+      }
+      o << ind << "  asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n" << ind << "}\n";
+    };
+    if (bst) {
+      o << "    int sdd = -1, slagS = 0, swl = 1;\n    long long sroff = 0;\n";
+      int i = 0;
+      for (int d = 0; d < nd; ++d) {
+        const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+        if (!D.store) continue;
+        o << "    " << (i ? "else if" : "if") << " (lane == " << i << ") { sdd = " << d << "; slagS = " << D.lagS << "; swl = " << D.W
+          << "; sroff = " << pl.pad + D.off << "; }\n";
+        ++i;
+      }
+      o << "    double* sg = nullptr;\n    long long ss0 = 0;\n    unsigned ssrc = 0, snb = 0;\n";
+      o << "    if (sdd >= 0) {\n";
+      o << "      const long long ce0 = c0 + ((c0 - p.box[sdd][2]) & 1), ce1 = c0 + " << pl.TC << " - ((c0 + " << pl.TC
+        << " - p.box[sdd][2]) & 1);\n";
+      o << "      sg = p.dst[sdd] + (rbase - slagS - p.box[sdd][0]) * p.s0[sdd] + (ce0 - p.box[sdd][2]);\n";
+      o << "      ss0 = p.s0[sdd];\n";
+      o << "      ssrc = sw_saddr(sw_sm) + static_cast<unsigned>((sroff + (ce0 - c0 + " << pl.HC << ") + ((c0 - " << pl.HC
+        << " - p.box[sdd][2]) & 1)) * 8);\n";
+      o << "      snb = ce1 > ce0 ? static_cast<unsigned>(ce1 - ce0) * 8u : 0u;\n";
+      o << "    }\n";
+    }
+    o << "    for (int s = 0; s < nsteps; ++s) {\n";
+    if (bst) o << "      asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n";
+    o << "      __syncthreads();\n";
     tma_issue("s + " + std::to_string(pl.P), l2_ahead > 0 ? "s + " + std::to_string(pl.P + l2_ahead) : "-1", "      ");
-    o << "    }\n    return;\n  }\n";
+    if (bst) bulk_store("s - 1", "      ");
+    o << "    }\n";
+    if (bst) {  // the consumers' last step: one more barrier, then its rows; drain before exit
+      o << "    __syncthreads();\n";
+      bulk_store("nsteps - 1", "    ");
+      o << "    asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
+    }
+    o << "    return;\n  }\n";
   } else
     for (int t = 0; t < pl.P; ++t) loads(std::to_string(t), "  ", false, false);
   int ci0 = 0;
@@ -1054,7 +1120,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       const SwDs& D = pl.D[static_cast<std::size_t>(d)];
       if (!D.store) continue;
       const std::string ds = std::to_string(d);
-      o << ind << "if (own_col) {\n";
+      if (!pl.bulk_st) o << ind << "if (own_col) {\n";
       for (int r = 0; r < K; ++r) {
         auto it = forward && last_writer[static_cast<std::size_t>(d)] >= 0 &&
                           pl.L[static_cast<std::size_t>(last_writer[static_cast<std::size_t>(d)])].lag == D.lagS
@@ -1062,10 +1128,21 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
                       : cache.end();
         if (it == cache.end() && info) info->miss[static_cast<std::size_t>(d)] = 1;
         const std::string v = it != cache.end() ? it->second : at(d, "u", r - D.lagS, 0);
-        o << ind << "  gs" << ds << "[" << r << " * p.s0[" << ds << "]] = " << v << ";\n";
+        if (pl.bulk_st) {
+          // the final row goes to its ring slot (if only in a register); the producer copies
+          // the aligned owned columns out after the next step barrier
+          if (it != cache.end()) o << ind << at(d, "u", r - D.lagS, 0) << " = " << v << ";\n";
+          o << ind << "if (stedge & (1u << " << d << ")) gs" << ds << "[" << r << " * p.s0[" << ds << "]] = " << v << ";\n";
+        } else {
+          o << ind << "  gs" << ds << "[" << r << " * p.s0[" << ds << "]] = " << v << ";\n";
+        }
       }
-      o << ind << "}\n";
+      if (!pl.bulk_st) o << ind << "}\n";
     }
+    bool any_store = false;
+    for (const SwDs& D : pl.D) any_store = any_store || D.store;
+    if (pl.bulk_st && any_store)  // generic-proxy ring writes before the producer's async-proxy reads
+      o << ind << "asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
     if (info) info->end = cache;
     for (const auto& [k, name] : carries) {  // parallel assignment: sources may be carries
       auto it = cache.find(std::make_tuple(std::get<0>(k), std::get<1>(k) + K, 0LL));
@@ -1263,6 +1340,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   o << "      prev_fast = false;\n    }\n";
   advance("    ");
   o << "    ++s;\n  }\n";
+  {
+    bool any_store = false;
+    for (const SwDs& D : pl.D) any_store = any_store || D.store;
+    if (pl.bulk_st && any_store) o << "  __syncthreads();  // the producer copies out the last step's rows\n";
+  }
   if (!pl.tma) o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
   if (pl.red_op != OOC_RED_NONE) {  // warp tree, then the CTA's warps in order: one partial per CTA
     o << "#pragma unroll\n  for (int w = 16; w > 0; w >>= 1) racc = ooc_red(" << pl.red_op
