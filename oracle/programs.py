@@ -390,14 +390,16 @@ def _rand_expr(rng, reads, depth, ops):  # support.hpp:45-64 (+ divide)
 
 
 def random_program(seed, max_loops=8, max_datasets=4, max_extent=2, min_size=8, max_size=24,
-                   reductions=True, allow_3d=True, divide=True, flushes=False):
+                   reductions=True, allow_3d=True, divide=True, flushes=False, max_3d=10, force_ndim=0):
     """A random validated-by-construction chain, support.hpp:66-138's distribution."""
     rng = random.Random(seed)
     roll = rng.randint(1, 6 if allow_3d else 4)
     ndim = 1 if roll <= 2 else 2 if roll <= 5 else 3
+    if force_ndim:  # (consumes the same random draw, so other seeds' programs are unchanged)
+        ndim = force_ndim
     dims = [1, 1, 1]
     for d in range(ndim):
-        dims[d] = min(rng.randint(min_size, max_size), 10) if ndim == 3 else rng.randint(min_size, max_size)
+        dims[d] = min(rng.randint(min_size, max_size), max_3d) if ndim == 3 else rng.randint(min_size, max_size)
     p = Prog()
     nds = rng.randint(1, max_datasets)
     names = [f"d{i}" for i in range(nds)]

@@ -66,6 +66,19 @@ def test_sweep_3d_apps_vs_oracle(app, nx, ny, nz, iters, span, jit_always):
         B.set_sweep_3d(True)
 
 
+def test_sweep_random_3d_chains_vs_oracle(jit_always):
+    """Random 3-D chains (mixed stencils along all three dimensions, read-write loops,
+    reductions) on meshes larger than a plane tile: several tiles per plane, interior
+    (fast, unrolled) and edge (predicated) tiles, against the oracle bit for bit."""
+    swept = 0
+    for seed in range(24):
+        prog = P.random_program(1000 + seed, force_ndim=3, min_size=20, max_size=44, max_3d=44, flushes=True)
+        diff, rt = _resident_vs_oracle(prog)
+        assert not diff, (seed, diff)
+        swept += rt.device()["sweep_launches"]
+    assert swept > 0
+
+
 def test_sweep_random_programs_vs_golden(golden_random, jit_always):
     """Random 2-D chains (mixed stencils, ranges, read-write loops, flushes, reductions)
     through the resident executor: the reference's golden buffers and reductions."""
