@@ -93,6 +93,20 @@ def test_slab_ranks_on_one_gpu_match_single_domain(app, executor, world, tmp_pat
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("executor", ["resident", "explicit"])
+def test_four_ranks_interior_slabs(executor, tmp_path):
+    """Four ranks: two interior slabs exchange with both neighbours every chain."""
+    parts = _run_ranks(4, executor, "miniflow2d", tmp_path)
+    full, red = _single_domain(executor, "miniflow2d")
+    for rank, part in enumerate(parts):
+        assert part["comm_bytes"][0] > 0
+        for d, (a0, want) in enumerate(full):
+            lo, hi = part[f"rows{d}"]
+            assert np.array_equal(part[f"data{d}"].view(np.uint64), want[lo - a0:hi - a0].view(np.uint64)), (rank, d)
+        assert abs(part["fieldsum"][0] - red) <= 1e-12 * abs(red)
+
+
+@pytest.mark.gpu
 def test_slab_out_of_core_cyclic_ranks(tmp_path):
     """Out-of-core slabs with cyclic temporaries: the fields the ranks keep on the host
     (non-stale) equal the single-domain run; stale temporaries are never exchanged."""
