@@ -415,7 +415,7 @@ def parity_vs_reference(B, n, gpu):
     (oracle/_ref, OpenMP on every host core, reference executor — proj/tools/ooc_cli.cpp:186-207
     --verify compares the same way) against this engine resident on the GPU: every field
     bitwise, the fieldsum within 1e-12 relative (the reference folds sequentially,
-    proj/src/kernel_exec.cpp:193-197)."""
+    proj/src/kernel_exec.cpp:193-197), and bitwise in exact-reduction mode."""
     from oracle import refo
     if not refo.available():
         return {"ok": None, "skipped": "oracle/_ref/libooc_ref.so not built"}
@@ -439,6 +439,17 @@ def parity_vs_reference(B, n, gpu):
     out["fieldsum_reference"] = b
     out["fieldsum_rel_err"] = abs(a - b) / max(abs(b), 1e-300)
     out["ok"] = out["fields_bitwise"] and out["fieldsum_rel_err"] <= 1e-12
+    rt.close()
+    # the same chain in exact-reduction mode (ooc_rt_set_exact_reductions): the fieldsum
+    # folded in the reference's row-major order by one GPU thread must match it bit for bit
+    t0 = time.perf_counter()
+    rt = B.Runtime("resident", gpu=gpu, exact_reductions=True)
+    rt.declare_app("miniflow2d", n, n)
+    rt.app_iterations("miniflow2d", n, n, 0, 0, ITERS_PER_STEP)
+    ex = rt.fetch_reduction("fieldsum")
+    out["fieldsum_exact_mode"] = "bitwise" if ex.hex() == b.hex() else f"differs ({ex!r})"
+    out["exact_mode_wall_s"] = time.perf_counter() - t0
+    out["ok"] = out["ok"] and ex.hex() == b.hex()
     rt.close()
     ref.close()
     return out

@@ -234,6 +234,12 @@ int ooc_jit_status(char* buf, int len);
 int ooc_reduce_reset(ooc_ctx* ctx, int queue, int slot, int op);
 /* Asynchronous device->host read of a slot into page-locked `dst` on `queue`. */
 int ooc_reduce_fetch(ooc_ctx* ctx, int queue, int slot, double* dst);
+/* Exact mode (debug; default 0): a reducing launch writes one contribution per point
+ * (row-major over its box) and one thread folds them into the slot in that order —
+ * the reference's sequential fold (proj/src/kernel_exec.cpp:156-159, 193-197), bitwise.
+ * Reducing groups then run loop by loop through the interpreter; ooc_launch_sweep
+ * refuses reducing runs. The contribution buffer grows outside graph captures only. */
+int ooc_set_reduce_exact(ooc_ctx* ctx, int on);
 
 /* ------------------------------------------------------------ multi-GPU (NCCL) */
 /* Slab decomposition plumbing (new; the reference is single-device).

@@ -177,6 +177,11 @@ const char* ooc_rt_chain_sweep_check(ooc_runtime* rt, int chain, int compile);
 void ooc_rt_set_row_recompute(int on);
 /* Process-wide: row-sweep kernels for resident untiled 2-D chains (default on; OOC_SWEEP=0). */
 void ooc_rt_set_sweep(int on);
+/* Exact reductions for the chains executed from now on (debug; default off): every
+ * reduction is folded by one thread in the reference's sequential row-major order
+ * (proj/src/kernel_exec.cpp:193-197), so fetch_reduction is bitwise equal to the
+ * reference's instead of within 1e-12. Reducing loops launch alone, graphs are off. */
+int ooc_rt_set_exact_reductions(ooc_runtime* rt, int on);
 /* dependency_oracle over recorded chain `chain` planned with `tiles`. */
 const char* ooc_rt_chain_oracle_json(ooc_runtime* rt, int chain, int tiles);
 

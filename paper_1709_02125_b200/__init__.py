@@ -100,7 +100,7 @@ class Runtime:
 
     def __init__(self, executor="resident", tiles=0, capacity=16_000_000_000, resident_budget=0,
                  prefetch=False, record=False, gpu=0, profile=False, arena_fill=0, tiled_dim=0,
-                 fuse=True, dist=(0, 1), own=None, ghost=0, timeline=False):
+                 fuse=True, dist=(0, 1), own=None, ghost=0, timeline=False, exact_reductions=False):
         L = _native.lib()
         o = _native.Options()
         L.ooc_rt_default_options(ctypes.byref(o))
@@ -124,6 +124,8 @@ class Runtime:
         _check(L.ooc_rt_create(ctypes.byref(o), ctypes.byref(h)))
         self._h = h
         self.executor = executor
+        if exact_reductions:
+            self.set_exact_reductions(True)
         self._shapes: Dict[int, Tuple[int, int, int]] = {}
 
     def close(self):
@@ -225,6 +227,12 @@ class Runtime:
 
     def set_cyclic_flag(self, on=True):
         _check(_native.lib().ooc_rt_set_cyclic(self._h, int(bool(on))))
+
+    def set_exact_reductions(self, on=True):
+        """Debug mode: reductions folded in the reference's sequential row-major order
+        (proj/src/kernel_exec.cpp:193-197), bitwise equal to it; slower (one thread per
+        fold), single rank only."""
+        _check(_native.lib().ooc_rt_set_exact_reductions(self._h, int(bool(on))))
 
     def fetch_dataset(self, d) -> np.ndarray:
         """Runtime::fetch_dataset (proj/src/runtime.cpp:13-19): flush, stale check, copy."""

@@ -67,6 +67,7 @@ def lib():
         "ooc_rt_finish": (i, [vp]),
         "ooc_rt_sync": (i, [vp]),
         "ooc_rt_set_cyclic": (i, [vp, i]),
+        "ooc_rt_set_exact_reductions": (i, [vp, i]),
         "ooc_rt_fetch_dataset": (i, [vp, i, dp, i64]),
         "ooc_rt_fetch_reduction": (i, [vp, cp, dp]),
         "ooc_rt_num_datasets": (i, [vp]),

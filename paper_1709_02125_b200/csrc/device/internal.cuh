@@ -49,6 +49,11 @@ struct ooc_ctx {
   double* red_acc = nullptr;   // OOC_REDUCE_SLOTS
   double* red_part[OOC_NUM_QUEUES] = {nullptr, nullptr, nullptr};
   int red_part_cap = 0;
+  // exact-reduction mode (ooc_set_reduce_exact): per-point contributions of a reducing
+  // launch, folded by one thread in row-major order (the reference's sequential fold)
+  int red_exact = 0;
+  double* red_scratch[OOC_NUM_QUEUES] = {nullptr, nullptr, nullptr};
+  long long red_scratch_elems[OOC_NUM_QUEUES] = {0, 0, 0};
   ooc_dev_stats stats{};
   // multi-GPU (comm.cu): NCCL communicator of the slab decomposition, or the CUDA-IPC
   // transport (shared-memory rendezvous + peer-mapped outboxes)

@@ -87,7 +87,8 @@ struct KParams {
   long long nA, nB, nC;  // canonical extents of the launch box; c is contiguous
   int ncode;
   int red_op;
-  double* part;  // reduction block partials
+  double* part;     // reduction block partials
+  double* scratch;  // exact mode: one contribution per point of the launch box
   KIns code[CAP];
 };
 
@@ -276,13 +277,23 @@ __global__ void __launch_bounds__(kBlock) k_interp(const __grid_constant__ KPara
         }
       }
       if constexpr (RED) {
+        if (p.scratch) {
+          // exact mode: the contribution of every point of the launch box in row-major
+          // order, the identity where the point is outside the loop's range
+          double* dst = p.scratch + row * p.nC + cx;
 #pragma unroll
-        for (int k = 0; k < P; ++k)
-          if (act[k]) acc = red_combine(p.red_op, acc, rv[k]);
+          for (int k = 0; k < P; ++k)
+            if (ok[k]) dst[k * kBlock] = act[k] ? rv[k] : red_identity(p.red_op);
+        } else {
+#pragma unroll
+          for (int k = 0; k < P; ++k)
+            if (act[k]) acc = red_combine(p.red_op, acc, rv[k]);
+        }
       }
     }
   }
   if constexpr (RED) {
+    if (p.scratch) return;
     // warp shuffle, then across the block's 4 warps, in a fixed order
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc = red_combine(p.red_op, acc, __shfl_down_sync(~0u, acc, o));
@@ -311,6 +322,52 @@ __global__ void __launch_bounds__(1024) k_fold(const double* part, int n, double
     __syncthreads();
   }
   if (threadIdx.x == 0) *acc = red_combine(op, *acc, sm[0]);
+}
+
+// Exact mode: acc = fold of the per-point contributions in row-major order by one
+// thread — the reference's sequential fold (kernel_exec.cpp:193-197), identity entries
+// being exact no-ops. The dependent add chain is the bound: warps 1.. stage the next
+// tile of contributions into shared memory (coalesced) while thread 0 folds the current
+// one from shared memory, so the folding thread never waits on HBM latency.
+constexpr int kSeqTile = 2048;
+__global__ void __launch_bounds__(256) k_fold_seq(const double* __restrict__ v, long long n,
+                                                  double* acc, int op) {
+  __shared__ __align__(16) double buf[2][kSeqTile];
+  const long long tiles = (n + kSeqTile - 1) / kSeqTile;
+  auto stage = [&](long long t) {
+    const long long base = t * kSeqTile;
+    const int len = static_cast<int>(n - base < kSeqTile ? n - base : kSeqTile);
+    double* dst = buf[t & 1];
+    for (int i = threadIdx.x - 32; i < len; i += blockDim.x - 32) dst[i] = __ldg(v + base + i);
+  };
+  double a = 0.0;
+  if (threadIdx.x == 0) a = *acc;
+  if (threadIdx.x >= 32 && tiles > 0) stage(0);
+  __syncthreads();
+  for (long long t = 0; t < tiles; ++t) {
+    if (threadIdx.x >= 32) {
+      if (t + 1 < tiles) stage(t + 1);
+    } else if (threadIdx.x == 0) {
+      const long long base = t * kSeqTile;
+      const int len = static_cast<int>(n - base < kSeqTile ? n - base : kSeqTile);
+      const double* src = buf[t & 1];
+      int i = 0;
+      for (; i + 16 <= len; i += 16) {
+        double x[16];
+#pragma unroll
+        for (int k = 0; k < 16; k += 2) {
+          const double2 p = *reinterpret_cast<const double2*>(src + i + k);
+          x[k] = p.x;
+          x[k + 1] = p.y;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) a = red_combine(op, a, x[k]);
+      }
+      for (; i < len; ++i) a = red_combine(op, a, src[i]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *acc = a;
 }
 
 __global__ void k_set(double* dst, double v) { *dst = v; }
@@ -530,6 +587,30 @@ int launch_variant(ooc_ctx* c, int q, const KParams<CAP>& kp, bool red) {
     grid.y = static_cast<unsigned>(std::min<long long>(rows, 65535));
   }
   cudaStream_t st = c->q[q];
+  if (red && c->red_exact) {
+    const long long pts = rows * kp.nC;
+    if (pts > c->red_scratch_elems[q]) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      OOC_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+      if (cs != cudaStreamCaptureStatusNone) {
+        set_error("exact reductions: the contribution buffer cannot grow inside a graph capture");
+        return OOC_ERR_ARG;
+      }
+      OOC_CUDA_TRY(cudaStreamSynchronize(st));
+      OOC_CUDA_TRY(cudaFree(c->red_scratch[q]));
+      c->red_scratch[q] = nullptr;
+      c->red_scratch_elems[q] = 0;
+      OOC_CUDA_TRY(cudaMalloc(&c->red_scratch[q], pts * sizeof(double)));
+      c->red_scratch_elems[q] = pts;
+    }
+    grid.x = static_cast<unsigned>(std::min<long long>(xblocks, 1 << 20));
+    grid.y = static_cast<unsigned>(std::min<long long>(rows, 65535));
+    KParams<CAP> kr = kp;
+    kr.scratch = c->red_scratch[q];
+    k_interp<CAP, P, S, W, R, true><<<grid, kBlock, 0, st>>>(kr);
+    OOC_CUDA_TRY(cudaGetLastError());
+    return 0;  // no block partials: the caller folds the contributions
+  }
   if (red) {
     KParams<CAP> kr = kp;
     kr.part = c->red_part[q];
@@ -573,9 +654,14 @@ int launch_cap(ooc_ctx* c, int q, const ooc_loop* Ls, int n) {
   else
     blocks = launch_variant<CAP, 1, 32, OOC_MAX_WRITES, kMaxReads>(c, q, *kp, red);
   const int red_op = kp->red_op;
+  const long long pts = kp->nA * kp->nB * kp->nC;
   delete kp;
   if (blocks < 0) return blocks;
-  if (red) {
+  if (red && c->red_exact) {
+    k_fold_seq<<<1, 256, 0, c->q[q]>>>(c->red_scratch[q], pts, c->red_acc + Ls[0].reduce_slot, red_op);
+    OOC_CUDA_TRY(cudaGetLastError());
+    ++c->stats.kernel_launches;
+  } else if (red) {
     k_fold<<<1, 1024, 0, c->q[q]>>>(c->red_part[q], blocks, c->red_acc + Ls[0].reduce_slot, red_op);
     OOC_CUDA_TRY(cudaGetLastError());
     ++c->stats.kernel_launches;
@@ -619,6 +705,18 @@ int ooc_launch_group(ooc_ctx* c, int q, const ooc_loop* loops, int n) {
     total += 1 + 2 * loops[i].ntape + 2 * loops[i].nwrites + 1;
   }
   if (live.empty()) return OOC_OK;
+  if (c->red_exact && live.back().reduce_op != OOC_RED_NONE) {
+    // exact reductions: the loops run one by one (the sequential semantics every fused
+    // launch reproduces) and the reducing one through the interpreter's contribution path
+    if (live.size() > 1) {
+      for (const ooc_loop& L : live) {
+        int rc = ooc_launch_group(c, q, &L, 1);
+        if (rc) return rc;
+      }
+      return OOC_OK;
+    }
+    return launch_cap<1000>(c, q, live.data(), 1);
+  }
   int blocks = 0;
   int jr = oocdev::jit_launch_group(c, q, live.data(), static_cast<int>(live.size()), &blocks);
   if (jr < 0) return jr;
@@ -659,6 +757,12 @@ int ooc_launch_group(ooc_ctx* c, int q, const ooc_loop* loops, int n) {
 int ooc_launch_loop(ooc_ctx* c, int q, const ooc_loop* L) {
   OOC_ARG_CHECK(c && L, "ooc_launch_loop: bad args");
   return ooc_launch_group(c, q, L, 1);
+}
+
+int ooc_set_reduce_exact(ooc_ctx* c, int on) {
+  OOC_ARG_CHECK(c, "ooc_set_reduce_exact: null ctx");
+  c->red_exact = on ? 1 : 0;
+  return OOC_OK;
 }
 
 int ooc_fill_box(ooc_ctx* c, int q, const ooc_view* v, double value) {

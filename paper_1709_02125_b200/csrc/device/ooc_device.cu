@@ -179,6 +179,7 @@ int ooc_ctx_destroy(ooc_ctx* c) {
   cudaFree(c->red_acc);
   for (int q = 0; q < OOC_NUM_QUEUES; ++q) {
     cudaFree(c->red_part[q]);
+    cudaFree(c->red_scratch[q]);
     cudaStreamDestroy(c->q[q]);
   }
   delete c;

@@ -1747,6 +1747,10 @@ extern "C" int ooc_sweep_report(char* buf, int len) {
 extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n, const ooc_redirect* red,
                                 int nred) {
   OOC_ARG_CHECK(c && loops && n > 0 && q >= 0 && q < OOC_NUM_QUEUES, "ooc_launch_sweep: bad args");
+  if (c->red_exact && loops[n - 1].reduce_op != OOC_RED_NONE) {
+    set_error("ooc_launch_sweep: exact reductions fold through ooc_launch_group, not in a sweep");
+    return OOC_ERR_UNSUPPORTED;
+  }
   const auto host0 = std::chrono::steady_clock::now();
   bool tma = false;
   const Key128 key = run_key(loops, n, red, nred, true, &tma);

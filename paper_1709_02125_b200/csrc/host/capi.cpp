@@ -336,6 +336,10 @@ const char* ooc_rt_audit_json(ooc_runtime* h) {
 void ooc_rt_set_row_recompute(int on) { ooc::set_row_recompute(on != 0); }
 void ooc_rt_set_sweep(int on) { ooc::set_sweep(on != 0); }
 
+int ooc_rt_set_exact_reductions(ooc_runtime* h, int on) {
+  return guard([&] { h->rt->set_exact_reductions(on != 0); });
+}
+
 const char* ooc_rt_report_csv(ooc_runtime* h, const char* app, const char* size, int iters) {
   std::string s;
   int rc = guard([&] { s = h->rt->report_csv(app ? app : "", size ? size : "", iters); });
@@ -517,7 +521,7 @@ const char* ooc_rt_chain_sweep_check(ooc_runtime* h, int chain, int compile) {
     }
     ooc::JsonWriter w;
     w.begin_array();
-    for (const ooc::SweepRun& run : ooc::plan_sweeps(m, c.loops, calls)) {
+    for (const ooc::SweepRun& run : ooc::plan_sweeps(m, c.loops, false, calls)) {
       const std::size_t a = run.a, b = run.b;
       std::vector<ooc_redirect> dead;
       for (ooc::DatasetId d : run.dead) dead.push_back({views[static_cast<std::size_t>(d)].data, nullptr});

@@ -101,10 +101,16 @@ ooc_view host_view(Dataset& ds) {
 GpuEngine::GpuEngine(const RuntimeOptions& opts) : opts_(opts) {
   DEV(ooc_ctx_create(opts.gpu, &ctx_));
   DEV(ooc_ctx_props(ctx_, &props_));
+  DEV(ooc_set_reduce_exact(ctx_, opts.exact_reductions ? 1 : 0));
   void* p = nullptr;
   DEV(ooc_host_alloc(sizeof(double) * OOC_REDUCE_SLOTS, &p));
   red_host_ = static_cast<double*>(p);
   std::memset(red_host_, 0, sizeof(double) * OOC_REDUCE_SLOTS);
+}
+
+void GpuEngine::set_exact_reductions(bool on) {
+  opts_.exact_reductions = on;
+  DEV(ooc_set_reduce_exact(ctx_, on ? 1 : 0));
 }
 
 GpuEngine::~GpuEngine() {
@@ -440,7 +446,7 @@ bool dead_after(const std::vector<ParLoop>& loops, std::size_t a, std::size_t b,
 }
 }  // namespace
 
-std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& loops,
+std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& loops, bool exact_reductions,
                                   const std::vector<ooc_loop>& calls) {
   // Least-traffic partition (dynamic programming) of the chain into sweep runs and
   // single loops left to the other kernels. A run costs one read of every dataset it
@@ -453,6 +459,7 @@ std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& 
   std::vector<int> flags;
   for (std::size_t i = 0; i < L; ++i)
     for (std::size_t j = i + 2; j <= L; ++j) {
+      if (exact_reductions && loops[j - 1].has_reduction()) break;  // folded on its own
       flags.assign((j - i) * OOC_MAX_ARGS, 0);
       if (ooc_sweep_check(&calls[i], static_cast<int>(j - i), flags.data()) != 1) {
         if (j > i + 2 || ooc_sweep_check(&calls[i], 1, nullptr) != 1) break;
@@ -1114,7 +1121,8 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
     const char* e = std::getenv("OOC_GRAPHS");
     return !(e && std::atoi(e) == 0);
   }();
-  const bool graphs_ok = graphs_on && !(halos && comm_ready_) && !opts_.profile_loops && !opts_.timeline;
+  const bool graphs_ok = graphs_on && !(halos && comm_ready_) && !opts_.profile_loops && !opts_.timeline &&
+                        !opts_.exact_reductions;  // the contribution buffer grows outside captures
   GraphEntry* ge = nullptr;
   int par = 0, sseen = 0;
   if (graphs_ok) {
@@ -1224,13 +1232,14 @@ void GpuEngine::run_resident(Mesh& mesh, const LoopChain& chain, const TilePlan*
     long long jmin = 0;
     ooc_jit_policy(&jm, &jmin);
     const std::string key = sweep_key(mesh, chain) + "|" + std::to_string(jm) + "|" + std::to_string(jmin) + "|" +
-                            std::to_string(ooc_sweep_3d_enabled());
+                            std::to_string(ooc_sweep_3d_enabled()) + "|" +
+                            std::to_string(opts_.exact_reductions ? 1 : 0);
     auto it = sweep_cache.find(key);
     if (it == sweep_cache.end()) {
       std::vector<ooc_loop> calls;
       for (std::size_t j = 0; j < chain.loops.size(); ++j)
         calls.push_back(make_call(lowered_store[j], chain.loops[j].range, views_of(chain.loops[j]), 0));
-      it = sweep_cache.emplace(key, plan_sweeps(mesh, chain.loops, calls)).first;
+      it = sweep_cache.emplace(key, plan_sweeps(mesh, chain.loops, opts_.exact_reductions, calls)).first;
     }
     sweeps = &it->second;
   } else {

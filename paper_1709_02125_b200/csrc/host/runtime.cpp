@@ -29,6 +29,11 @@ GpuEngine& Runtime::engine() {
   return *device_.engine;
 }
 
+void Runtime::set_exact_reductions(bool on) {
+  opts_.exact_reductions = on;  // applies to every chain executed from now on
+  if (device_.engine) device_.engine->set_exact_reductions(on);
+}
+
 DeviceState& Runtime::device_state() {
   engine();
   return device_;
@@ -201,6 +206,8 @@ void Runtime::execute(LoopChain&& chain) {  // runtime.cpp:64-148
   // dependency depth) and, with neighbours, refreshed and combined after it — never run
   // a multi-rank slab silently without its exchange
   const bool slabbed = windowed() && opts_.dist_world > 1;
+  if (slabbed && opts_.exact_reductions)
+    throw ValidationError("exact reductions fold on one rank; the slab decomposition all-reduces per-rank folds");
   if (slabbed && !g.comm_ready())
     throw ValidationError("slab decomposition over " + std::to_string(opts_.dist_world) +
                           " ranks needs a communicator (comm_init / comm_init_ipc) before its first chain");

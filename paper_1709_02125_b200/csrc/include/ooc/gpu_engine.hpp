@@ -60,7 +60,7 @@ struct SweepRun {
 };
 /// Row-sweep partition of an untiled chain: the least-traffic split into sweep runs
 /// (>= 2 loops each, accepted by ooc_sweep_check) and loops left to the other kernels.
-std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& loops,
+std::vector<SweepRun> plan_sweeps(const Mesh& mesh, const std::vector<ParLoop>& loops, bool exact_reductions,
                                   const std::vector<ooc_loop>& calls);
 std::string sweep_key(const Mesh& mesh, const LoopChain& chain);
 bool sweep_enabled();  // OOC_SWEEP=0 disables
@@ -119,6 +119,10 @@ class GpuEngine {
   ooc_ctx* ctx() { return ctx_; }
   /// ExecOptions::prefetch per call (run_chain_explicit seam).
   void set_prefetch(bool on) { opts_.prefetch = on; }
+  /// Exact reductions: reducing loops run alone through the contribution path and one
+  /// thread folds them in row-major order; sweeps stop before them, graphs are off.
+  void set_exact_reductions(bool on);
+  bool exact_reductions() const { return opts_.exact_reductions; }
   int slot_cursor() const { return slot_cursor_; }
   /// Datasets whose next-chain first tile is staged in HBM, with the staged region.
   std::map<DatasetId, Extent> staged_regions() const {

@@ -70,6 +70,8 @@ struct RuntimeOptions {
   int arena_fill = 0;               // debug: 0 none, 1 zero (reference behaviour), 2 NaN poison
   bool fuse = true;                 // run point-wise-dependent consecutive loops in one launch
   bool timeline = false;            // record a real event timeline of every command
+  bool exact_reductions = false;    // debug: fold reductions in the reference's sequential
+                                    // row-major order (bitwise equal; one thread per fold)
   // ---- slab decomposition (multi-GPU, one runtime per GPU): this rank owns rows
   // [own_lo, own_hi) of dimension 0 and recomputes `ghost` rows on each side. Any
   // program runs unchanged: declared datasets and loop ranges are clipped to the
@@ -158,6 +160,8 @@ class Runtime {
   double fetch_reduction(const std::string& name);
 
   void set_cyclic_flag(bool on) { cyclic_ = on; }
+  /// Exact reductions (RuntimeOptions::exact_reductions) for the chains flushed from now on.
+  void set_exact_reductions(bool on);
   bool cyclic_flag() const { return cyclic_; }
 
   void flush(FlushReason reason = FlushReason::explicit_flush);

@@ -49,6 +49,31 @@ def test_apps_vs_reference_golden(golden_apps):
     assert not bad, bad
 
 
+def test_exact_reductions_vs_reference_golden(golden_random, golden_apps):
+    """Exact mode (ooc_rt_set_exact_reductions): every reduction bit-equal to the
+    reference's sequential fold, resident and streamed, across tile counts."""
+    bad = []
+    cases = [(P.random_program(c["seed"], **c["kwargs"]), c["runs"]) for c in golden_random]
+    for c in golden_apps:
+        name, kw = c["case"]
+        kw = dict(kw)
+        cases.append((P.app_program(name, kw.pop("nx"), kw.pop("ny"), kw.pop("nz", 0), **kw), c["runs"]))
+    nred = 0
+    for prog, runs in cases:
+        for want in runs:
+            got = product_record(prog, EXEC_OF[want["executor"]], want["tiles"], want["capacity"],
+                                 want["cyclic"], prefetch=want.get("prefetch", False),
+                                 exact_reductions=True)
+            got.pop("_rt", None)
+            nred += len(want.get("reductions", {}))
+            diff = compare(want, got, exact_reductions=True, check_audit=want["executor"] == "explicit",
+                           check_totals=want["executor"] == "explicit")
+            if diff:
+                bad.append((want["executor"], want["tiles"], want["cyclic"], diff))
+    assert not bad, bad[:5]
+    assert nred > 50
+
+
 @pytest.mark.parametrize("fill", [1, 2])
 def test_arena_initialisation_is_unobservable(fill):
     """Zero (reference) or NaN-poisoned arenas give identical results: no kernel

@@ -26,7 +26,7 @@ def reference():
     ref.close()
 
 
-def _check(rt, ref, allow_stale=False):
+def _check(rt, ref, allow_stale=False, exact=False):
     names = ref.datasets()
     checked = 0
     for d in range(rt.num_datasets):
@@ -37,6 +37,8 @@ def _check(rt, ref, allow_stale=False):
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), names[d]
         checked += 1
     a, b = rt.fetch_reduction("fieldsum"), ref.fetch_reduction("fieldsum")
+    if exact:
+        assert a.hex() == b.hex(), (a, b)
     assert abs(a - b) <= 1e-12 * abs(b), (a, b)
     return checked
 
@@ -58,4 +60,31 @@ def test_out_of_core_2048_vs_reference(reference):
     rt.run_app("miniflow2d", N, N, 0, ITERS, cyclic=True)
     rt.finish()
     assert _check(rt, reference, allow_stale=True) >= 4  # rho, e, v, gamma stay fresh
+    rt.close()
+
+
+@pytest.mark.gpu
+def test_exact_reductions_2048_vs_reference(reference):
+    """Exact mode: the fieldsum folded in the reference's row-major order, bit for bit,
+    while the non-reducing loops still run as row sweeps."""
+    rt = B.Runtime("resident", exact_reductions=True)
+    rt.run_app("miniflow2d", N, N, 0, ITERS)
+    rt.finish()
+    assert _check(rt, reference, exact=True) == 10
+    assert rt.device()["sweep_launches"] > 0
+    rt.close()
+    cap = B.problem_bytes("miniflow2d", N, N) // 3
+    rt = B.Runtime("explicit", capacity=cap, prefetch=True, exact_reductions=True)
+    rt.run_app("miniflow2d", N, N, 0, ITERS, cyclic=True)
+    rt.finish()
+    assert _check(rt, reference, allow_stale=True, exact=True) >= 4
+    rt.close()
+
+
+@pytest.mark.gpu
+def test_exact_reductions_refuse_slabs():
+    rt = B.Runtime("resident", dist=(0, 2), own=(0, 64), ghost=4, exact_reductions=True)
+    with pytest.raises(B.ValidationError, match="exact"):
+        rt.run_app("miniflow2d", 128, 128, 0, 2)
+        rt.finish()
     rt.close()
