@@ -99,6 +99,7 @@ struct SweepParams {
   long long B0, B1;          // 3-D: launch box along dim 1 (2-D: [0,1))
   long long ntc;             // CTA tiles along the columns (blockIdx.x = tile_b * ntc + tile_c)
   long long seg_rows;        // rows owned per CTA row-segment
+  long long edge_first;      // 1: the column-edge strips' CTAs dispatch first (see the prologue)
   long long rng[SW_MAXL][6];  // per loop: rows [0,1), columns [2,3), dim 1 [4,5), absolute
   const double* src[SW_MAXD];
   double* dst[SW_MAXD];
@@ -115,6 +116,7 @@ struct SweepParams {
   long long B0, B1;
   long long ntc;
   long long seg_rows;
+  long long edge_first;
   long long rng[SW_MAXL][6];
   const double* src[SW_MAXD];
   double* dst[SW_MAXD];
@@ -196,6 +198,7 @@ struct SwPlan {
   long long pad = 32;              // doubles before/after the rings (edge neighbour reads)
   bool tma = false;  // loads: bulk async copies (one thread, mbarrier ring) instead of per-thread cp.async
   bool bulk_st = false;  // 2-D TMA: interior rows stored by the producer with bulk copies (smem -> global)
+  bool trace = false;    // debug (OOC_SWEEP_TRACE=file): per-CTA SM id + start / end times
   long long U = 8;   // ring period: every ring length divides it (0: none small enough, no unrolling)
   int NB = 8;        // load barriers (a multiple of U's steps: constant indices in unrolled steps)
   int RCp = 128;     // ring row pitch in doubles (RC, or RC + 2 with TMA: even-column row copies)
@@ -258,6 +261,8 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   // chain's last run, which stores nine datasets (6.1 vs 5.1 ms): off by default
   static const bool bulk_env = std::getenv("OOC_SWEEP_BULKST") && std::atoi(std::getenv("OOC_SWEEP_BULKST")) == 1;
   pl.bulk_st = tma && pl.nd == 2 && bulk_env;
+  static const bool trace_env = std::getenv("OOC_SWEEP_TRACE") != nullptr;
+  pl.trace = trace_env;
   pl.RCp = tma ? pl.RC + 2 : pl.RC;
   if (tma) pl.NT += 32;  // + one producer warp issuing the bulk-copy loads
   pl.L.resize(static_cast<std::size_t>(n));
@@ -609,9 +614,26 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // thread -> ring column lc (and, 3-D, tile row lb); CTA tile origin (c0, b0)
   o << "  const int lc = threadIdx.x % " << pl.RC << ", lb = threadIdx.x / " << pl.RC << ";\n";
   o << "  double* const B = sw_sm + " << pl.pad << " + lb * " << pl.RCp << " + lc;\n";
-  o << "  const long long c0 = p.C0 + (static_cast<long long>(blockIdx.x) % p.ntc) * " << pl.TC << ";\n";
+  // CTA -> (strip, row segment). The column-edge strips run the masked step body (their
+  // halo columns leave some loop's range), ~3x longer than an interior strip's CTA: with
+  // p.edge_first their CTAs take the first linear block indices — the block scheduler
+  // dispatches in that order — so they start in the first wave instead of forming the
+  // kernel's tail (measured: 58 edge CTAs of 905 us ending 550 us after the rest).
+  o << "  long long sw_tx, sw_ty;\n  {\n"
+       "    const long long lin = static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x;\n"
+       "    const long long nx = gridDim.x, ny = gridDim.y, ne = p.edge_first ? 2 * (nx / p.ntc) : 0;\n"
+       "    if (lin < ne * ny) {\n"
+       "      const long long k = lin % ne;\n"
+       "      sw_ty = lin / ne;\n"
+       "      sw_tx = (k >> 1) * p.ntc + ((k & 1) ? p.ntc - 1 : 0);\n"
+       "    } else {\n"
+       "      const long long l = lin - ne * ny, ni = nx - ne, i = l % ni;\n"
+       "      sw_ty = l / ni;\n"
+       "      sw_tx = p.edge_first ? (i / (p.ntc - 2)) * p.ntc + 1 + i % (p.ntc - 2) : i;\n"
+       "    }\n  }\n";
+  o << "  const long long c0 = p.C0 + (sw_tx % p.ntc) * " << pl.TC << ";\n";
   if (d3) {
-    o << "  const long long b0 = p.B0 + (static_cast<long long>(blockIdx.x) / p.ntc) * " << pl.TB << ";\n";
+    o << "  const long long b0 = p.B0 + (sw_tx / p.ntc) * " << pl.TB << ";\n";
     o << "  const long long b = b0 - " << pl.HB << " + lb;\n";
   }
   // one restrict-qualified base per ring: rings never overlap, so the compiler may move
@@ -627,7 +649,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       o << " + static_cast<int>((c0 - " << pl.HC << " - p.box[" << d << "][2]) & 1)";
     o << ";\n";
   }
-  o << "  const long long r_own0 = p.R0 + static_cast<long long>(blockIdx.y) * p.seg_rows;\n";
+  o << "  const long long r_own0 = p.R0 + sw_ty * p.seg_rows;\n";
   o << "  const long long r_own1 = min(p.R1, r_own0 + p.seg_rows);\n";
   o << "  const long long rbase = r_own0 - " << pl.warm << ";\n";
   o << "  const long long c = c0 - " << pl.HC << " + lc;\n";
@@ -728,6 +750,12 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   }
   o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
+  if (pl.trace && pl.red_op == OOC_RED_NONE)  // CTA schedule: SM id, start (ns), end (ns)
+    o << "  if (threadIdx.x == 0) {\n    unsigned long long t_; unsigned sm_;\n"
+         "    asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(t_));\n"
+         "    asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(sm_));\n"
+         "    unsigned long long* tr_ = reinterpret_cast<unsigned long long*>(p.part) + 3 * (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x);\n"
+         "    tr_[0] = sm_; tr_[1] = t_;\n  }\n";
   // element (dataset d, row u + q) of this thread's column; u, q relative to rbase
   // In an unrolled step (unroll_u >= 0: u = unroll_u modulo the ring period) the slot is a
   // constant; otherwise (u + q) mod W at run time (a mask for power-of-two lengths).
@@ -1346,6 +1374,10 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     if (pl.bulk_st && any_store) o << "  __syncthreads();  // the producer copies out the last step's rows\n";
   }
   if (!pl.tma) o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
+  if (pl.trace && pl.red_op == OOC_RED_NONE)
+    o << "  if (threadIdx.x == 0) {\n    unsigned long long t_;\n"
+         "    asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(t_));\n"
+         "    reinterpret_cast<unsigned long long*>(p.part)[3 * (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x) + 2] = t_;\n  }\n";
   if (pl.red_op != OOC_RED_NONE) {  // warp tree, then the CTA's warps in order: one partial per CTA
     o << "#pragma unroll\n  for (int w = 16; w > 0; w >>= 1) racc = ooc_red(" << pl.red_op
       << ", racc, __shfl_down_sync(0xffffffffu, racc, w));\n";
@@ -1886,12 +1918,27 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   }
   sp.seg_rows = (rows + nseg - 1) / nseg;
   nseg = (rows + sp.seg_rows - 1) / sp.seg_rows;
+  static const bool edge_env = !(std::getenv("OOC_SWEEP_EDGEFIRST") && std::atoi(std::getenv("OOC_SWEEP_EDGEFIRST")) == 0);
+  sp.edge_first = edge_env && ntc >= 3 ? 1 : 0;
   if (red_run) {
     if (strips * nseg > c->red_part_cap) {
       set_error("ooc_launch_sweep: too many CTAs for the reduction partials");
       return OOC_ERR_UNSUPPORTED;
     }
     sp.part = c->red_part[q];
+  }
+  static const char* trace_file = std::getenv("OOC_SWEEP_TRACE");
+  static unsigned long long* trace_buf = nullptr;
+  static long long trace_cap = 0;
+  const bool tracing = trace_file && pl.trace && !red_run;
+  if (tracing) {
+    const long long need = 3 * strips * nseg;
+    if (need > trace_cap) {
+      cudaFree(trace_buf);
+      OOC_CUDA_TRY(cudaMalloc(&trace_buf, need * sizeof(unsigned long long)));
+      trace_cap = need;
+    }
+    sp.part = reinterpret_cast<double*>(trace_buf);
   }
   c->stats.sweep_launches++;
   // 3-D: one tiled tensor map per loaded dataset view (box = the RB x RCp plane tile)
@@ -1931,6 +1978,21 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   if (timing) {
     cudaEventRecord(tev->second, c->q[q]);
     T.issued[static_cast<std::size_t>(pick)] = 1;
+  }
+  if (tracing && rc == OOC_OK) {  // debug: append "launch cta sm start end" lines
+    static int tl = 0;
+    const long long nc = strips * nseg;
+    std::vector<unsigned long long> h(static_cast<std::size_t>(3 * nc));
+    OOC_CUDA_TRY(cudaStreamSynchronize(c->q[q]));
+    OOC_CUDA_TRY(cudaMemcpy(h.data(), trace_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (FILE* fp = std::fopen(trace_file, "a")) {
+      std::fprintf(fp, "# launch %d loops %d grid %lld x %lld seg_rows %lld P %d\n", tl, n, strips, nseg,
+                   sp.seg_rows, pl.P);
+      for (long long i = 0; i < nc; ++i)
+        std::fprintf(fp, "%d %lld %llu %llu %llu\n", tl, i, h[3 * i], h[3 * i + 1], h[3 * i + 2]);
+      std::fclose(fp);
+    }
+    ++tl;
   }
   // host cost of the launch itself (key, lookup, parameters, launch): NVRTC builds excluded
   c->stats.sweep_host_us +=
