@@ -1311,6 +1311,95 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         << ";\n" << ind << "  }\n" << ind << "}\n";
     }
   };
+  // Masked fast steps (column-edge strips, OOC_SWEEP_MASKED=0 disables): the general
+  // body's semantics — every value through the rings, each loop under its column mask —
+  // inside the fast row range, where every row predicate holds (s_lo / s_hi), with the K
+  // rows unrolled at generation so an unrolled step's ring slots fold to constants.
+  auto masked_body = [&](const std::string& uexpr) {
+    const char* ind = "      ";
+    o << ind << "const int u = " << uexpr << ";\n";
+    int ci = ci0;
+    for (int i = 0; i < pl.n; ++i) {
+      const ooc_loop& L = Ls[i];
+      const SwLoop& S = pl.L[static_cast<std::size_t>(i)];
+      if (S.barrier) o << ind << cbar << "\n";
+      const std::string is = std::to_string(i);
+      o << ind << "if (colmask & (1ull << " << i << ")) {  // loop " << i << " (lag " << S.lag << ", halo " << S.h << ")\n";
+      int dsof_arg[OOC_MAX_ARGS];
+      for (int a = 0; a < L.nargs; ++a) {
+        dsof_arg[a] = -1;
+        for (int d = 0; d < nd; ++d)
+          if (pl.D[static_cast<std::size_t>(d)].v->data == L.args[a].data) dsof_arg[a] = d;
+      }
+      std::vector<std::vector<std::string>> outs(static_cast<std::size_t>(K));
+      const int ci_loop = ci;
+      for (int r = 0; r < K; ++r) {
+        ci = ci_loop;
+        const long long q0 = r - S.lag;
+        int tmp = 0;
+        const ooc_ins* t = L.tape;
+        const std::string pre = "m" + is + "_" + std::to_string(r) + "_";
+        for (int w = 0; w < L.nwrites + (L.reduce_op != OOC_RED_NONE ? 1 : 0); ++w) {
+          std::vector<std::string> st;
+          for (int k = 0; k < (w < L.nwrites ? L.write_len[w] : L.reduce_len); ++k, ++t) {
+            const ooc_ins& in = *t;
+            if (in.op == OOC_OP_CONST) {
+              st.push_back("p.cst[" + std::to_string(ci++) + "]");
+            } else if (in.op == OOC_OP_READ) {
+              const std::string name = pre + std::to_string(tmp++);
+              o << ind << "  const double " << name << " = " << at(dsof_arg[in.arg], "u", q0 + in.offset[0], xoff(in)) << ";\n";
+              st.push_back(name);
+            } else {
+              const std::string y = st.back();
+              st.pop_back();
+              const std::string x = st.back();
+              st.pop_back();
+              const std::string name = pre + std::to_string(tmp++);
+              o << ind << "  const double " << name << " = ";
+              switch (in.op) {
+                case OOC_OP_ADD: o << x << " + " << y; break;
+                case OOC_OP_SUB: o << x << " - " << y; break;
+                case OOC_OP_MUL: o << x << " * " << y; break;
+                case OOC_OP_DIV: o << x << " / " << y; break;
+                case OOC_OP_MIN: o << "ooc_min(" << x << ", " << y << ")"; break;
+                default: o << "ooc_max(" << x << ", " << y << ")"; break;
+              }
+              o << ";\n";
+              st.push_back(name);
+            }
+          }
+          outs[static_cast<std::size_t>(r)].push_back(st.back());
+        }
+      }
+      for (int r = 0; r < K; ++r) {  // writes after every row's tapes (as in the general body)
+        for (int w = 0; w < L.nwrites; ++w)
+          o << ind << "  " << at(S.wds[static_cast<std::size_t>(w)], "u", r - S.lag, 0) << " = "
+            << outs[static_cast<std::size_t>(r)][static_cast<std::size_t>(w)] << ";\n";
+        if (L.reduce_op != OOC_RED_NONE)
+          o << ind << "  if (own_col) racc = ooc_red(" << L.reduce_op << ", racc, "
+            << outs[static_cast<std::size_t>(r)][static_cast<std::size_t>(L.nwrites)] << ");\n";
+      }
+      o << ind << "}\n";
+    }
+    for (int d = 0; d < nd; ++d) {  // final rows: owned, inside the box (fast row range)
+      const SwDs& D = pl.D[static_cast<std::size_t>(d)];
+      if (!D.store) continue;
+      const std::string ds = std::to_string(d);
+      o << ind << "if ((stmask & (1u << " << ds << "))";
+      if (!D.oop) {
+        o << " && (false";
+        for (int j : D.writers)
+          o << " || (c >= p.rng[" << j << "][2] && c < p.rng[" << j << "][3]"
+            << (d3 ? " && b >= p.rng[" + std::to_string(j) + "][4] && b < p.rng[" + std::to_string(j) + "][5]" : "") << ")";
+        o << ")";
+      }
+      o << ") {\n";
+      for (int r = 0; r < K; ++r)
+        o << ind << "  gs" << ds << "[" << r << " * p.s0[" << ds << "]] = " << at(d, "u", r - D.lagS, 0) << ";\n";
+      o << ind << "}\n";
+    }
+    o << ind << "prev_fast = false;\n";
+  };
   auto step_top = [&](const std::string& ind, long long j = -1) {
     if (pl.tma && j >= 0) {  // unrolled step j of a period block (U == NB): constant barrier
       o << ind << "sw_wait(sw_saddr(sw_bar) + " << (j % pl.NB) * 8 << "u, static_cast<unsigned>(sbl & 1));\n";
@@ -1359,6 +1448,24 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       o << "      }\n";
     }
     o << "      s += " << U << ";\n      continue;\n    }\n";
+    static const bool masked_env = !(std::getenv("OOC_SWEEP_MASKED") && std::atoi(std::getenv("OOC_SWEEP_MASKED")) == 0);
+    if (masked_env && !pl.bulk_st) {
+      o << "    if (!strip_in && s % " << U << " == 0 && s >= s_lo && s + " << U << " <= s_hi) {\n";
+      o << "      const int sbl = s / " << U << ";\n";
+      for (long long j = 0; j < U; ++j) {
+        o << "      {  // unrolled masked step " << j << "\n";
+        o << "        const int s = sbl * " << U << " + " << j << ";\n";
+        step_top("        ", j);
+        o << "        {\n";
+        unroll_u = j * K;
+        masked_body("(sbl * " + std::to_string(U) + " + " + std::to_string(j) + ") * " + std::to_string(K));
+        unroll_u = -1;
+        o << "        }\n";
+        advance("        ");
+        o << "      }\n";
+      }
+      o << "      s += " << U << ";\n      continue;\n    }\n";
+    }
   }
   step_top("    ");
   o << "    if (strip_in && s >= s_lo && s < s_hi) {\n";

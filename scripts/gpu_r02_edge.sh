@@ -8,4 +8,4 @@ timeout 900 python -m pytest tests/test_gpu_sweep.py tests/test_gpu_parity_large
 echo "rc=$?" >> gpurun_out/edge_pytest.log
 timeout 900 python bench.py --steps 5 --warmup 3 --no-parity > gpurun_out/edge_bench.json 2> gpurun_out/edge_bench.err
 echo "rc=$?" >> gpurun_out/edge_bench.err
-OOC_SWEEP_WARPFAST=0 timeout 900 python bench.py --steps 5 --warmup 3 --no-parity > gpurun_out/edge0_bench.json 2> gpurun_out/edge0_bench.err
+OOC_SWEEP_MASKED=0 timeout 900 python bench.py --steps 5 --warmup 3 --no-parity > gpurun_out/edge0_bench.json 2> gpurun_out/edge0_bench.err
