@@ -1449,7 +1449,9 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     }
     o << "      s += " << U << ";\n      continue;\n    }\n";
     static const bool masked_env = !(std::getenv("OOC_SWEEP_MASKED") && std::atoi(std::getenv("OOC_SWEEP_MASKED")) == 0);
-    if (masked_env && !pl.bulk_st) {
+    // 2-D only: on the 3-D plane tiles the extra unrolled body cost the interior CTAs
+    // more than it saved on the edge tiles (miniflow3d 600^3: 4.61 vs 4.31 ms per timestep)
+    if (masked_env && !pl.bulk_st && pl.nd == 2) {
       o << "    if (!strip_in && s % " << U << " == 0 && s >= s_lo && s + " << U << " <= s_hi) {\n";
       o << "      const int sbl = s / " << U << ";\n";
       for (long long j = 0; j < U; ++j) {
@@ -2006,23 +2008,29 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   const long long depth_rows = (red_run ? 2 : pl.P) * pl.K;
   const long long min_seg = std::max<long long>(64, 8 * (pl.warm + pl.lagS_max + pl.K));
   const long long max_nseg = std::max<long long>(1, rows / min_seg);
+  // Time model in swept rows per CTA slot: the work spread over the slots plus a tail of
+  // about half a CTA (CTAs finish desynchronised: the edge strips' longer CTAs and the
+  // shared DRAM stagger them — measured with OOC_SWEEP_TRACE), each CTA also sweeping its
+  // warm-up / lag / prefetch rows without storing them.
   long long nseg = 1;
-  double best = -1.0;
+  double best = 1e300;
+  const double overhead = static_cast<double>(pl.warm + pl.lagS_max + depth_rows) + 8.0;  // + pipeline fill
+  static const long long force_nseg = [] {
+    const char* e = std::getenv("OOC_SWEEP_NSEG");
+    return e ? std::atoll(e) : 0LL;
+  }();
   for (long long ns = 1; ns <= std::min<long long>(max_nseg, 4096); ++ns) {
     const long long seg = (rows + ns - 1) / ns, real = (rows + seg - 1) / seg, ctas = strips * real;
     if (red_run && ctas > c->red_part_cap) break;  // one partial per CTA
-    const long long waves = (ctas + cap - 1) / cap;
-    // wave efficiency, with a mild preference for >= 4 waves (dynamic balance)
-    const double overhead = static_cast<double>(pl.warm + pl.lagS_max + depth_rows);  // rows swept, not stored
-    const double eff = static_cast<double>(ctas) / static_cast<double>(waves * cap) * static_cast<double>(seg) /
-                           (static_cast<double>(seg) + overhead) -
-                       (waves < 4 ? 0.05 * (4 - waves) : 0.0);
-    if (eff > best + 1e-9) {
-      best = eff;
+    const double per = static_cast<double>(seg) + overhead;
+    const double t = static_cast<double>(ctas) * per / static_cast<double>(cap) + 0.5 * per +
+                     (ctas < cap ? static_cast<double>(cap - ctas) * per / static_cast<double>(cap) : 0.0);
+    if (t < best - 1e-9) {
+      best = t;
       nseg = real;
     }
-    if (waves > 16) break;
   }
+  if (force_nseg > 0 && !red_run) nseg = std::min<long long>(force_nseg, std::max<long long>(1, rows));
   sp.seg_rows = (rows + nseg - 1) / nseg;
   nseg = (rows + sp.seg_rows - 1) / sp.seg_rows;
   static const bool edge_env = !(std::getenv("OOC_SWEEP_EDGEFIRST") && std::atoi(std::getenv("OOC_SWEEP_EDGEFIRST")) == 0);

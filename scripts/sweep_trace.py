@@ -18,9 +18,11 @@ if os.path.exists(path):
 import paper_1709_02125_b200 as B  # noqa: E402
 
 rt = B.Runtime("resident")
-rt.declare_app("miniflow2d", n, n)
+app = sys.argv[2] if len(sys.argv) > 2 else "miniflow2d"
+nz = n if app.endswith("3d") else 0
+rt.declare_app(app, n, n, nz)
 for c in range(3):
-    rt.app_iterations("miniflow2d", n, n, 0, 10 * c, 10 * (c + 1))
+    rt.app_iterations(app, n, n, nz, 10 * c, 10 * (c + 1))
     rt.sync()
 rt.close()
 
@@ -33,7 +35,7 @@ for line in open(path):
         continue
     l, i, sm, t0, t1 = map(int, line.split())
     launches[l].append((i, sm, t0, t1))
-last = sorted(launches)[-12:]
+last = sorted(launches)[-6:]
 for l in last:
     rows = launches[l]
     k0 = min(r[2] for r in rows)
