@@ -100,6 +100,7 @@ struct SweepParams {
   long long ntc;             // CTA tiles along the columns (blockIdx.x = tile_b * ntc + tile_c)
   long long seg_rows;        // rows owned per CTA row-segment
   long long edge_first;      // 1: the column-edge strips' CTAs dispatch first (see the prologue)
+  unsigned long long* trace; // debug (OOC_SWEEP_TRACE): per CTA SM id, start, end
   long long rng[SW_MAXL][6];  // per loop: rows [0,1), columns [2,3), dim 1 [4,5), absolute
   const double* src[SW_MAXD];
   double* dst[SW_MAXD];
@@ -117,6 +118,7 @@ struct SweepParams {
   long long ntc;
   long long seg_rows;
   long long edge_first;
+  unsigned long long* trace;
   long long rng[SW_MAXL][6];
   const double* src[SW_MAXD];
   double* dst[SW_MAXD];
@@ -750,11 +752,11 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   }
   o << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   o << "  asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n";
-  if (pl.trace && pl.red_op == OOC_RED_NONE)  // CTA schedule: SM id, start (ns), end (ns)
+  if (pl.trace)  // CTA schedule: SM id, start (ns), end (ns)
     o << "  if (threadIdx.x == 0) {\n    unsigned long long t_; unsigned sm_;\n"
          "    asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(t_));\n"
          "    asm volatile(\"mov.u32 %0, %%smid;\" : \"=r\"(sm_));\n"
-         "    unsigned long long* tr_ = reinterpret_cast<unsigned long long*>(p.part) + 3 * (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x);\n"
+         "    unsigned long long* tr_ = p.trace + 3 * (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x);\n"
          "    tr_[0] = sm_; tr_[1] = t_;\n  }\n";
   // element (dataset d, row u + q) of this thread's column; u, q relative to rbase
   // In an unrolled step (unroll_u >= 0: u = unroll_u modulo the ring period) the slot is a
@@ -1483,10 +1485,10 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
     if (pl.bulk_st && any_store) o << "  __syncthreads();  // the producer copies out the last step's rows\n";
   }
   if (!pl.tma) o << "  asm volatile(\"cp.async.wait_group 0;\" ::: \"memory\");\n";
-  if (pl.trace && pl.red_op == OOC_RED_NONE)
+  if (pl.trace)
     o << "  if (threadIdx.x == 0) {\n    unsigned long long t_;\n"
          "    asm volatile(\"mov.u64 %0, %%globaltimer;\" : \"=l\"(t_));\n"
-         "    reinterpret_cast<unsigned long long*>(p.part)[3 * (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x) + 2] = t_;\n  }\n";
+         "    p.trace[3 * (static_cast<long long>(blockIdx.y) * gridDim.x + blockIdx.x) + 2] = t_;\n  }\n";
   if (pl.red_op != OOC_RED_NONE) {  // warp tree, then the CTA's warps in order: one partial per CTA
     o << "#pragma unroll\n  for (int w = 16; w > 0; w >>= 1) racc = ooc_red(" << pl.red_op
       << ", racc, __shfl_down_sync(0xffffffffu, racc, w));\n";
@@ -2045,7 +2047,7 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
   static const char* trace_file = std::getenv("OOC_SWEEP_TRACE");
   static unsigned long long* trace_buf = nullptr;
   static long long trace_cap = 0;
-  const bool tracing = trace_file && pl.trace && !red_run;
+  const bool tracing = trace_file && pl.trace;
   if (tracing) {
     const long long need = 3 * strips * nseg;
     if (need > trace_cap) {
@@ -2053,7 +2055,7 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
       OOC_CUDA_TRY(cudaMalloc(&trace_buf, need * sizeof(unsigned long long)));
       trace_cap = need;
     }
-    sp.part = reinterpret_cast<double*>(trace_buf);
+    sp.trace = trace_buf;
   }
   c->stats.sweep_launches++;
   // 3-D: one tiled tensor map per loaded dataset view (box = the RB x RCp plane tile)

@@ -69,4 +69,13 @@ for l in last:
     # slot occupancy: CTA-slots busy (2 per SM) over the span
     slot_busy = sum(t1 - t0 for _, _, t0, t1 in rows) / (2 * nsm * span)
     starts = sorted(t0 - k0 for _, _, t0, _ in rows)
-    print(f"  CTA-slot occupancy {slot_busy:.3f}; first start spread {starts[0]/1e3:.1f}..{starts[2*nsm-1]/1e3:.1f} us")
+    print(f"  CTA-slot occupancy {slot_busy:.3f}; first start spread {starts[0]/1e3:.1f}..{starts[min(len(starts), 2*nsm)-1]/1e3:.1f} us")
+    conc = defaultdict(int)
+    for _, sm, _, _ in rows:
+        pass
+    # concurrent CTAs per SM (max over time, sampled at CTA starts)
+    mx = 0
+    for sm, iv in per_sm.items():
+        for a, _ in iv:
+            mx = max(mx, sum(1 for x, y in iv if x <= a < y))
+    print(f"  max concurrent CTAs per SM {mx}")
