@@ -158,6 +158,20 @@ def test_sweep_variants(K, P_, smem, rc):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
+@pytest.mark.parametrize("env", [
+    {"OOC_SWEEP_EDGEFIRST": "0", "OOC_SWEEP_MASKED": "0"},
+    {"OOC_SWEEP_RC": "64", "OOC_SWEEP_SMEM": "60000", "OOC_SWEEP_NSEG": "3"},
+    {"OOC_SWEEP_RC": "64", "OOC_SWEEP_SMEM": "60000", "OOC_SWEEP_MASKED": "0"},
+])
+def test_sweep_schedule_variants(env):
+    """CTA scheduling — column-edge strips dispatched first, masked fast steps on edge
+    strips, forced segment counts — with narrow rings (many strips, so most CTAs are
+    edge-first reordered and several take masked steps) never changes the bits."""
+    r = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "sweep_parity_child.py")],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
 def test_sweep_build_failure_falls_back():
     """A row-sweep kernel that cannot be built (forced by OOC_SWEEP_FAIL_BUILD) falls back
     to the fused loop-group launches: bits unchanged, each loop's bytes billed once."""
