@@ -79,7 +79,7 @@ int ring_rows3() {
   static int rb = [] {
     const char* e = std::getenv("OOC_SWEEP_RB");
     const int v = e ? std::atoi(e) : 16;
-    return v == 8 || v == 16 || v == 32 ? v : 16;
+    return v >= 4 && v <= 32 ? v : 16;
   }();
   return rb;
 }
@@ -204,6 +204,7 @@ struct SwPlan {
   long long U = 8;   // ring period: every ring length divides it (0: none small enough, no unrolling)
   int NB = 8;        // load barriers (a multiple of U's steps: constant indices in unrolled steps)
   int RCp = 128;     // ring row pitch in doubles (RC, or RC + 2 with TMA: even-column row copies)
+  long long SP = 128;  // ring slot pitch in doubles: RB x RCp, 3-D rounded up to 128 bytes (tensor-copy destinations)
   long long HC = 0, TC = 0, warm = 0, lagS_max = 0, smem = 0;
   int red_op = OOC_RED_NONE;  // the run's last loop reduces (no writes): folded per CTA
   long long red_lag = 0;
@@ -364,7 +365,8 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
   // shared memory around the rings: the farthest neighbour read of an edge lane
   // (a multiple of 16 doubles: 3-D tensor copies land on 128-byte aligned plane slots)
   pl.pad = (std::max<long long>(32, pl.HB * pl.RCp + pl.HC + 4) + 15) / 16 * 16;
-  if (pl.nd == 3 && (static_cast<long long>(pl.RB) * pl.RCp) % 16 != 0) return fail(why, "plane tile not 128-byte aligned");
+  pl.SP = static_cast<long long>(pl.RB) * pl.RCp;
+  if (pl.nd == 3) pl.SP = (pl.SP + 15) / 16 * 16;  // every plane slot starts 128-byte aligned
   // ---- loaded / written / out-of-place
   for (int d = 0; d < nd; ++d) {
     SwDs& D = pl.D[static_cast<std::size_t>(d)];
@@ -490,7 +492,7 @@ bool analyze(const ooc_loop* Ls, int n, int K, int P, SwPlan& pl, std::string* w
         while (D.W < D.need) D.W *= 2;
       }
       D.off = off;
-      off += D.W * pl.RCp * pl.RB;
+      off += D.W * pl.SP;
     }
   }
   pl.smem = (off + 2 * pl.pad) * 8;
@@ -762,7 +764,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // In an unrolled step (unroll_u >= 0: u = unroll_u modulo the ring period) the slot is a
   // constant; otherwise (u + q) mod W at run time (a mask for power-of-two lengths).
   long long unroll_u = -1;
-  const long long PL = static_cast<long long>(pl.RB) * pl.RCp;  // ring "row": a plane tile in 3-D
+  const long long PL = pl.SP;  // ring slot pitch ("row": a plane tile in 3-D)
   // a read's cross-thread offset in ring elements: dim-1 offset x pitch + column offset
   // (0: the thread's own element, so it can be forwarded / carried in registers)
   auto xoff = [&](const ooc_ins& in) -> long long {
@@ -909,7 +911,7 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         o << "        dd_" << js << " = dd;\n";
         o << "        tx_" << js << " = static_cast<int>(cs - (cs & 1));  // even (16-byte aligned) column at or below the tile\n";
         o << "        ty_" << js << " = static_cast<int>(b0 - " << pl.HB << " - p.box[dd][4]);\n";
-        o << "        tn_" << js << " = " << PL * 8 << "u;  // the whole box, zero-filled out of bounds\n";
+        o << "        tn_" << js << " = " << static_cast<long long>(pl.RB) * pl.RCp * 8 << "u;  // the whole box, zero-filled out of bounds\n";
         o << "        vr0_" << js << " = rbase - p.box[dd][0] - lagL_" << js << ";\n";
         o << "        nrows_" << js << " = p.box[dd][1] - p.box[dd][0];\n";
         o << "        dst_" << js << " = sw_saddr(sw_sm) + static_cast<unsigned>(roff * 8);\n";
