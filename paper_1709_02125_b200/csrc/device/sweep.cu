@@ -878,8 +878,12 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
         o << ind << "    {\n" << ind << "      const long long v = vr0_" << js << " + static_cast<long long>(pf) * " << K << " + " << r
           << ";\n";
         o << ind << "      if (tn_" << js << " && v >= 0 && v < nrows_" << js << ")\n";
-        o << ind << "        asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(src_" << js << " + v * s0_" << js
-          << "), \"r\"(tn_" << js << ") : \"memory\");\n";
+        if (d3)  // the plane tile of a later step into L2 (tensor prefetch, same box as the ring load)
+          o << ind << "        asm volatile(\"cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\" :: \"l\"(&m.t[dd_"
+            << js << "][0]), \"r\"(tx_" << js << "), \"r\"(ty_" << js << "), \"r\"(static_cast<int>(v)) : \"memory\");\n";
+        else
+          o << ind << "        asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], %1;\" :: \"l\"(src_" << js << " + v * s0_" << js
+            << "), \"r\"(tn_" << js << ") : \"memory\");\n";
         o << ind << "    }\n";
       }
     o << ind << "  }\n" << ind << "}\n";
