@@ -1480,6 +1480,14 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   step_top("    ");
   o << "    if (strip_in && s >= s_lo && s < s_hi) {\n";
   fast_body(nullptr, "s * " + std::to_string(K));
+  // 3-D edge tiles: the masked steps without the unrolling (one compact copy of the loops,
+  // dynamic ring slots, no row predicates) — the unrolled copy doubles the 3-D kernel's
+  // code and slowed every CTA (OOC_SWEEP_MASKED=0 disables)
+  static const bool masked1 = !(std::getenv("OOC_SWEEP_MASKED") && std::atoi(std::getenv("OOC_SWEEP_MASKED")) == 0);
+  if (masked1 && pl.nd == 3 && !pl.bulk_st) {
+    o << "    } else if (s >= s_lo && s < s_hi) {\n";
+    masked_body("s * " + std::to_string(K));
+  }
   o << "    } else {\n";
   body(false);
   o << "      prev_fast = false;\n    }\n";
