@@ -223,8 +223,10 @@ bool sweep_3d_enabled() {
 }
 long long smem_budget3() {  // 3-D rings of plane tiles: one CTA per SM
   static long long b = [] {
+    // measured: 225 000 B lets rk3chain3d's 8-loop stage run fit one sweep (33.2 vs 36.2 ms
+    // per ten 9-loop runs at 512^3), miniflow3d unchanged (profiles/r02_summary.md)
     const char* e = std::getenv("OOC_SWEEP_SMEM3");
-    return e ? std::atoll(e) : 200LL * 1024;
+    return e ? std::atoll(e) : 225000LL;
   }();
   return b;
 }
