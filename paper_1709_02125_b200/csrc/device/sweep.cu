@@ -2060,13 +2060,17 @@ extern "C" int ooc_launch_sweep(ooc_ctx* c, int q, const ooc_loop* loops, int n,
     }
     sp.part = c->red_part[q];
   }
+  // debug trace (OOC_SWEEP_TRACE): one buffer for the process, reallocated when a launch
+  // needs more or runs on another device; each traced launch synchronises before returning
   static const char* trace_file = std::getenv("OOC_SWEEP_TRACE");
   static unsigned long long* trace_buf = nullptr;
   static long long trace_cap = 0;
+  static int trace_dev = -1;
   const bool tracing = trace_file && pl.trace;
   if (tracing) {
     const long long need = 3 * strips * nseg;
-    if (need > trace_cap) {
+    if (need > trace_cap || trace_dev != c->device) {
+      trace_dev = c->device;
       cudaFree(trace_buf);
       OOC_CUDA_TRY(cudaMalloc(&trace_buf, need * sizeof(unsigned long long)));
       trace_cap = need;
