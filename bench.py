@@ -499,10 +499,10 @@ def main():
     OUT = os.fdopen(os.dup(1), "w")
     sys.stdout.flush()
     os.dup2(2, 1)
-    rank, world, local, dist = dist_init()
-
     if args.impl == "reference":
-        if rank != 0:
+        # the reference arm is host code: rank 0 alone runs it (no process group, no GPU);
+        # the other ranks of a torchrun launch exit 0 without work
+        if int(os.environ.get("RANK", "0")) != 0:
             return
         ref = cpu_reference(args.steps, warmup=0)
         line = {"metric": METRIC, "value": ref["value"], "unit": UNIT, "n_gpus": args.gpus,
@@ -518,6 +518,7 @@ def main():
         print(json.dumps(line), file=OUT, flush=True)
         return
 
+    rank, world, local, dist = dist_init()
     import paper_1709_02125_b200 as B
     gpu = local if dist is not None else 0
     n = args.n
