@@ -1458,7 +1458,10 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
       o << "      }\n";
     }
     o << "      s += " << U << ";\n      continue;\n    }\n";
-    static const bool masked_env = !(std::getenv("OOC_SWEEP_MASKED") && std::atoi(std::getenv("OOC_SWEEP_MASKED")) == 0);
+    // OOC_SWEEP_MASKED: 0 general body on edge strips, 1 (default) unrolled masked steps
+    // in 2-D and compact ones in 3-D, 2 compact masked steps in both
+    static const int masked_mode = std::getenv("OOC_SWEEP_MASKED") ? std::atoi(std::getenv("OOC_SWEEP_MASKED")) : 1;
+    const bool masked_env = masked_mode == 1;
     // 2-D only: on the 3-D plane tiles the extra unrolled body cost the interior CTAs
     // more than it saved on the edge tiles (miniflow3d 600^3: 4.61 vs 4.31 ms per timestep)
     if (masked_env && !pl.bulk_st && pl.nd == 2) {
@@ -1485,8 +1488,8 @@ std::string generate(const ooc_loop* Ls, const SwPlan& pl, std::vector<double>* 
   // 3-D edge tiles: the masked steps without the unrolling (one compact copy of the loops,
   // dynamic ring slots, no row predicates) — the unrolled copy doubles the 3-D kernel's
   // code and slowed every CTA (OOC_SWEEP_MASKED=0 disables)
-  static const bool masked1 = !(std::getenv("OOC_SWEEP_MASKED") && std::atoi(std::getenv("OOC_SWEEP_MASKED")) == 0);
-  if (masked1 && pl.nd == 3 && !pl.bulk_st) {
+  static const int masked_mode1 = std::getenv("OOC_SWEEP_MASKED") ? std::atoi(std::getenv("OOC_SWEEP_MASKED")) : 1;
+  if (((masked_mode1 == 1 && pl.nd == 3) || masked_mode1 == 2) && !pl.bulk_st) {
     o << "    } else if (s >= s_lo && s < s_hi) {\n";
     masked_body("s * " + std::to_string(K));
   }
